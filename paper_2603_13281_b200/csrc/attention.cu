@@ -1,0 +1,305 @@
+// Shared-KV paged decode attention (reference: `layer_attention`, src/model.py:384-425,
+// with the fused 2H query heads of `block_forward` decode, src/model.py:495-501).
+//
+// Work decomposition (built on the host by attn_plan.cpp):
+//   * each sequence's keys are cut into fixed chunks of CHUNK_PAGES pages at ABSOLUTE
+//     positions [c*CHUNK, (c+1)*CHUNK);
+//   * sequences whose chunk c maps to the SAME physical pages (a cross-model shared
+//     prefix) are grouped into one work item, so each shared page is staged into shared
+//     memory once and reused by the encoder and every adapter's decoder queries;
+//   * a work item x one KV head = one CTA; up to 64 query rows (4 warps x 16).
+// Per (row, head, chunk) the kernel emits an unnormalised partial (o, m, l); the merge
+// kernel folds chunks 0..last in fixed order. Partials depend only on the row's own
+// query, the chunk's keys and the row's position, never on which other rows share the
+// CTA -- the batch-invariance the reference gets from its per-head loop (2H == H||H,
+// tests/test_model.py:225-239) and that makes prefill / decode KV bytes identical.
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace icr {
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+__device__ __forceinline__ void mma_bf16_16816(float (&d)[4], const uint32_t (&a)[4],
+                                               uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                        uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                          uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// Row-major [rows][HD] bf16 tile with 16-byte chunks XOR-swizzled by (row & 7):
+// conflict-free ldmatrix for both K (non-trans) and V (trans) reads.
+template <int HD>
+__device__ __forceinline__ uint32_t swz(int row, int chunk) {
+  return (uint32_t)(row * HD * 2 + ((chunk ^ (row & 7)) << 4));
+}
+
+template <int HD>
+__global__ void __launch_bounds__(128)
+    attn_partial_kernel(const __nv_bfloat16* __restrict__ q, int q_ld,
+                        const __nv_bfloat16* __restrict__ k_pages,
+                        const __nv_bfloat16* __restrict__ v_pages, int num_kv_heads, int group,
+                        const AttnItem* __restrict__ items, const int* __restrict__ item_pages,
+                        const int2* __restrict__ item_rows, const int* __restrict__ row_pos,
+                        int num_heads, int max_chunks, float scale, float* __restrict__ part_o,
+                        float2* __restrict__ part_ml, const int* __restrict__ n_items_dev) {
+  constexpr int CH = HD / 8;  // 16-byte chunks per row
+  __shared__ __align__(128) __nv_bfloat16 sQ[64 * HD];
+  __shared__ __align__(128) __nv_bfloat16 sK[2][16 * HD];
+  __shared__ __align__(128) __nv_bfloat16 sV[2][16 * HD];
+
+  const int item_id = blockIdx.x;
+  if (item_id >= *n_items_dev) return;
+  const AttnItem it = items[item_id];
+  const int g = blockIdx.y;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  // ---- stage Q rows (swizzled) ----
+  for (int idx = tid; idx < 64 * CH; idx += 128) {
+    const int row = idx / CH, ch = idx % CH;
+    uint4 val = make_uint4(0, 0, 0, 0);
+    if (row < it.n_rows) {
+      const int2 rr = item_rows[it.row_off + row];
+      const int head = g * group + rr.y;
+      val = *reinterpret_cast<const uint4*>(q + (size_t)rr.x * q_ld + head * HD + ch * 8);
+    }
+    *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sQ) + swz<HD>(row, ch)) = val;
+  }
+
+  auto load_page = [&](int pi, int buf) {
+    const int page = item_pages[it.page_off + pi];
+    const size_t off = ((size_t)page * num_kv_heads + g) * 16 * HD;
+    const uint8_t* ks = reinterpret_cast<const uint8_t*>(k_pages + off);
+    const uint8_t* vs = reinterpret_cast<const uint8_t*>(v_pages + off);
+    const uint32_t kd = smem_u32(sK[buf]), vd = smem_u32(sV[buf]);
+    for (int idx = tid; idx < 16 * CH; idx += 128) {
+      const int row = idx / CH, ch = idx % CH;
+      cp_async16(kd + swz<HD>(row, ch), ks + idx * 16);
+      cp_async16(vd + swz<HD>(row, ch), vs + idx * 16);
+    }
+    cp_async_commit();
+  };
+
+  load_page(0, 0);
+  __syncthreads();
+
+  // ---- per-warp query fragments ----
+  const int r_lo = warp * 16 + (lane >> 2);  // rows r_lo and r_lo + 8 of the item
+  int pos_lo = -1, pos_hi = -1;
+  if (r_lo < it.n_rows) pos_lo = row_pos[item_rows[it.row_off + r_lo].x];
+  if (r_lo + 8 < it.n_rows) pos_hi = row_pos[item_rows[it.row_off + r_lo + 8].x];
+
+  uint32_t qa[HD / 16][4];
+  {
+    const uint32_t qbase = smem_u32(sQ);
+#pragma unroll
+    for (int kk = 0; kk < HD / 16; ++kk) {
+      const int row = warp * 16 + (lane & 15);
+      const int ch = kk * 2 + (lane >> 4);
+      ldsm_x4(qbase + swz<HD>(row, ch), qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3]);
+    }
+  }
+
+  float o[HD / 8][4];
+#pragma unroll
+  for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;
+
+  for (int pi = 0; pi < it.n_pages; ++pi) {
+    const int buf = pi & 1;
+    if (pi + 1 < it.n_pages) {
+      load_page(pi + 1, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+
+    // S = Q K^T for 16 keys (two n8 tiles)
+    float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    const uint32_t kbase = smem_u32(sK[buf]);
+#pragma unroll
+    for (int kk = 0; kk < HD / 16; ++kk) {
+      // x4: matrices (keys0-7, dims lo), (keys0-7, dims hi), (keys8-15, lo), (keys8-15, hi)
+      const int key = (lane & 7) + ((lane >> 4) << 3);
+      const int ch = kk * 2 + ((lane >> 3) & 1);
+      uint32_t b0, b1, b2, b3;
+      ldsm_x4(kbase + swz<HD>(key, ch), b0, b1, b2, b3);
+      mma_bf16_16816(s[0], qa[kk], b0, b1);
+      mma_bf16_16816(s[1], qa[kk], b2, b3);
+    }
+    // scale, mask, online softmax (src/model.py:415-423, src/tensor.py:249-267)
+    const int kpos0 = it.chunk_start + pi * 16;
+    float mx_lo = m_lo, mx_hi = m_hi;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int kp = kpos0 + nt * 8 + (lane & 3) * 2 + e;
+        float a = __fmul_rn(s[nt][e], scale);
+        float b = __fmul_rn(s[nt][2 + e], scale);
+        a = (kp <= pos_lo) ? a : -INFINITY;
+        b = (kp <= pos_hi) ? b : -INFINITY;
+        s[nt][e] = a;
+        s[nt][2 + e] = b;
+        mx_lo = fmaxf(mx_lo, a);
+        mx_hi = fmaxf(mx_hi, b);
+      }
+    }
+    mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, 1));
+    mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, 2));
+    mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 1));
+    mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 2));
+    const float corr_lo = (mx_lo == -INFINITY) ? 1.f : expf(m_lo - mx_lo);
+    const float corr_hi = (mx_hi == -INFINITY) ? 1.f : expf(m_hi - mx_hi);
+    float sum_lo = 0.f, sum_hi = 0.f;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const float a = (s[nt][e] == -INFINITY) ? 0.f : expf(s[nt][e] - mx_lo);
+        const float b = (s[nt][2 + e] == -INFINITY) ? 0.f : expf(s[nt][2 + e] - mx_hi);
+        s[nt][e] = a;
+        s[nt][2 + e] = b;
+        sum_lo += a;
+        sum_hi += b;
+      }
+    }
+    sum_lo += __shfl_xor_sync(0xffffffffu, sum_lo, 1);
+    sum_lo += __shfl_xor_sync(0xffffffffu, sum_lo, 2);
+    sum_hi += __shfl_xor_sync(0xffffffffu, sum_hi, 1);
+    sum_hi += __shfl_xor_sync(0xffffffffu, sum_hi, 2);
+    l_lo = l_lo * corr_lo + sum_lo;
+    l_hi = l_hi * corr_hi + sum_hi;
+    m_lo = mx_lo;
+    m_hi = mx_hi;
+#pragma unroll
+    for (int i = 0; i < HD / 8; ++i) {
+      o[i][0] *= corr_lo; o[i][1] *= corr_lo;
+      o[i][2] *= corr_hi; o[i][3] *= corr_hi;
+    }
+    // O += P V
+    uint32_t pa[4];
+    pa[0] = pack_bf16(s[0][0], s[0][1]);
+    pa[1] = pack_bf16(s[0][2], s[0][3]);
+    pa[2] = pack_bf16(s[1][0], s[1][1]);
+    pa[3] = pack_bf16(s[1][2], s[1][3]);
+    const uint32_t vbase = smem_u32(sV[buf]);
+#pragma unroll
+    for (int dt = 0; dt < HD / 16; ++dt) {
+      // x4.trans: (keys0-7, dims d0..d0+7), (keys8-15, d0..), (keys0-7, d0+8..), (keys8-15, d0+8..)
+      const int key = (lane & 7) + (((lane >> 3) & 1) << 3);
+      const int ch = dt * 2 + (lane >> 4);
+      uint32_t b0, b1, b2, b3;
+      ldsm_x4_t(vbase + swz<HD>(key, ch), b0, b1, b2, b3);
+      mma_bf16_16816(o[dt * 2], pa, b0, b1);
+      mma_bf16_16816(o[dt * 2 + 1], pa, b2, b3);
+    }
+    __syncthreads();
+  }
+
+  // ---- write partials ----
+  const int chunk = it.chunk_idx;
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    const int r = r_lo + half * 8;
+    if (r >= it.n_rows) continue;
+    const int2 rr = item_rows[it.row_off + r];
+    const int head = g * group + rr.y;
+    const size_t slot = ((size_t)rr.x * num_heads + head) * max_chunks + chunk;
+    float* dst = part_o + slot * HD;
+#pragma unroll
+    for (int i = 0; i < HD / 8; ++i) {
+      const int col = i * 8 + (lane & 3) * 2;
+      *reinterpret_cast<float2*>(dst + col) =
+          half == 0 ? make_float2(o[i][0], o[i][1]) : make_float2(o[i][2], o[i][3]);
+    }
+    if ((lane & 3) == 0)
+      part_ml[slot] = half == 0 ? make_float2(m_lo, l_lo) : make_float2(m_hi, l_hi);
+  }
+}
+
+// Fixed-order merge of chunk partials; one CTA per (row, head), one thread per dim.
+template <int HD>
+__global__ void __launch_bounds__(HD)
+    attn_merge_kernel(const float* __restrict__ part_o, const float2* __restrict__ part_ml,
+                      const int* __restrict__ row_pos, const int* __restrict__ row_kind,
+                      int num_heads, int max_chunks, int chunk_tokens, __nv_bfloat16* __restrict__ out,
+                      int out_ld) {
+  const int rh = blockIdx.x;
+  const int r = rh / num_heads, h = rh % num_heads;
+  const int d = threadIdx.x;
+  __nv_bfloat16* dst = out + (size_t)r * out_ld + h * HD + d;
+  if (row_kind[r] < 0) { *dst = __float2bfloat16_rn(0.f); return; }
+  const int nch = row_pos[r] / chunk_tokens + 1;
+  const size_t base = ((size_t)r * num_heads + h) * max_chunks;
+  float M = -INFINITY;
+  for (int c = 0; c < nch; ++c) M = fmaxf(M, part_ml[base + c].x);
+  float L = 0.f, O = 0.f;
+  for (int c = 0; c < nch; ++c) {
+    const float2 ml = part_ml[base + c];
+    const float w = expf(ml.x - M);
+    L = fmaf(ml.y, w, L);
+    O = fmaf(part_o[(base + c) * HD + d], w, O);
+  }
+  *dst = __float2bfloat16_rn(__fdiv_rn(O, L));
+}
+
+cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t s) {
+  if (a.n_items_cap > 0) {
+    dim3 grid(a.n_items_cap, a.num_kv_heads);
+    if (a.head_dim == 128)
+      attn_partial_kernel<128><<<grid, 128, 0, s>>>(
+          a.q, a.q_ld, a.k_pages, a.v_pages, a.num_kv_heads, a.group, a.items, a.item_pages,
+          a.item_rows, a.row_pos, a.num_heads, a.max_chunks, a.scale, a.part_o, a.part_ml,
+          a.n_items_dev);
+    else if (a.head_dim == 64)
+      attn_partial_kernel<64><<<grid, 128, 0, s>>>(
+          a.q, a.q_ld, a.k_pages, a.v_pages, a.num_kv_heads, a.group, a.items, a.item_pages,
+          a.item_rows, a.row_pos, a.num_heads, a.max_chunks, a.scale, a.part_o, a.part_ml,
+          a.n_items_dev);
+    else
+      return cudaErrorInvalidValue;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  if (a.n_rows > 0) {
+    if (a.head_dim == 128)
+      attn_merge_kernel<128><<<a.n_rows * a.num_heads, 128, 0, s>>>(
+          a.part_o, a.part_ml, a.row_pos, a.row_kind, a.num_heads, a.max_chunks, a.chunk_tokens,
+          a.out, a.out_ld);
+    else
+      attn_merge_kernel<64><<<a.n_rows * a.num_heads, 64, 0, s>>>(
+          a.part_o, a.part_ml, a.row_pos, a.row_kind, a.num_heads, a.max_chunks, a.chunk_tokens,
+          a.out, a.out_ld);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace icr
