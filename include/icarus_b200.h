@@ -131,6 +131,16 @@ icr_status icr_decode_loop(icr_model* m, const icr_batch* first, const int32_t* 
                            int steps, int32_t* out_tokens_host_last, float* step_ms_host,
                            void* stream);
 
+/* --- instrumentation ------------------------------------------------------------- */
+
+/* out3 = {kernel launches, metadata bytes uploaded, attention work items} of the last
+ * icr_forward / icr_decode_loop step. */
+icr_status icr_model_stats(icr_model* m, int64_t* out3);
+
+/* Average device time of one projection-GEMM launch (which: 0 wo, 1 gate|up, 2 down,
+ * 3 lm_head) re-run `iters` times over all layers with the last forward's rows. */
+icr_status icr_profile_gemm(icr_model* m, int which, int iters, float* avg_ms, void* stream);
+
 /* --- building blocks, exported for parity tests -------------------------------- */
 
 /* out_f32[n, m] = sum_k W[m, k] X[n, k]; W [M, K] bf16 (dev), X [n_rows, K] bf16 (dev).

@@ -47,6 +47,7 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
       const int n = n0 + j;
       if (n >= p.n_rows || p.row_kind[n] != 1) continue;
       const int a = p.row_adapter[n];
+      if (a < 0) continue;  // base decoder row (read-only replay): no adapter
       const __nv_bfloat16* b = p.lora_b + ((size_t)a * p.lora_m + m) * p.rank;
       const float* u = p.lora_u + ((size_t)n * p.n_u + uidx) * p.rank;
       float acc = 0.f;

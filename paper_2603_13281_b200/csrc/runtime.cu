@@ -189,6 +189,13 @@ static icr_status build_attn_plan(int n_rows, const int* kind, const int* seq, c
   return ICR_OK;
 }
 
+// Device-side view of one forward's metadata (offsets into meta_dev).
+struct Meta {
+  int n_rows, rp, n_lm, n_dec, n_items;
+  size_t o_tokens, o_kind, o_seq, o_pos, o_adapter, o_lm_rows, o_seg_off, o_seg_rows, o_bt,
+      o_items, o_item_pages, o_item_rows, o_n_items, o_feedback, total;
+};
+
 // ------------------------------------------------------------------ model
 struct LayerMaps {
   CUtensorMap qkv, o, gu, down;
@@ -224,6 +231,12 @@ struct icr_model {
   size_t staging_cap = 0;
   cudaEvent_t staging_ev[2];
   cudaEvent_t step_ev[2];
+  // instrumentation of the last forward
+  long long last_launches = 0;
+  long long last_meta_bytes = 0;
+  long long last_items = 0;
+  Meta last_mt{};
+  bool has_last = false;
 };
 
 static icr_status ensure_meta(icr_model* m, size_t ints) {
@@ -237,13 +250,6 @@ static icr_status ensure_meta(icr_model* m, size_t ints) {
   m->meta_cap = cap;
   return ICR_OK;
 }
-
-// Device-side view of one forward's metadata (offsets into meta_dev).
-struct Meta {
-  int n_rows, rp, n_lm, n_dec, n_items;
-  size_t o_tokens, o_kind, o_seq, o_pos, o_adapter, o_lm_rows, o_seg_off, o_seg_rows, o_bt,
-      o_items, o_item_pages, o_item_rows, o_n_items, o_feedback, total;
-};
 
 // Packs host batch metadata into `stage` (capacity checked by caller via sizing pass).
 static icr_status pack_meta(icr_model* m, const icr_batch* b, const int* pos_override,
@@ -337,7 +343,7 @@ static icr_status validate_batch(icr_model* m, const icr_batch* b, const int* po
     const int k = b->row_kind[r];
     if (k != 0 && k != 1) return fail(ICR_MODE, "row %d kind %d must be 0 (encoder) or 1 (decoder)", r, k);
     if (k == 1) {
-      if (c.lora_rank > 0 && (b->row_adapter[r] < 0 || b->row_adapter[r] >= c.adapter_slots))
+      if (b->row_adapter[r] >= 0 && (c.lora_rank == 0 || b->row_adapter[r] >= c.adapter_slots))
         return fail(ICR_CONFIG, "row %d adapter slot %d outside [0, %d)", r, b->row_adapter[r], c.adapter_slots);
     }
     if (pos[r] < 0 || pos[r] >= c.max_positions)
@@ -361,6 +367,7 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
   const int* bt = md + mt.o_bt;
   const bool lora = c.lora_rank > 0 && mt.n_dec > 0;
   const int d = c.hidden_dim, rp = mt.rp;
+  long long launches = 0;
 
   auto gemm = [&](const CUtensorMap& wmap, CUtensorMap* xmaps, GemmParams p, int rows,
                   int row_stride_out) -> icr_status {
@@ -380,6 +387,7 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
       if (p.tile_best) q.tile_best = p.tile_best + g0;
       cudaError_t e = gemm_launch(wmap, xmaps[nt_index(nt)], q, g0, nt, m->num_sms, s);
       if (e != cudaSuccess) return fail(ICR_CUDA, "gemm launch: %s", cudaGetErrorString(e));
+      ++launches;
     }
     return ICR_OK;
   };
@@ -418,12 +426,15 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
   for (int l = 0; l < c.num_layers; ++l) {
     const icr_layer_weights& w = m->layers[l];
     const LayerMaps& lm = m->maps[l];
+    ++launches;
     CUDA_TRY(rmsnorm_launch(m->x, tokens, l == 0 ? m->embed : nullptr, m->x, m->h, kind, nullptr,
                             rp, d, c.rms_eps, s));
-    if (lora)
+    if (lora) {
+      ++launches;
       CUDA_TRY(lora_shrink_launch(m->h, d, d, (const __nv_bfloat16*)w.a_q, nullptr, 1,
                                   c.adapter_slots, c.lora_rank, m->scaling, seg_off, seg_rows,
                                   m->U, s));
+    }
     {
       GemmParams p = base;
       p.mode = EPI_QKV;
@@ -452,12 +463,15 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
     al.v_pages = (const __nv_bfloat16*)w.v_pages;
     {
       cudaError_t e = attn_launch(al, s);
+      launches += 2;
       if (e != cudaSuccess) return fail(ICR_CUDA, "attention launch: %s", cudaGetErrorString(e));
     }
-    if (lora)
+    if (lora) {
+      ++launches;
       CUDA_TRY(lora_shrink_launch(m->att, m->q_dim, m->q_dim, (const __nv_bfloat16*)w.a_o, nullptr,
                                   1, c.adapter_slots, c.lora_rank, m->scaling, seg_off, seg_rows,
                                   m->U, s));
+    }
     {
       GemmParams p = base;
       p.mode = EPI_RESID;
@@ -471,11 +485,14 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
       p.resid = m->x;
       if ((st = gemm(lm.o, m->xmap_att, p, rp, 0))) return st;
     }
+    ++launches;
     CUDA_TRY(rmsnorm_launch(m->x, nullptr, nullptr, m->x, m->h, kind, nullptr, rp, d, c.rms_eps, s));
-    if (lora)
+    if (lora) {
+      ++launches;
       CUDA_TRY(lora_shrink_launch(m->h, d, d, (const __nv_bfloat16*)w.a_gate,
                                   (const __nv_bfloat16*)w.a_up, 2, c.adapter_slots, c.lora_rank,
                                   m->scaling, seg_off, seg_rows, m->U, s));
+    }
     {
       GemmParams p = base;
       p.mode = EPI_SILU;
@@ -490,10 +507,12 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
       p.out_bf16 = m->f;
       if ((st = gemm(lm.gu, m->xmap_h, p, rp, c.ffn_dim))) return st;
     }
-    if (lora)
+    if (lora) {
+      ++launches;
       CUDA_TRY(lora_shrink_launch(m->f, c.ffn_dim, c.ffn_dim, (const __nv_bfloat16*)w.a_down,
                                   nullptr, 1, c.adapter_slots, c.lora_rank, m->scaling, seg_off,
                                   seg_rows, m->U, s));
+    }
     {
       GemmParams p = base;
       p.mode = EPI_RESID;
@@ -511,6 +530,7 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
   // final norm (emitting rows only) + LM head + argmax (src/engine.py:188-193)
   if (mt.n_lm > 0) {
     const int nlm_p = (mt.n_lm + 15) & ~15;
+    ++launches;
     CUDA_TRY(rmsnorm_launch(m->x, nullptr, nullptr, nullptr, m->hlm, nullptr, lm_rows, mt.n_lm, d,
                             c.rms_eps, s));
     if (nlm_p > mt.n_lm)
@@ -524,6 +544,7 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
     p.tile_best = m->tile_best;
     p.best_stride = rp;
     if ((st = gemm(m->lm_map, m->xmap_hlm, p, mt.n_lm, 0))) return st;
+    ++launches;
     CUDA_TRY(argmax_reduce_launch(m->tile_best, m->vpad / 128, rp, mt.n_lm, m->out_tok, s));
     if (logits_dev) {
       GemmParams q = base;
@@ -535,6 +556,10 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
       if ((st = gemm(m->lm_map, m->xmap_hlm, q, mt.n_lm, 0))) return st;
     }
   }
+  m->last_launches = launches;
+  m->last_items = mt.n_items;
+  m->last_mt = mt;
+  m->has_last = true;
   return ICR_OK;
 }
 
@@ -689,6 +714,7 @@ icr_status icr_forward(icr_model* m, const icr_batch* b, int32_t* out_tokens_hos
   CUDA_TRY(cudaEventSynchronize(m->staging_ev[0]));
   if ((st = pack_meta(m, b, nullptr, nullptr, m->staging[0], mt, plan, false))) return st;
   CUDA_TRY(cudaMemcpyAsync(m->meta_dev, m->staging[0], mt.total * sizeof(int), cudaMemcpyHostToDevice, s));
+  m->last_meta_bytes = (long long)mt.total * sizeof(int);
   CUDA_TRY(cudaEventRecord(m->staging_ev[0], s));
   if ((st = enqueue_forward(m, mt, logits_dev, s))) return st;
   if (mt.n_lm > 0 && out_tokens_host) {
@@ -737,6 +763,7 @@ icr_status icr_decode_loop(icr_model* m, const icr_batch* first, const int32_t* 
     const size_t from = (i == 0) ? 0 : mt.o_kind;
     cudaMemcpyAsync(m->meta_dev + from, m->staging[slot] + from, (mt.total - from) * sizeof(int),
                     cudaMemcpyHostToDevice, s);
+    m->last_meta_bytes = (long long)(mt.total - from) * sizeof(int);
     cudaEventRecord(m->staging_ev[slot], s);
     cudaEventRecord(evs[i], s);
     if ((st = enqueue_forward(m, mt, nullptr, s))) break;
@@ -755,6 +782,81 @@ icr_status icr_decode_loop(icr_model* m, const icr_batch* first, const int32_t* 
     cudaMemcpy(out_tokens_host_last, m->out_tok, n_lm * sizeof(int), cudaMemcpyDeviceToHost);
   for (auto& e : evs) cudaEventDestroy(e);
   return st;
+}
+
+// Instrumentation: [launches, metadata bytes, attention items] of the last forward.
+icr_status icr_model_stats(icr_model* m, int64_t* out3) {
+  if (!m || !out3) return fail(ICR_CONFIG, "null argument");
+  out3[0] = m->last_launches;
+  out3[1] = m->last_meta_bytes;
+  out3[2] = m->last_items;
+  return ICR_OK;
+}
+
+// Re-launch one projection GEMM family of the last forward `iters` times, cycling through
+// all layers so no weight tile is served from L2, and return the average device time per
+// launch (CUDA events on the launch stream). which: 0 wo, 1 gate|up, 2 down, 3 lm_head.
+// Side effects are confined to scratch buffers (residual stream, f, tile maxima).
+icr_status icr_profile_gemm(icr_model* m, int which, int iters, float* avg_ms, void* stream) {
+  if (!m || !avg_ms || iters < 1) return fail(ICR_CONFIG, "bad arguments");
+  if (!m->has_last) return fail(ICR_STATE, "profile needs a previous forward");
+  cudaStream_t s = (cudaStream_t)stream;
+  const icr_model_config& c = m->cfg;
+  const Meta& mt = m->last_mt;
+  int* md = m->meta_dev;
+  const bool lora = c.lora_rank > 0 && mt.n_dec > 0;
+  GemmParams p{};
+  p.ws = m->ws;
+  p.counters = m->counters;
+  p.rank = c.lora_rank;
+  p.n_u = 1;
+  p.m_valid = 1 << 30;
+  p.row_kind = md + mt.o_kind;
+  p.row_adapter = md + mt.o_adapter;
+  p.lora_u = m->U;
+  int rows = mt.rp;
+  CUtensorMap* xmaps = m->xmap_att;
+  const void* bptr_off = nullptr;
+  (void)bptr_off;
+  switch (which) {
+    case 0: p.mode = EPI_RESID; p.M = c.hidden_dim; p.K = m->q_dim; p.lora_m = c.hidden_dim;
+            p.resid = m->x; xmaps = m->xmap_att; break;
+    case 1: p.mode = EPI_SILU; p.M = 2 * c.ffn_dim; p.K = c.hidden_dim; p.lora_m = 2 * c.ffn_dim;
+            p.n_u = 2; p.out_bf16 = m->f; xmaps = m->xmap_h; break;
+    case 2: p.mode = EPI_RESID; p.M = c.hidden_dim; p.K = c.ffn_dim; p.lora_m = c.hidden_dim;
+            p.resid = m->x; xmaps = m->xmap_f; break;
+    case 3: p.mode = EPI_ARGMAX; p.M = m->vpad; p.K = c.hidden_dim; p.m_valid = c.vocab_size;
+            p.tile_best = m->tile_best; p.best_stride = mt.rp; rows = mt.n_lm; xmaps = m->xmap_hlm;
+            p.row_kind = nullptr; break;
+    default: return fail(ICR_MODE, "which must be 0..3");
+  }
+  if (rows > 256) return fail(ICR_SHAPE, "profile supports <= 256 rows");
+  p.n_rows = rows;
+  const int nt = gemm_pick_nt(rows);
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  const int L = which == 3 ? 1 : c.num_layers;
+  CUDA_TRY(cudaEventRecord(e0, s));
+  for (int it = 0; it < iters; ++it)
+    for (int l = 0; l < L; ++l) {
+      const icr_layer_weights& w = m->layers[l];
+      GemmParams q = p;
+      const CUtensorMap* wm = &m->lm_map;
+      if (which == 0) { wm = &m->maps[l].o; q.lora_b = lora ? (const __nv_bfloat16*)w.b_o : nullptr; }
+      if (which == 1) { wm = &m->maps[l].gu; q.lora_b = lora ? (const __nv_bfloat16*)w.b_gu : nullptr; }
+      if (which == 2) { wm = &m->maps[l].down; q.lora_b = lora ? (const __nv_bfloat16*)w.b_down : nullptr; }
+      cudaError_t e = gemm_launch(*wm, xmaps[nt_index(nt)], q, 0, nt, m->num_sms, s);
+      if (e != cudaSuccess) return fail(ICR_CUDA, "gemm: %s", cudaGetErrorString(e));
+    }
+  CUDA_TRY(cudaEventRecord(e1, s));
+  CUDA_TRY(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+  *avg_ms = ms / (float)(iters * L);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return ICR_OK;
 }
 
 // ---- building blocks for parity tests ----

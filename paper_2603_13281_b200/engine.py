@@ -1,0 +1,344 @@
+"""Generation sessions on the B200: prefill, the fused multi-model decode step, generate.
+
+Drop-in for the reference's src/engine.py (same names, arguments, guards, ledger
+arithmetic and error classes). Semantics carried over exactly:
+  * prefill is encoder-only work and emits the BASE model's greedy token (engine.py:84-153),
+    reusing the longest pooled block prefix and computing only the suffix;
+  * a fused step runs the encoder row (base weights, writes K/V for `pos` before
+    attention) and the decoder row (base + LoRA, predicts the next token) in ONE pass
+    (engine.py:179-193, model.py:480-506);
+  * greedy argmax, lowest id on ties (engine.py:75-76).
+
+B200 generalisation: `decode_step_batch(sessions, tokens)` advances many sessions --
+each with its own adapter -- in one forward over 2N token rows, with sessions that share
+a prompt reading the same KV pages. The single-session calls are batch-of-one wrappers.
+All compute goes through runtime.Runtime.forward (the C ABI); there is no CPU path.
+"""
+
+from __future__ import annotations
+
+from typing import Optional, Sequence
+
+import numpy as np
+
+from .errors import (CapacityError, ConfigError, ContractViolationError, ModeError,
+                     StateError)
+from .metrics import Ledger
+from .model import BLOCK_TOKENS, DECODER_TARGETS, AdapterSet, BaseWeights, KvCacheTensor
+
+
+class GenerationSession:
+    """One sequence in flight: block-table row, page-backed cache, counters, predictions.
+
+    `base_next` maps a computed position to the base model's greedy next token (the
+    encoder row's argmax) -- what the reference derives from `final_hidden` for chunk-end
+    commits (engine.py:274-284)."""
+
+    def __init__(self, base: BaseWeights, adapter: Optional[AdapterSet], max_context: int,
+                 ledger: Optional[Ledger] = None, runtime=None, capture_logits: bool = False):
+        if adapter is not None:
+            bad = set(adapter.targets) - set(DECODER_TARGETS)
+            if bad:
+                raise ContractViolationError(
+                    f"adapter targets {sorted(bad)} cannot ride a shared cache; "
+                    f"decoder-side targets are {DECODER_TARGETS}")
+            if adapter.config != base.config:
+                raise ConfigError("adapter was built for a different model config")
+        if max_context < 1:
+            raise ConfigError(f"max_context must be positive, got {max_context}")
+        self.runtime = runtime if runtime is not None else base.runtime()
+        if max_context > self.runtime.max_context:
+            raise ConfigError(f"max_context {max_context} exceeds the runtime's "
+                              f"{self.runtime.max_context}")
+        self.base = base
+        self.adapter = adapter
+        self.config = base.config
+        self.max_context = max_context
+        self.ledger = ledger if ledger is not None else Ledger()
+        self.capture_logits = capture_logits
+        self.adapter_slot = self.runtime.slots.slot_of(adapter) if adapter is not None else -1
+        self.seq = self.runtime.acquire_seq()
+        self.cache = KvCacheTensor(base.config, max_context, arena=self.runtime.arena)
+        self.prompt: list[int] = []
+        self.produced: list[int] = []
+        self.base_next: dict[int, int] = {}
+        self.last_logits: Optional[np.ndarray] = None
+        self.borrowed_chain: list = []
+        self._prefilled = False
+        self._closed = False
+
+    def close(self) -> None:
+        """Return the sequence slot and this session's page references."""
+        if self._closed:
+            return
+        self._closed = True
+        self.cache.release()
+        self.runtime.release_seq(self.seq)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _sync_block_table(self) -> None:
+        self.runtime.set_pages(self.seq, self.cache.pages)
+
+
+def new_session(base: BaseWeights, adapter: Optional[AdapterSet] = None, max_context: int = 512,
+                ledger: Optional[Ledger] = None, runtime=None,
+                capture_logits: bool = False) -> GenerationSession:
+    return GenerationSession(base, adapter, max_context, ledger, runtime, capture_logits)
+
+
+def _check_tokens(session: GenerationSession, tokens) -> list[int]:
+    toks = [int(t) for t in tokens]
+    vocab = session.config.vocab_size
+    for t in toks:
+        if not (0 <= t < vocab):
+            raise IndexError(f"token {t} outside vocab [0, {vocab})")
+    return toks
+
+
+def _reads_per_step(session) -> int:
+    # 7 projections per layer (wk, wv, wq, wo, gate, up, down) + the LM head (ledger
+    # arithmetic of src/engine.py:166-176 with base_linear counting at model.py:334-336)
+    return 7 * session.config.num_layers + 1
+
+
+def _logits_np(lg, row: int) -> Optional[np.ndarray]:
+    return None if lg is None else lg[row].float().cpu().numpy()
+
+
+def prefill(session: GenerationSession, prompt, pool=None, namespace: Optional[str] = None,
+            reader: Optional[str] = None) -> int:
+    """Encode the prompt, reuse the pooled prefix, emit the first (base) token."""
+    if session._prefilled:
+        raise StateError("session already prefilled")
+    toks = _check_tokens(session, prompt)
+    if not toks:
+        raise ValueError("prompt must contain at least one token")
+    if len(toks) > session.max_context:
+        raise CapacityError(f"prompt length {len(toks)} exceeds max context {session.max_context}")
+    cfg, rt, led = session.config, session.runtime, session.ledger
+    matched, chain = 0, []
+    if pool is not None:
+        matched, chain = pool.lookup(namespace, toks, reader=reader)
+        if chain:
+            if any(b.arena is not rt.arena for b in chain):
+                pool.release(chain)
+                raise ContractViolationError("pooled blocks live in another page arena")
+            session.cache.attach_shared([b.page for b in chain])
+            session.borrowed_chain = chain
+        led.prefix_hit_tokens += matched
+
+    n = len(toks)
+    suffix = toks[matched:]
+    if suffix:
+        session.cache.ensure_pages(n - 1)
+        session._sync_block_table()
+        step = rt.max_rows
+        token, last_lg = None, None
+        for c0 in range(matched, n, step):
+            c1 = min(n, c0 + step)
+            pos = np.arange(c0, c1, dtype=np.int32)
+            emit = ((pos % BLOCK_TOKENS) == BLOCK_TOKENS - 1) | (pos == n - 1)
+            out, lg = rt.forward(tokens=toks[c0:c1], kind=np.zeros(c1 - c0, np.int32),
+                                 seq=np.full(c1 - c0, session.seq, np.int32), pos=pos,
+                                 adapter=np.full(c1 - c0, -1, np.int32), emit=emit.astype(np.int32),
+                                 logits=session.capture_logits and c1 == n)
+            session.cache.advance(c1 - c0)
+            for p, t in zip(pos[emit], out):
+                session.base_next[int(p)] = int(t)
+            if c1 == n:
+                token = int(out[-1])
+                last_lg = _logits_np(lg, int(emit.sum()) - 1)
+        led.prefill_tokens += len(suffix)
+        led.kv_bytes_written += len(suffix) * cfg.kv_bytes_per_token
+        led.param_matrix_reads += _reads_per_step(session)
+        session.last_logits = last_lg
+    else:
+        stored = chain[-1].next_token if chain else None
+        if stored is not None:
+            token = int(stored)
+            session.last_logits = None
+        else:
+            # Older blocks lack the chunk-end prediction: replay the last position through a
+            # read-only (decoder-kind, no adapter) row -- it cannot write KV (engine.py:140-148).
+            session._sync_block_table()
+            out, lg = rt.forward(tokens=[toks[-1]], kind=[1], seq=[session.seq], pos=[n - 1],
+                                 adapter=[-1], emit=[1], logits=session.capture_logits)
+            token = int(out[0])
+            session.base_next[n - 1] = token
+            session.last_logits = _logits_np(lg, 0)
+            led.prefill_tokens += 1
+            led.param_matrix_reads += 5 * cfg.num_layers + 1
+    session.prompt = toks
+    session.produced = [token]
+    session._prefilled = True
+    return token
+
+
+def _pre_step(session: GenerationSession, token: int) -> int:
+    if session._closed:
+        raise StateError("session is closed")
+    if not session._prefilled:
+        raise StateError("decode before prefill")
+    _check_tokens(session, [token])
+    pos = session.cache.position_count
+    if pos + 1 > session.max_context:
+        raise CapacityError(f"context full at {pos}/{session.max_context}")
+    return pos
+
+
+def _account_step(session: GenerationSession, pos: int, passes: int, reads: int) -> None:
+    """src/engine.py:166-176."""
+    led, cfg = session.ledger, session.config
+    led.decode_steps += 1
+    led.param_passes += passes
+    led.param_matrix_reads += reads
+    led.kv_read_events += 1
+    led.kv_bytes_read += (pos + 1) * cfg.kv_bytes_per_token
+    led.kv_bytes_written += cfg.kv_bytes_per_token
+
+
+def _prepare_write(session: GenerationSession, pos: int) -> None:
+    session.cache.ensure_pages(pos)
+    page = session.cache.pages[pos // BLOCK_TOKENS]
+    if session.runtime.arena.refcount(page) != 1:
+        raise ContractViolationError(f"position {pos} would be written into shared page {page}")
+    session._sync_block_table()
+
+
+def decode_step_batch(sessions: Sequence[GenerationSession], tokens: Sequence[int]) -> list[int]:
+    """ONE fused forward for many sessions (each its own adapter): per session an encoder
+    row and -- if adapted -- a decoder row. Returns each session's next token."""
+    if len(sessions) != len(tokens):
+        raise ValueError("one token per session")
+    if not sessions:
+        return []
+    rt = sessions[0].runtime
+    if any(s.runtime is not rt for s in sessions):
+        raise ConfigError("sessions in one batch must share a runtime")
+    if len({s.seq for s in sessions}) != len(sessions):
+        raise StateError("a session appears twice in one batch")
+    tok, kind, seq, pos, ad, emit = [], [], [], [], [], []
+    plan = []
+    for s, t in zip(sessions, tokens):
+        p = _pre_step(s, int(t))
+        _prepare_write(s, p)
+        enc = len(tok)
+        tok.append(int(t)); kind.append(0); seq.append(s.seq); pos.append(p); ad.append(-1); emit.append(1)
+        dec = enc
+        if s.adapter is not None:
+            dec = len(tok)
+            tok.append(int(t)); kind.append(1); seq.append(s.seq); pos.append(p)
+            ad.append(s.adapter_slot); emit.append(1)
+        plan.append((s, p, enc, dec))
+    want_logits = any(s.capture_logits for s in sessions)
+    out, lg = rt.forward(tok, kind, seq, pos, ad, emit, logits=want_logits)
+    nxt = []
+    for s, p, enc, dec in plan:
+        s.cache.advance(1)
+        s.base_next[p] = int(out[enc])
+        s.last_logits = _logits_np(lg, dec) if s.capture_logits else None
+        _account_step(s, p, passes=1, reads=_reads_per_step(s))
+        nxt.append(int(out[dec]))
+    return nxt
+
+
+def decode_step_fused(session: GenerationSession, token: int) -> int:
+    """One fused pair step (engine.py:179-193): a batch of one session."""
+    return decode_step_batch([session], [token])[0]
+
+
+def decode_step_sequential(session: GenerationSession, token: int) -> int:
+    """Oracle-shaped path (engine.py:196-215): an encoder pass that writes K/V, then a
+    read-only decoder pass -- two parameter sweeps. Same kernels, two forwards."""
+    pos = _pre_step(session, token)
+    _prepare_write(session, pos)
+    rt = session.runtime
+    out, _ = rt.forward([token], [0], [session.seq], [pos], [-1], [1])
+    session.cache.advance(1)
+    session.base_next[pos] = int(out[0])
+    out2, lg = rt.forward([token], [1], [session.seq], [pos], [session.adapter_slot], [1],
+                          logits=session.capture_logits)
+    session.last_logits = _logits_np(lg, 0)
+    L = session.config.num_layers
+    _account_step(session, pos, passes=2, reads=7 * L + 5 * L + 1)
+    return int(out2[0])
+
+
+def decode_step_base(session: GenerationSession, token: int) -> int:
+    """Bare-base step (engine.py:218-233); refuses adapted sessions."""
+    if session.adapter is not None:
+        raise StateError("base decode on a session that carries an adapter")
+    return decode_step_batch([session], [token])[0]
+
+
+_STEPS = {"fused": decode_step_fused, "sequential": decode_step_sequential}
+
+
+def generate(session: GenerationSession, prompt, max_new: int, path: str = "fused", pool=None,
+             namespace: Optional[str] = None, reader: Optional[str] = None,
+             end_token: Optional[int] = None) -> list[int]:
+    """Prefill then greedy-decode up to max_new tokens, first one included (engine.py:239-252)."""
+    if max_new < 1:
+        raise ValueError(f"max_new must be at least 1, got {max_new}")
+    if path not in _STEPS:
+        raise ModeError(f"decode path must be one of {sorted(_STEPS)}, got {path!r}")
+    step = _STEPS[path]
+    out = [prefill(session, prompt, pool=pool, namespace=namespace, reader=reader)]
+    while len(out) < max_new and out[-1] != end_token:
+        out.append(step(session, out[-1]))
+    session.produced = list(out)
+    return out
+
+
+def generate_batch(sessions: Sequence[GenerationSession], prompts, max_new: int, pool=None,
+                   namespace: Optional[str] = None, readers=None,
+                   end_token: Optional[int] = None) -> list[list[int]]:
+    """B200 extension: prefill each session (pool-aware, in order, so later sessions hit
+    the prefix earlier ones committed) then advance all of them with batched fused steps."""
+    readers = readers or [None] * len(sessions)
+    outs = [[prefill(s, p, pool=pool, namespace=namespace, reader=r)]
+            for s, p, r in zip(sessions, prompts, readers)]
+    live = [i for i in range(len(sessions)) if max_new > 1 and outs[i][-1] != end_token]
+    while live:
+        nxt = decode_step_batch([sessions[i] for i in live], [outs[i][-1] for i in live])
+        for i, t in zip(live, nxt):
+            outs[i].append(t)
+        live = [i for i in live if len(outs[i]) < max_new and outs[i][-1] != end_token]
+    for s, o in zip(sessions, outs):
+        s.produced = list(o)
+    return outs
+
+
+def replay_base(base: BaseWeights, tokens, prompt_len: int, max_context: Optional[int] = None,
+                ledger: Optional[Ledger] = None, runtime=None) -> GenerationSession:
+    """Force the bare base model over a fixed token sequence (engine.py:255-271)."""
+    toks = [int(t) for t in tokens]
+    if not (1 <= prompt_len <= len(toks)):
+        raise ValueError(f"prompt_len {prompt_len} outside [1, {len(toks)}]")
+    session = new_session(base, None, max_context or len(toks) + 1, ledger, runtime)
+    prefill(session, toks[:prompt_len])
+    for t in toks[prompt_len:]:
+        decode_step_base(session, t)
+    return session
+
+
+def base_next_token_at(session: GenerationSession, pos: int) -> int:
+    """Greedy base prediction at a computed position (engine.py:274-284)."""
+    if pos < 0 or pos >= session.cache.position_count:
+        raise StateError(f"position {pos} was not computed by this session")
+    tok = session.base_next.get(pos)
+    if tok is None:
+        # Not emitted during prefill: a read-only row at `pos` reproduces the encoder row's
+        # prediction bit for bit (row-independent kernels, same keys 0..pos).
+        session._sync_block_table()
+        fed = session.prompt + session.produced
+        out, _ = session.runtime.forward([fed[pos]], [1], [session.seq], [pos], [-1], [1])
+        tok = int(out[0])
+        session.base_next[pos] = tok
+    session.ledger.param_matrix_reads += 1
+    return tok

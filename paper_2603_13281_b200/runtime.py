@@ -1,0 +1,433 @@
+"""Device residency and the bridge to the sm_100a library.
+
+  PageArena      the shared KV page store: K and V arenas [L, pages, H_kv, 16, hd] bf16,
+                 a free list and per-page reference counts. One page = one pool block
+                 (BLOCK_TOKENS = 16 positions) for all layers.
+  DeviceWeights  the base model packed for the kernels: bf16, [out, in] (K-major),
+                 RMSNorm gains folded into the following projection, wq|wk|wv fused,
+                 gate/up rows interleaved, LM head padded to a multiple of 128 rows.
+  AdapterSlots   resident LoRA adapters (reference A as-is, B pre-multiplied by
+                 alpha/rank), addressed by slot; the decode step picks a slot per row.
+  Runtime        owns the above plus the C model handle and the host block table;
+                 `forward` is one fused multi-model step (icr_forward).
+
+Memory is allocated with torch (plumbing); all compute is the library's CUDA kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .errors import CapacityError, ConfigError, ContractViolationError, DeviceError
+from .model import BLOCK_TOKENS, DECODER_TARGETS, AdapterSet, ModelConfig
+
+
+def _torch():
+    import torch
+    return torch
+
+
+# ----------------------------------------------------------------------------- pages
+class PageArena:
+    """Reference-counted 16-token KV pages shared by sessions and the prefix pool."""
+
+    def __init__(self, config: ModelConfig, num_pages: int, device="cuda"):
+        torch = _torch()
+        if num_pages < 1:
+            raise ConfigError(f"page arena needs at least one page, got {num_pages}")
+        self.config = config
+        self.num_pages = num_pages
+        shape = (config.num_layers, num_pages, config.num_kv_heads, BLOCK_TOKENS, config.head_dim)
+        self.k = torch.zeros(shape, dtype=torch.bfloat16, device=device)
+        self.v = torch.zeros(shape, dtype=torch.bfloat16, device=device)
+        self.refs = np.zeros(num_pages, dtype=np.int32)
+        self._free = list(range(num_pages - 1, -1, -1))
+
+    @classmethod
+    def host_only(cls, config: ModelConfig, pages: int) -> "PageArena":
+        return cls(config, max(pages, 1), device="cpu")
+
+    @property
+    def page_bytes(self) -> int:
+        return self.config.num_layers * 2 * self.config.num_kv_heads * BLOCK_TOKENS * self.config.head_dim * 2
+
+    def layer_ptrs(self, layer: int) -> tuple[int, int]:
+        stride = self.k.stride(0) * self.k.element_size()
+        return self.k.data_ptr() + layer * stride, self.v.data_ptr() + layer * stride
+
+    def free_pages(self) -> int:
+        return len(self._free)
+
+    def alloc(self) -> int:
+        if not self._free:
+            raise CapacityError(f"KV page arena exhausted ({self.num_pages} pages)")
+        pid = self._free.pop()
+        self.refs[pid] = 1
+        return pid
+
+    def incref(self, pid: int) -> None:
+        if self.refs[pid] < 1:
+            raise ContractViolationError(f"incref of free page {pid}")
+        self.refs[pid] += 1
+
+    def decref(self, pid: int) -> None:
+        if self.refs[pid] < 1:
+            raise ContractViolationError(f"double free of page {pid}")
+        self.refs[pid] -= 1
+        if self.refs[pid] == 0:
+            self._free.append(pid)
+
+    def refcount(self, pid: int) -> int:
+        return int(self.refs[pid])
+
+    # host-side row access (tests, copy-in, fingerprints) --------------------------
+    def _index(self, pages, start, stop):
+        pos = np.arange(start, stop)
+        return (np.asarray(pages, dtype=np.int64)[pos // BLOCK_TOKENS], pos % BLOCK_TOKENS)
+
+    def write_rows(self, layer, pages, at, k, v) -> None:
+        torch = _torch()
+        pid, slot = self._index(pages, at, at + k.shape[0])
+        pid_t = torch.as_tensor(pid, device=self.k.device)
+        slot_t = torch.as_tensor(slot, device=self.k.device)
+        kt = torch.as_tensor(np.asarray(k, dtype=np.float32)).to(self.k.device, torch.bfloat16)
+        vt = torch.as_tensor(np.asarray(v, dtype=np.float32)).to(self.k.device, torch.bfloat16)
+        self.k[layer, pid_t, :, slot_t] = kt
+        self.v[layer, pid_t, :, slot_t] = vt
+
+    def _gather(self, layer, pages, start, stop):
+        torch = _torch()
+        pid, slot = self._index(pages, start, stop)
+        pid_t = torch.as_tensor(pid, device=self.k.device)
+        slot_t = torch.as_tensor(slot, device=self.k.device)
+        return self.k[layer, pid_t, :, slot_t], self.v[layer, pid_t, :, slot_t]  # [n, Hkv, hd]
+
+    def read_rows(self, layer, pages, start, stop):
+        k, v = self._gather(layer, pages, start, stop)
+        return k.float().cpu().numpy(), v.float().cpu().numpy()
+
+    def read_raw(self, layer, pages, start, stop) -> tuple[bytes, bytes]:
+        if stop <= start:
+            return b"", b""
+        torch = _torch()
+        k, v = self._gather(layer, pages, start, stop)
+        as_bytes = lambda t: t.contiguous().view(torch.int16).cpu().numpy().tobytes()  # noqa: E731
+        return as_bytes(k), as_bytes(v)
+
+
+# ----------------------------------------------------------------------------- weights
+class DeviceWeights:
+    """Base weights in the kernel layout (see module doc)."""
+
+    def __init__(self, config: ModelConfig):
+        self.config = config
+        self.layers: list[dict] = []
+        self.embed = None
+        self.lm_head = None
+
+    @property
+    def vocab_pad(self) -> int:
+        return (self.config.vocab_size + 127) // 128 * 128
+
+    @classmethod
+    def from_host(cls, base, device="cuda") -> "DeviceWeights":
+        torch = _torch()
+        cfg = base.config
+        cfg.check_device_shapes()
+        self = cls(cfg)
+        bf = torch.bfloat16
+
+        def t(a):
+            return torch.from_numpy(np.array(a, dtype=np.float32, copy=True))
+
+        for lw in base.layers:
+            g_attn = t(lw.attn_gain.data)[None, :]
+            g_ffn = t(lw.ffn_gain.data)[None, :]
+            qkv = torch.cat([t(lw.wq.data).T, t(lw.wk.data).T, t(lw.wv.data).T], 0) * g_attn
+            gate = t(lw.gate.data).T * g_ffn
+            up = t(lw.up.data).T * g_ffn
+            gu = torch.stack([gate, up], 1).reshape(2 * cfg.ffn_dim, cfg.hidden_dim)
+            self.layers.append({
+                "w_qkv": qkv.to(device, bf).contiguous(),
+                "w_o": t(lw.wo.data).T.to(device, bf).contiguous(),
+                "w_gu": gu.to(device, bf).contiguous(),
+                "w_down": t(lw.down.data).T.to(device, bf).contiguous(),
+            })
+        self.embed = t(base.embed.data).to(device, bf).contiguous()
+        lm = torch.zeros(self.vocab_pad, cfg.hidden_dim)
+        lm[:cfg.vocab_size] = t(base.lm_head.data).T * t(base.final_gain.data)[None, :]
+        self.lm_head = lm.to(device, bf).contiguous()
+        return self
+
+    @classmethod
+    def random(cls, cfg: ModelConfig, seed: int, device="cuda") -> "DeviceWeights":
+        torch = _torch()
+        cfg.check_device_shapes()
+        self = cls(cfg)
+        gen = torch.Generator(device=device)
+        gen.manual_seed(int(seed))
+        bf = torch.bfloat16
+        d, qd, kvd, f = cfg.hidden_dim, cfg.q_dim, cfg.kv_dim, cfg.ffn_dim
+
+        def draw(rows, cols, fan_in):
+            out = torch.empty(rows, cols, dtype=bf, device=device)
+            step = max(1, (1 << 26) // cols)
+            for r0 in range(0, rows, step):
+                r1 = min(rows, r0 + step)
+                out[r0:r1] = (torch.randn(r1 - r0, cols, generator=gen, device=device)
+                              / math.sqrt(fan_in)).to(bf)
+            return out
+
+        for _ in range(cfg.num_layers):
+            self.layers.append({
+                "w_qkv": draw(qd + 2 * kvd, d, d), "w_o": draw(d, qd, qd),
+                "w_gu": draw(2 * f, d, d), "w_down": draw(d, f, f)})
+        self.embed = draw(cfg.vocab_size, d, d)
+        lm = draw(self.vocab_pad, d, d)
+        lm[cfg.vocab_size:] = 0
+        self.lm_head = lm
+        return self
+
+    def checksum(self) -> str:
+        torch = _torch()
+        acc = 0.0
+        for lw in self.layers:
+            for w in lw.values():
+                acc += float(w.float().sum(dtype=torch.float64)) if w.numel() < (1 << 24) else float(
+                    w[::97].float().sum(dtype=torch.float64))
+        acc += float(self.embed.float().sum(dtype=torch.float64))
+        return f"{acc:.10e}"
+
+    def nbytes_streamed(self) -> int:
+        """Weight bytes one decode step streams (embedding is gathered, not streamed)."""
+        n = sum(w.numel() * w.element_size() for lw in self.layers for w in lw.values())
+        return n + self.config.vocab_size * self.config.hidden_dim * 2
+
+
+# ----------------------------------------------------------------------------- adapters
+_A_KEYS = ("a_q", "a_o", "a_gate", "a_up", "a_down")
+_B_KEYS = ("b_q", "b_o", "b_gu", "b_down")
+
+
+class AdapterSlots:
+    """Resident LoRA adapters; slot s of every tensor belongs to one AdapterSet."""
+
+    def __init__(self, cfg: ModelConfig, slots: int, rank: int, device="cuda"):
+        torch = _torch()
+        self.cfg, self.n, self.rank, self.device = cfg, slots, rank, device
+        L, d, qd, f = cfg.num_layers, cfg.hidden_dim, cfg.q_dim, cfg.ffn_dim
+        z = lambda *s: torch.zeros(*s, dtype=torch.bfloat16, device=device)  # noqa: E731
+        if slots > 0 and rank > 0:
+            self.t = {
+                "a_q": z(L, slots, rank, d), "b_q": z(L, slots, qd, rank),
+                "a_o": z(L, slots, rank, qd), "b_o": z(L, slots, d, rank),
+                "a_gate": z(L, slots, rank, d), "a_up": z(L, slots, rank, d),
+                "b_gu": z(L, slots, 2 * f, rank),
+                "a_down": z(L, slots, rank, f), "b_down": z(L, slots, d, rank),
+            }
+        else:
+            self.t = {}
+        self._owner: dict[int, int] = {}  # id(adapter) -> slot
+        self._refs: list = [None] * slots
+
+    def slot_of(self, adapter: AdapterSet) -> int:
+        key = id(adapter)
+        if key in self._owner:
+            return self._owner[key]
+        if self.n == 0 or self.rank == 0:
+            raise CapacityError("runtime has no adapter slots (adapter_slots=0)")
+        if adapter.rank > self.rank:
+            raise ConfigError(f"adapter rank {adapter.rank} exceeds slot rank {self.rank}")
+        free = [i for i, r in enumerate(self._refs) if r is None]
+        if not free:
+            raise CapacityError(f"all {self.n} adapter slots are in use")
+        s = free[0]
+        self._upload(s, adapter)
+        self._owner[key] = s
+        self._refs[s] = adapter
+        return s
+
+    def _upload(self, s: int, ad: AdapterSet) -> None:
+        torch = _torch()
+        cfg, r, bf = self.cfg, ad.rank, torch.bfloat16
+        for key in self.t:
+            self.t[key][:, s].zero_()
+        if ad.device_seed is not None:
+            self._upload_random(s, ad)
+            return
+        sc = float(ad.scaling)
+        for layer, per in enumerate(ad.layers):
+            def A(name):
+                return torch.as_tensor(np.asarray(per[name].a.data, np.float32))
+
+            def B(name):
+                return torch.as_tensor(np.asarray(per[name].b.data, np.float32)) * sc
+
+            if "q" in per:
+                self.t["a_q"][layer, s, :r] = A("q").to(self.device, bf)
+                self.t["b_q"][layer, s, :, :r] = B("q").to(self.device, bf)
+            if "o" in per:
+                self.t["a_o"][layer, s, :r] = A("o").to(self.device, bf)
+                self.t["b_o"][layer, s, :, :r] = B("o").to(self.device, bf)
+            if "gate" in per:
+                self.t["a_gate"][layer, s, :r] = A("gate").to(self.device, bf)
+                self.t["b_gu"][layer, s, 0::2, :r] = B("gate").to(self.device, bf)
+            if "up" in per:
+                self.t["a_up"][layer, s, :r] = A("up").to(self.device, bf)
+                self.t["b_gu"][layer, s, 1::2, :r] = B("up").to(self.device, bf)
+            if "down" in per:
+                self.t["a_down"][layer, s, :r] = A("down").to(self.device, bf)
+                self.t["b_down"][layer, s, :, :r] = B("down").to(self.device, bf)
+
+    def _upload_random(self, s: int, ad: AdapterSet) -> None:
+        torch = _torch()
+        gen = torch.Generator(device=self.device)
+        gen.manual_seed(int(ad.device_seed))
+        r, sc = ad.rank, float(ad.scaling)
+        cfg = self.cfg
+        fan = {"a_q": cfg.hidden_dim, "a_o": cfg.q_dim, "a_gate": cfg.hidden_dim,
+               "a_up": cfg.hidden_dim, "a_down": cfg.ffn_dim}
+        for key in _A_KEYS:
+            t = self.t[key][:, s, :r]
+            t.copy_(torch.randn(t.shape, generator=gen, device=self.device) / math.sqrt(fan[key]))
+        for key in _B_KEYS:
+            t = self.t[key][:, s, :, :r]
+            t.copy_(torch.randn(t.shape, generator=gen, device=self.device) * (ad.b_scale * sc))
+
+    def release(self, adapter: AdapterSet) -> None:
+        s = self._owner.pop(id(adapter), None)
+        if s is not None:
+            self._refs[s] = None
+
+    def layer_ptrs(self, layer: int) -> dict:
+        return {k: v[layer].data_ptr() for k, v in self.t.items()}
+
+
+# ----------------------------------------------------------------------------- runtime
+class Runtime:
+    """The device side of one BaseWeights: page arena, adapter slots, block table and the
+    C model handle. Sessions borrow a block-table row (sequence slot) each."""
+
+    def __init__(self, base, max_seqs: int = 64, max_context: int = 4096,
+                 num_pages: Optional[int] = None, max_rows: int = 512, adapter_slots: int = 8,
+                 lora_rank: int = 16, chunk_pages: int = 16, device="cuda"):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise DeviceError("no CUDA device: the B200 path has no CPU fallback")
+        cfg = base.config
+        cfg.check_device_shapes()
+        self.config = cfg
+        self.base = base
+        self.device = device
+        self.max_seqs = max_seqs
+        self.max_context = max_context
+        self.max_pages_per_seq = (max_context + BLOCK_TOKENS - 1) // BLOCK_TOKENS
+        if num_pages is None:
+            num_pages = min(max_seqs * self.max_pages_per_seq, 1 << 16)
+        self.max_rows = max_rows
+        self.chunk_pages = chunk_pages
+        self.dw = base.device(device)
+        self.arena = PageArena(cfg, num_pages, device)
+        self.slots = AdapterSlots(cfg, adapter_slots, lora_rank if adapter_slots else 0, device)
+        self.block_table = np.full((max_seqs, self.max_pages_per_seq), -1, dtype=np.int32)
+        self._free_seq = list(range(max_seqs - 1, -1, -1))
+        self._handle = C.c_void_p()
+        self._lib = _lib.load()
+        self._create()
+
+    def check_capacity(self, **caps) -> None:
+        for k, v in caps.items():
+            have = getattr(self, k, None)
+            if have is not None and isinstance(v, int) and v > have:
+                raise ConfigError(f"runtime already created with {k}={have} < requested {v}")
+
+    def _create(self) -> None:
+        cfg = self.config
+        c = _lib.ModelConfigC(
+            num_layers=cfg.num_layers, hidden_dim=cfg.hidden_dim, num_heads=cfg.num_heads,
+            num_kv_heads=cfg.num_kv_heads, head_dim=cfg.head_dim, ffn_dim=cfg.ffn_dim,
+            vocab_size=cfg.vocab_size, rms_eps=cfg.rms_eps, rope_theta=cfg.rope_theta,
+            max_positions=self.max_context, num_pages=self.arena.num_pages,
+            max_seqs=self.max_seqs, max_pages_per_seq=self.max_pages_per_seq,
+            max_rows=self.max_rows, adapter_slots=self.slots.n, lora_rank=self.slots.rank,
+            chunk_pages=self.chunk_pages)
+        layers = (_lib.LayerWeightsC * cfg.num_layers)()
+        for l in range(cfg.num_layers):
+            lw = self.dw.layers[l]
+            kp, vp = self.arena.layer_ptrs(l)
+            ap = self.slots.layer_ptrs(l)
+            layers[l] = _lib.LayerWeightsC(
+                w_qkv=lw["w_qkv"].data_ptr(), w_o=lw["w_o"].data_ptr(),
+                w_gu=lw["w_gu"].data_ptr(), w_down=lw["w_down"].data_ptr(),
+                a_q=ap.get("a_q"), b_q=ap.get("b_q"), a_o=ap.get("a_o"), b_o=ap.get("b_o"),
+                a_gate=ap.get("a_gate"), a_up=ap.get("a_up"), b_gu=ap.get("b_gu"),
+                a_down=ap.get("a_down"), b_down=ap.get("b_down"), k_pages=kp, v_pages=vp)
+        self._layers_c = layers
+        _lib.check(self._lib.icr_model_create(C.byref(c), layers, self.dw.embed.data_ptr(),
+                                              self.dw.lm_head.data_ptr(), C.c_float(1.0),
+                                              C.byref(self._handle)))
+
+    def __del__(self):
+        try:
+            if self._handle:
+                self._lib.icr_model_destroy(self._handle)
+                self._handle = C.c_void_p()
+        except Exception:
+            pass
+
+    # -- sequence slots -------------------------------------------------------------------
+    def acquire_seq(self) -> int:
+        if not self._free_seq:
+            raise CapacityError(f"all {self.max_seqs} sequence slots are in use")
+        return self._free_seq.pop()
+
+    def release_seq(self, slot: int) -> None:
+        self.block_table[slot] = -1
+        self._free_seq.append(slot)
+
+    def set_pages(self, slot: int, pages: list) -> None:
+        row = self.block_table[slot]
+        row[:len(pages)] = pages
+        row[len(pages):] = -1
+
+    # -- the step ---------------------------------------------------------------------------
+    def forward(self, tokens, kind, seq, pos, adapter, emit, logits: bool = False):
+        """One fused forward over token rows (see include/icarus_b200.h icr_batch).
+        Returns (tokens for emitting rows, logits tensor or None)."""
+        torch = _torch()
+        arrs = [np.ascontiguousarray(a, dtype=np.int32) for a in (tokens, kind, seq, pos, adapter, emit)]
+        n = arrs[0].shape[0]
+        n_seqs = int(max(arrs[2].max(), 0)) + 1
+        b = _lib.BatchC(n, *[_lib.i32_ptr(a) for a in arrs], _lib.i32_ptr(self.block_table), n_seqs)
+        n_emit = int(arrs[5].sum())
+        out = np.zeros(max(n_emit, 1), dtype=np.int32)
+        lg = None
+        if logits and n_emit:
+            lg = torch.empty(n_emit, self.dw.vocab_pad, dtype=torch.float32, device=self.device)
+        _lib.check(self._lib.icr_forward(self._handle, C.byref(b), _lib.i32_ptr(out),
+                                         lg.data_ptr() if lg is not None else None,
+                                         _lib.stream_handle()))
+        if lg is not None:
+            lg = lg[:, :self.config.vocab_size]
+        return out[:n_emit], lg
+
+    def decode_loop(self, tokens, kind, seq, pos, adapter, emit, feedback, steps: int):
+        """Device-resident decode loop (icr_decode_loop): returns per-step device ms and
+        the last step's emitted tokens."""
+        arrs = [np.ascontiguousarray(a, dtype=np.int32) for a in (tokens, kind, seq, pos, adapter, emit)]
+        n = arrs[0].shape[0]
+        n_seqs = int(max(arrs[2].max(), 0)) + 1
+        fb = np.ascontiguousarray(feedback, dtype=np.int32)
+        b = _lib.BatchC(n, *[_lib.i32_ptr(a) for a in arrs], _lib.i32_ptr(self.block_table), n_seqs)
+        ms = np.zeros(steps, dtype=np.float32)
+        last = np.zeros(max(int(arrs[5].sum()), 1), dtype=np.int32)
+        _lib.check(self._lib.icr_decode_loop(self._handle, C.byref(b), _lib.i32_ptr(fb), steps,
+                                             _lib.i32_ptr(last),
+                                             ms.ctypes.data_as(C.POINTER(C.c_float)),
+                                             _lib.stream_handle()))
+        return ms, last

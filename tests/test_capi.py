@@ -1,0 +1,41 @@
+"""The C-ABI library loads on a CPU-only box and exports every symbol the header declares."""
+
+import re
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def test_header_and_binding_agree():
+    from paper_2603_13281_b200 import _lib
+    header = (ROOT / "include" / "icarus_b200.h").read_text()
+    declared = set(re.findall(r"\b(icr_[a-z_0-9]+)\s*\(", header))
+    assert declared == set(_lib.EXPORTED)
+
+
+def test_library_exports_every_symbol():
+    from paper_2603_13281_b200 import _lib
+    if not _lib.LIB_PATH.exists():
+        pytest.skip("library not built")
+    lib = _lib.load()
+    for name in _lib.EXPORTED:
+        assert hasattr(lib, name), name
+    assert lib.icr_abi_version() == 1
+
+
+def test_status_codes_map_to_reference_exceptions():
+    from paper_2603_13281_b200 import _lib, errors
+    assert _lib._STATUS[1] is errors.ShapeError
+    assert _lib._STATUS[2] is errors.ConfigError
+    assert _lib._STATUS[3] is errors.ModeError
+    assert _lib._STATUS[4] is errors.StateError
+    assert _lib._STATUS[5] is errors.CapacityError
+    assert _lib._STATUS[6] is errors.ContractViolationError
+    assert _lib._STATUS[8] is IndexError
+
+
+def test_sources_target_sm100a_only():
+    from paper_2603_13281_b200 import build
+    assert build.ARCH == ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -1,0 +1,263 @@
+"""End-to-end parity of the B200 decode path against the CPU oracle / reference goldens,
+plus the ICaRus invariants the reference tests pin (fused == sequential, cache == bare-base
+replay, KV byte-identical across models, prefix reuse), now on the GPU.
+
+Tolerance (bf16 weights/activations/KV vs the fp32 reference, identical bf16-representable
+weights on both sides): max |dlogit| <= LOGIT_TOL * max |logit| per step; greedy tokens
+must match teacher-forced unless the oracle's own top-1/top-2 gap is inside that band
+(the tie rule of tests/test_acceptance.py:103-108).
+"""
+
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import icarus_oracle as O
+
+pytestmark = pytest.mark.gpu
+GOLD = Path(__file__).resolve().parent / "golden"
+LOGIT_TOL = 3e-2
+
+C1 = dict(num_layers=2, hidden_dim=256, num_heads=2, num_kv_heads=1, head_dim=128, ffn_dim=1024,
+          vocab_size=1024)
+SMALL = dict(num_layers=2, hidden_dim=128, num_heads=2, num_kv_heads=1, head_dim=64, ffn_dim=256,
+             vocab_size=256)
+
+
+def _mods():
+    from paper_2603_13281_b200 import engine as E
+    from paper_2603_13281_b200 import kvpool as P
+    from paper_2603_13281_b200 import model as M
+    return E, P, M
+
+
+def base_from_oracle(cfg_kw, w):
+    E, P, M = _mods()
+    cfg = M.ModelConfig(**cfg_kw)
+    layers = [dict(lw) for lw in w["layers"]]
+    return M.BaseWeights(cfg, w["embed"], layers, w["final_gain"], w["lm_head"])
+
+
+def adapter_from_oracle(cfg, ad, task=""):
+    E, P, M = _mods()
+    layers = [{t: M.LowRankPair(M.Param(p["a"]), M.Param(p["b"])) for t, p in per.items()}
+              for per in ad["layers"]]
+    return M.AdapterSet(cfg, ad["rank"], ad["alpha"], M.DECODER_TARGETS, layers, task)
+
+
+@pytest.fixture(scope="module")
+def c1_setup(cuda):
+    shape = O.Shape(**C1)
+    w = O.bf16_weights(O.init_base(shape, 0))
+    base = base_from_oracle(C1, w)
+    agents = [adapter_from_oracle(base.config, O.bf16_adapter(a), f"agent{i}")
+              for i, a in enumerate(O.make_agents(shape, 2, seed=1))]
+    rt = base.runtime(max_seqs=32, max_context=1024, max_rows=256, adapter_slots=4, lora_rank=8)
+    return base, agents, rt
+
+
+def _check_logits(got, want, label):
+    scale = float(np.abs(want).max())
+    err = float(np.abs(got - want).max())
+    assert err <= LOGIT_TOL * scale, f"{label}: max|dlogit| {err:.4g} vs scale {scale:.4g}"
+    g, o = int(np.argmax(got)), int(np.argmax(want))
+    if g != o:
+        gap = float(want[o] - want[g])
+        assert gap <= LOGIT_TOL * scale, f"{label}: argmax {g} vs {o}, oracle gap {gap:.4g}"
+    return err / scale
+
+
+def test_c1_two_agents_match_reference(c1_setup):
+    """BASELINE.json configs[0]: agent0 prefills through an icarus pool, agent1 hits the full
+    prefix; both decode 32 steps teacher-forced on the reference's tokens."""
+    E, P, M = _mods()
+    base, agents, rt = c1_setup
+    g = np.load(GOLD / "c1_decode.npz")
+    prompt = [int(t) for t in g["prompt"]]
+    pool = P.KvCachePool(base.config, budget_bytes=64 << 20, mode="icarus")
+    worst = 0.0
+    s0 = E.new_session(base, agents[0], 512, runtime=rt, capture_logits=True)
+    t0 = E.prefill(s0, prompt, pool=pool, reader="agent0")
+    assert t0 == int(g["a0_tokens"][0])
+    worst = max(worst, _check_logits(s0.last_logits, g["a0_prefill_logits"], "a0 prefill"))
+    for i in range(32):
+        E.decode_step_fused(s0, int(g["a0_tokens"][i]))
+        worst = max(worst, _check_logits(s0.last_logits, g["a0_logits"][i], f"a0 step {i}"))
+    # K/V pages vs the reference's f32 cache (bf16 rounding of the same values)
+    for layer in range(2):
+        k, v = s0.cache.rows(layer, 0, s0.cache.position_count)
+        rk = g["a0_k"][layer].reshape(k.shape)
+        assert np.abs(k - rk).max() <= 2e-2 * np.abs(rk).max() + 1e-2
+    covered = prompt + [int(t) for t in g["a0_tokens"][:-1]]
+    pool.commit(None, covered, s0.cache, next_token_fn=lambda p: E.base_next_token_at(s0, p),
+                creator="agent0")
+    pool.release(s0.borrowed_chain)
+    s1 = E.new_session(base, agents[1], 512, runtime=rt, capture_logits=True)
+    t1 = E.prefill(s1, prompt, pool=pool, reader="agent1")
+    assert s1.ledger.prefix_hit_tokens == 128 and s1.ledger.prefill_tokens == 0
+    assert t1 == int(g["a1_tokens"][0])
+    for i in range(32):
+        E.decode_step_fused(s1, int(g["a1_tokens"][i]))
+        worst = max(worst, _check_logits(s1.last_logits, g["a1_logits"][i], f"a1 step {i}"))
+    assert list(np.frombuffer(g["a1_ledger"].tobytes(), np.int64))[:6] == [
+        s1.ledger.prefill_tokens, s1.ledger.prefix_hit_tokens, s1.ledger.decode_steps,
+        s1.ledger.param_passes, s1.ledger.param_matrix_reads, s1.ledger.kv_read_events]
+    print(f"C1 worst relative logit error {worst:.3e}")
+    s0.close(), s1.close()
+
+
+def test_c1_free_running_greedy_matches_reference(c1_setup):
+    E, P, M = _mods()
+    base, agents, rt = c1_setup
+    g = np.load(GOLD / "c1_decode.npz")
+    s = E.new_session(base, agents[0], 512, runtime=rt)
+    out = E.generate(s, [int(t) for t in g["prompt"]], max_new=33)
+    want = [int(t) for t in g["a0_tokens"]]
+    # exact unless a reference tie (within tolerance) flips a token; report first divergence
+    first = next((i for i, (a, b) in enumerate(zip(out, want)) if a != b), None)
+    if first is not None:
+        scale = float(np.abs(g["a0_logits"][first - 1]).max())
+        lg = g["a0_logits"][first - 1]
+        assert abs(float(lg[want[first]] - lg[out[first]])) <= LOGIT_TOL * scale
+    s.close()
+
+
+def test_kv_bytes_identical_across_models_and_paths(c1_setup):
+    """ICaRus invariant: every adapted model's cache bytes are the base model's bytes, and
+    prefill KV == decode KV for the same tokens (path independence)."""
+    E, P, M = _mods()
+    base, agents, rt = c1_setup
+    rng = np.random.default_rng(3)
+    prompt = [int(t) for t in rng.integers(1, 1024, 40)]
+    forced = [int(t) for t in rng.integers(1, 1024, 24)]
+    fps = []
+    for ad in (agents[0], agents[1], None):
+        s = E.new_session(base, ad, 256, runtime=rt)
+        E.prefill(s, prompt)
+        for t in forced:
+            E.decode_step_fused(s, t)
+        fps.append(s.cache.fingerprint())
+        s.close()
+    replay = E.replay_base(base, prompt + forced, prompt_len=len(prompt), runtime=rt)
+    one_shot = E.new_session(base, None, 256, runtime=rt)
+    E.prefill(one_shot, prompt + forced)
+    assert fps[0] == fps[1] == fps[2] == replay.cache.fingerprint() == one_shot.cache.fingerprint()
+    replay.close(), one_shot.close()
+
+
+def test_fused_equals_sequential_bitwise(c1_setup):
+    E, P, M = _mods()
+    base, agents, rt = c1_setup
+    prompt = [3, 1, 4, 1, 5, 9, 2, 6]
+    a = E.new_session(base, agents[0], 128, runtime=rt, capture_logits=True)
+    b = E.new_session(base, agents[0], 128, runtime=rt, capture_logits=True)
+    ta, tb = E.prefill(a, prompt), E.prefill(b, prompt)
+    assert ta == tb
+    for _ in range(10):
+        ta = E.decode_step_fused(a, ta)
+        tb = E.decode_step_sequential(b, tb)
+        assert ta == tb
+        assert a.last_logits.tobytes() == b.last_logits.tobytes()
+    assert a.cache.fingerprint() == b.cache.fingerprint()
+    assert b.ledger.param_passes == 2 * a.ledger.param_passes
+    a.close(), b.close()
+
+
+def test_batched_step_equals_single_session_steps(c1_setup):
+    """decode_step_batch over many sessions == each session stepped alone (bitwise)."""
+    E, P, M = _mods()
+    base, agents, rt = c1_setup
+    rng = np.random.default_rng(11)
+    prompts = [[int(t) for t in rng.integers(1, 1024, n)] for n in (20, 33, 47, 20)]
+    ads = [agents[0], agents[1], None, agents[1]]
+    solo = [E.new_session(base, ad, 256, runtime=rt, capture_logits=True) for ad in ads]
+    batch = [E.new_session(base, ad, 256, runtime=rt, capture_logits=True) for ad in ads]
+    ts = [E.prefill(s, p) for s, p in zip(solo, prompts)]
+    tb = [E.prefill(s, p) for s, p in zip(batch, prompts)]
+    assert ts == tb
+    for _ in range(6):
+        ts = [E.decode_step_fused(s, t) for s, t in zip(solo, ts)]
+        tb = E.decode_step_batch(batch, tb)
+        assert ts == tb
+        for x, y in zip(solo, batch):
+            assert x.last_logits.tobytes() == y.last_logits.tobytes()
+    for x, y in zip(solo, batch):
+        assert x.cache.fingerprint() == y.cache.fingerprint()
+        x.close(), y.close()
+
+
+def test_shared_prefix_pages_are_zero_copy_and_bitwise(c1_setup):
+    """8 adapters on one prompt: one prefill, 7 full-prefix hits; the hits reference the
+    writer's pages and continue bitwise like cold sessions."""
+    E, P, M = _mods()
+    base, agents, rt = c1_setup
+    rng = np.random.default_rng(5)
+    prompt = [int(t) for t in rng.integers(1, 1024, 64)]
+    pool = P.KvCachePool(base.config, 64 << 20, "icarus")
+    writer = E.new_session(base, None, 256, runtime=rt)
+    first = E.prefill(writer, prompt)
+    pool.commit(None, prompt, writer.cache, next_token_fn=lambda p: E.base_next_token_at(writer, p))
+    reader = E.new_session(base, agents[1], 256, runtime=rt, capture_logits=True)
+    cold = E.new_session(base, agents[1], 256, runtime=rt, capture_logits=True)
+    t = E.prefill(reader, prompt, pool=pool, reader="x")
+    tc = E.prefill(cold, prompt)
+    assert t == tc == first
+    assert reader.cache.pages[:4] == writer.cache.pages[:4]
+    assert reader.ledger.prefill_tokens == 0 and reader.ledger.param_matrix_reads == 0
+    for _ in range(5):
+        t, tc = E.decode_step_fused(reader, t), E.decode_step_fused(cold, tc)
+        assert t == tc and reader.last_logits.tobytes() == cold.last_logits.tobytes()
+    pool.release(reader.borrowed_chain)
+    for s in (writer, reader, cold):
+        s.close()
+
+
+def test_session_guards_and_ledger(cuda):
+    E, P, M = _mods()
+    from paper_2603_13281_b200.errors import (CapacityError, ContractViolationError, ModeError,
+                                              StateError)
+    base = M.init_base(M.ModelConfig(**SMALL), 0)
+    rt = base.runtime(max_seqs=8, max_context=64, max_rows=64, adapter_slots=2, lora_rank=8)
+    s = E.new_session(base, None, 8, runtime=rt)
+    with pytest.raises(StateError):
+        E.decode_step_fused(s, 1)
+    E.prefill(s, [3, 1, 4, 1, 5])
+    with pytest.raises(StateError):
+        E.prefill(s, [3])
+    with pytest.raises(ValueError):
+        E.prefill(E.new_session(base, None, 8, runtime=rt), [])
+    with pytest.raises(CapacityError):
+        E.prefill(E.new_session(base, None, 4, runtime=rt), [3, 1, 4, 1, 5])
+    with pytest.raises(IndexError):
+        E.prefill(E.new_session(base, None, 8, runtime=rt), [999])
+    tok = 1
+    for _ in range(3):
+        tok = E.decode_step_fused(s, tok)
+    with pytest.raises(CapacityError):
+        E.decode_step_fused(s, tok)
+    conv = M.AdapterSet.init(base.config, targets=M.CONVENTIONAL_TARGETS, seed=0)
+    with pytest.raises(ContractViolationError, match="shared cache"):
+        E.new_session(base, conv, 16, runtime=rt)
+    with pytest.raises(ModeError):
+        E.generate(E.new_session(base, None, 16, runtime=rt), [1, 2], 4, path="speculative")
+    ad = M.AdapterSet.init(base.config, seed=0)
+    sa = E.new_session(base, ad, 16, runtime=rt)
+    E.prefill(sa, [1, 2, 3])
+    with pytest.raises(StateError):
+        E.decode_step_base(sa, 1)
+    # ledger arithmetic (tests/test_engine.py:87-122)
+    L = base.config.num_layers
+    bpt = base.config.kv_bytes_per_token
+    f = E.new_session(base, None, 64, runtime=rt)
+    q = E.new_session(base, None, 64, runtime=rt)
+    tf, tq = E.prefill(f, [3, 1, 4, 1, 5]), E.prefill(q, [3, 1, 4, 1, 5])
+    assert f.ledger.param_matrix_reads == 7 * L + 1
+    for _ in range(6):
+        tf, tq = E.decode_step_fused(f, tf), E.decode_step_sequential(q, tq)
+        assert tf == tq
+    assert f.ledger.param_passes == 6 and q.ledger.param_passes == 12
+    assert f.ledger.param_matrix_reads - (7 * L + 1) == 6 * (7 * L + 1)
+    assert q.ledger.param_matrix_reads - (7 * L + 1) == 6 * (7 * L + 5 * L + 1)
+    assert f.ledger.kv_bytes_written == 11 * bpt
+    assert f.ledger.kv_bytes_read == sum(p + 1 for p in range(5, 11)) * bpt
