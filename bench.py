@@ -257,7 +257,10 @@ def run_b200(args) -> None:
     # ---------------- roofline of the dominant kernel (gate|up GEMM) ----------------
     import ctypes as C
     avg = C.c_float()
-    _lib.check(rt._lib.icr_profile_gemm(rt._handle, 1, 2, C.byref(avg), _lib.stream_handle()))
+    per_kind = {}
+    for which, name in ((0, "o"), (2, "down"), (3, "lm_head"), (1, "gate_up")):
+        _lib.check(rt._lib.icr_profile_gemm(rt._handle, which, 2, C.byref(avg), _lib.stream_handle()))
+        per_kind[name] = round(avg.value * 1e3, 2)
     rows = 2 * n
     gu_bytes = (2 * cfg.ffn_dim * cfg.hidden_dim * 2 + rows * cfg.hidden_dim * 2
                 + rows * cfg.ffn_dim * 2 + N_ADAPTERS * 2 * cfg.ffn_dim * RANK * 2)
@@ -299,7 +302,8 @@ def run_b200(args) -> None:
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "avg_launch_ms": avg.value,
                      "algorithmic_bytes_per_launch": gu_bytes,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650"},
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",
+                     "gemm_launch_us": per_kind},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         res = cpu_baseline_sample(1, 2, 0)

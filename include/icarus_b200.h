@@ -70,7 +70,10 @@ typedef struct icr_model_config {
  *   b_gu   [slots][2*ffn][r]      gate/up rows interleaved like w_gu
  *   b_down [slots][d][r]
  * KV pages (this layer): k_pages, v_pages [num_pages][num_kv_heads][16][head_dim].
- * All bf16. The reference has no slot for k/v adapters: there is none here either. */
+ * All bf16. The four projection matrices and lm_head are stored TILE-MAJOR: the [M, K]
+ * matrix above is laid out as [M/128][K/64][128][64] so every 128x64 GEMM tile is one
+ * contiguous 16 KB block (runtime.py: tile_major). The reference has no slot for k/v
+ * adapters: there is none here either. */
 typedef struct icr_layer_weights {
   const void* w_qkv;
   const void* w_o;
@@ -91,7 +94,8 @@ typedef struct icr_layer_weights {
 
 /* Replaces BaseWeights/AdapterSet residency (model.py:88-256): binds device weights,
  * builds TMA descriptors, allocates scratch sized by cfg->max_rows.
- * embed [vocab, d] bf16; lm_head [vocab, d] bf16 (final_gain folded). lora_scaling is
+ * embed [vocab, d] bf16; lm_head [ceil(vocab/128)*128, d] bf16 tile-major, final_gain folded,
+ * zero rows past vocab. lora_scaling is
  * AdapterSet.scaling = alpha / rank (model.py:220-222), identical for all slots. */
 icr_status icr_model_create(const icr_model_config* cfg, const icr_layer_weights* layers,
                             const void* embed, const void* lm_head, float lora_scaling,
@@ -140,6 +144,13 @@ icr_status icr_model_stats(icr_model* m, int64_t* out3);
 /* Average device time of one projection-GEMM launch (which: 0 wo, 1 gate|up, 2 down,
  * 3 lm_head) re-run `iters` times over all layers with the last forward's rows. */
 icr_status icr_profile_gemm(icr_model* m, int which, int iters, float* avg_ms, void* stream);
+
+/* Weight-streaming GEMM micro-benchmark (tuning): cycles n_mats matrices [n_mats][M][K]
+ * (tile-major if blocked) against `rows` token rows; stages / ctas_per_sm / skip_mma
+ * override the ring depth, CTAs per SM and bypass tcgen05.mma (0 = defaults). */
+icr_status icr_bench_gemm(const void* w, const void* x, int M, int K, int rows, int n_mats,
+                          int blocked, int stages, int ctas_per_sm, int skip_mma, int iters,
+                          float* avg_ms, void* stream);
 
 /* --- building blocks, exported for parity tests -------------------------------- */
 

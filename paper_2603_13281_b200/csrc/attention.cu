@@ -1,7 +1,7 @@
 // Shared-KV paged decode attention (reference: `layer_attention`, src/model.py:384-425,
 // with the fused 2H query heads of `block_forward` decode, src/model.py:495-501).
 //
-// Work decomposition (built on the host by attn_plan.cpp):
+// Work decomposition (built on the host by runtime.cu build_attn_plan):
 //   * each sequence's keys are cut into fixed chunks of CHUNK_PAGES pages at ABSOLUTE
 //     positions [c*CHUNK, (c+1)*CHUNK);
 //   * sequences whose chunk c maps to the SAME physical pages (a cross-model shared
@@ -9,8 +9,7 @@
 //     memory once and reused by the encoder and every adapter's decoder queries;
 //   * a work item x one KV head = one CTA; up to 64 query rows (4 warps x 16).
 // Per (row, head, chunk) the kernel emits an unnormalised partial (o, m, l); the merge
-// kernel folds chunks 0..last in fixed order. Partials depend only on the row's own
-// query, the chunk's keys and the row's position, never on which other rows share the
+// kernel folds chunks 0..last in fixed order. Partials depend only on the row's own query, the chunk's keys and the row's position, never on which other rows share the
 // CTA -- the batch-invariance the reference gets from its per-head loop (2H == H||H,
 // tests/test_model.py:225-239) and that makes prefill / decode KV bytes identical.
 #include "kernels.h"
@@ -60,6 +59,11 @@ __device__ __forceinline__ uint32_t swz(int row, int chunk) {
   return (uint32_t)(row * HD * 2 + ((chunk ^ (row & 7)) << 4));
 }
 
+constexpr int PAGE_STAGES = 6;  // K/V pages in flight per CTA
+
+template <int HD>
+constexpr size_t attn_smem() { return (size_t)64 * HD * 2 + (size_t)PAGE_STAGES * 2 * 16 * HD * 2; }
+
 template <int HD>
 __global__ void __launch_bounds__(128)
     attn_partial_kernel(const __nv_bfloat16* __restrict__ q, int q_ld,
@@ -70,15 +74,36 @@ __global__ void __launch_bounds__(128)
                         int num_heads, int max_chunks, float scale, float* __restrict__ part_o,
                         float2* __restrict__ part_ml, const int* __restrict__ n_items_dev) {
   constexpr int CH = HD / 8;  // 16-byte chunks per row
-  __shared__ __align__(128) __nv_bfloat16 sQ[64 * HD];
-  __shared__ __align__(128) __nv_bfloat16 sK[2][16 * HD];
-  __shared__ __align__(128) __nv_bfloat16 sV[2][16 * HD];
+  extern __shared__ __align__(128) uint8_t attn_smem_raw[];
+  __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(attn_smem_raw);
+  __nv_bfloat16* sKV = sQ + 64 * HD;  // [stage][K | V][16][HD]
 
+  pdl_launch();
   const int item_id = blockIdx.x;
   if (item_id >= *n_items_dev) return;
+  pdl_wait();
   const AttnItem it = items[item_id];
   const int g = blockIdx.y;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  auto load_page = [&](int pi, int buf) {
+    const int page = item_pages[it.page_off + pi];
+    const size_t off = ((size_t)page * num_kv_heads + g) * 16 * HD;
+    const uint8_t* ks = reinterpret_cast<const uint8_t*>(k_pages + off);
+    const uint8_t* vs = reinterpret_cast<const uint8_t*>(v_pages + off);
+    const uint32_t kd = smem_u32(sKV + (size_t)buf * 32 * HD), vd = kd + 16 * HD * 2;
+    for (int idx = tid; idx < 16 * CH; idx += 128) {
+      const int row = idx / CH, ch = idx % CH;
+      cp_async16(kd + swz<HD>(row, ch), ks + idx * 16);
+      cp_async16(vd + swz<HD>(row, ch), vs + idx * 16);
+    }
+  };
+  // K/V ring prologue: pages 0 .. PAGE_STAGES-2 in flight before touching Q
+#pragma unroll
+  for (int s = 0; s < PAGE_STAGES - 1; ++s) {
+    if (s < it.n_pages) load_page(s, s);
+    cp_async_commit();
+  }
 
   // ---- stage Q rows (swizzled) ----
   for (int idx = tid; idx < 64 * CH; idx += 128) {
@@ -91,22 +116,6 @@ __global__ void __launch_bounds__(128)
     }
     *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sQ) + swz<HD>(row, ch)) = val;
   }
-
-  auto load_page = [&](int pi, int buf) {
-    const int page = item_pages[it.page_off + pi];
-    const size_t off = ((size_t)page * num_kv_heads + g) * 16 * HD;
-    const uint8_t* ks = reinterpret_cast<const uint8_t*>(k_pages + off);
-    const uint8_t* vs = reinterpret_cast<const uint8_t*>(v_pages + off);
-    const uint32_t kd = smem_u32(sK[buf]), vd = smem_u32(sV[buf]);
-    for (int idx = tid; idx < 16 * CH; idx += 128) {
-      const int row = idx / CH, ch = idx % CH;
-      cp_async16(kd + swz<HD>(row, ch), ks + idx * 16);
-      cp_async16(vd + swz<HD>(row, ch), vs + idx * 16);
-    }
-    cp_async_commit();
-  };
-
-  load_page(0, 0);
   __syncthreads();
 
   // ---- per-warp query fragments ----
@@ -132,18 +141,18 @@ __global__ void __launch_bounds__(128)
   float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;
 
   for (int pi = 0; pi < it.n_pages; ++pi) {
-    const int buf = pi & 1;
-    if (pi + 1 < it.n_pages) {
-      load_page(pi + 1, buf ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
+    const int buf = pi % PAGE_STAGES;
+    {
+      const int nxt = pi + PAGE_STAGES - 1;
+      if (nxt < it.n_pages) load_page(nxt, nxt % PAGE_STAGES);
+      cp_async_commit();
     }
+    cp_async_wait<PAGE_STAGES - 1>();
     __syncthreads();
 
     // S = Q K^T for 16 keys (two n8 tiles)
     float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-    const uint32_t kbase = smem_u32(sK[buf]);
+    const uint32_t kbase = smem_u32(sKV + (size_t)buf * 32 * HD);
 #pragma unroll
     for (int kk = 0; kk < HD / 16; ++kk) {
       // x4: matrices (keys0-7, dims lo), (keys0-7, dims hi), (keys8-15, lo), (keys8-15, hi)
@@ -210,7 +219,7 @@ __global__ void __launch_bounds__(128)
     pa[1] = pack_bf16(s[0][2], s[0][3]);
     pa[2] = pack_bf16(s[1][0], s[1][1]);
     pa[3] = pack_bf16(s[1][2], s[1][3]);
-    const uint32_t vbase = smem_u32(sV[buf]);
+    const uint32_t vbase = kbase + 16 * HD * 2;
 #pragma unroll
     for (int dt = 0; dt < HD / 16; ++dt) {
       // x4.trans: (keys0-7, dims d0..d0+7), (keys8-15, d0..), (keys0-7, d0+8..), (keys8-15, d0+8..)
@@ -245,61 +254,62 @@ __global__ void __launch_bounds__(128)
   }
 }
 
-// Fixed-order merge of chunk partials; one CTA per (row, head), one thread per dim.
+// Fixed-order merge of chunk partials: one CTA per (row, KV group), one thread per
+// (head-in-group, dim). Chunks 0..last are folded in index order, so the result is
+// independent of how the chunks were grouped into work items.
 template <int HD>
-__global__ void __launch_bounds__(HD)
+__global__ void __launch_bounds__(256)
     attn_merge_kernel(const float* __restrict__ part_o, const float2* __restrict__ part_ml,
                       const int* __restrict__ row_pos, const int* __restrict__ row_kind,
-                      int num_heads, int max_chunks, int chunk_tokens, __nv_bfloat16* __restrict__ out,
-                      int out_ld) {
-  const int rh = blockIdx.x;
-  const int r = rh / num_heads, h = rh % num_heads;
-  const int d = threadIdx.x;
-  __nv_bfloat16* dst = out + (size_t)r * out_ld + h * HD + d;
-  if (row_kind[r] < 0) { *dst = __float2bfloat16_rn(0.f); return; }
+                      int num_heads, int group, int max_chunks, int chunk_tokens,
+                      __nv_bfloat16* __restrict__ out, int out_ld) {
+  pdl_launch();
+  pdl_wait();
+  const int r = blockIdx.x, g = blockIdx.y;
+  if (row_kind[r] < 0) return;
   const int nch = row_pos[r] / chunk_tokens + 1;
-  const size_t base = ((size_t)r * num_heads + h) * max_chunks;
-  float M = -INFINITY;
-  for (int c = 0; c < nch; ++c) M = fmaxf(M, part_ml[base + c].x);
-  float L = 0.f, O = 0.f;
-  for (int c = 0; c < nch; ++c) {
-    const float2 ml = part_ml[base + c];
-    const float w = expf(ml.x - M);
-    L = fmaf(ml.y, w, L);
-    O = fmaf(part_o[(base + c) * HD + d], w, O);
+  for (int idx = threadIdx.x; idx < group * HD; idx += blockDim.x) {
+    const int head = g * group + idx / HD, d = idx % HD;
+    const size_t base = ((size_t)r * num_heads + head) * max_chunks;
+    float M = -INFINITY;
+    for (int c = 0; c < nch; ++c) M = fmaxf(M, part_ml[base + c].x);
+    float L = 0.f, O = 0.f;
+    for (int c = 0; c < nch; ++c) {
+      const float2 ml = part_ml[base + c];
+      const float w = expf(ml.x - M);
+      L = fmaf(ml.y, w, L);
+      O = fmaf(part_o[(base + c) * HD + d], w, O);
+    }
+    out[(size_t)r * out_ld + head * HD + d] = __float2bfloat16_rn(__fdiv_rn(O, L));
   }
-  *dst = __float2bfloat16_rn(__fdiv_rn(O, L));
+}
+
+template <int HD>
+static cudaError_t attn_launch_hd(const AttnLaunch& a, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_partial_kernel<HD>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)attn_smem<HD>());
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid(a.n_items_cap, a.num_kv_heads);
+  cudaError_t e = launch_pdl(attn_partial_kernel<HD>, grid, dim3(128), attn_smem<HD>(), s, a.q,
+                             a.q_ld, a.k_pages, a.v_pages, a.num_kv_heads, a.group, a.items,
+                             a.item_pages, a.item_rows, a.row_pos, a.num_heads, a.max_chunks,
+                             a.scale, a.part_o, a.part_ml, a.n_items_dev);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(attn_merge_kernel<HD>, dim3(a.n_rows, a.num_kv_heads), dim3(256), 0, s,
+                    a.part_o, a.part_ml, a.row_pos, a.row_kind, a.num_heads, a.group,
+                    a.max_chunks, a.chunk_tokens, a.out, a.out_ld);
 }
 
 cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t s) {
-  if (a.n_items_cap > 0) {
-    dim3 grid(a.n_items_cap, a.num_kv_heads);
-    if (a.head_dim == 128)
-      attn_partial_kernel<128><<<grid, 128, 0, s>>>(
-          a.q, a.q_ld, a.k_pages, a.v_pages, a.num_kv_heads, a.group, a.items, a.item_pages,
-          a.item_rows, a.row_pos, a.num_heads, a.max_chunks, a.scale, a.part_o, a.part_ml,
-          a.n_items_dev);
-    else if (a.head_dim == 64)
-      attn_partial_kernel<64><<<grid, 128, 0, s>>>(
-          a.q, a.q_ld, a.k_pages, a.v_pages, a.num_kv_heads, a.group, a.items, a.item_pages,
-          a.item_rows, a.row_pos, a.num_heads, a.max_chunks, a.scale, a.part_o, a.part_ml,
-          a.n_items_dev);
-    else
-      return cudaErrorInvalidValue;
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-  }
-  if (a.n_rows > 0) {
-    if (a.head_dim == 128)
-      attn_merge_kernel<128><<<a.n_rows * a.num_heads, 128, 0, s>>>(
-          a.part_o, a.part_ml, a.row_pos, a.row_kind, a.num_heads, a.max_chunks, a.chunk_tokens,
-          a.out, a.out_ld);
-    else
-      attn_merge_kernel<64><<<a.n_rows * a.num_heads, 64, 0, s>>>(
-          a.part_o, a.part_ml, a.row_pos, a.row_kind, a.num_heads, a.max_chunks, a.chunk_tokens,
-          a.out, a.out_ld);
-  }
-  return cudaGetLastError();
+  if (a.n_items_cap <= 0) return cudaSuccess;
+  if (a.head_dim == 128) return attn_launch_hd<128>(a, s);
+  if (a.head_dim == 64) return attn_launch_hd<64>(a, s);
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace icr

@@ -8,16 +8,22 @@ namespace icr {
 constexpr int BM = 128;  // MMA M (weight rows per tile)
 constexpr int BK = 64;   // K elements per stage (one 128-byte swizzle row)
 constexpr uint32_t W_BYTES = BM * BK * 2;
+constexpr int MAX_RANK = 32;
+// barriers, reduction scratch, staged row metadata and the LoRA U rows of the launch
+template <int NT>
+constexpr size_t aux_smem() {
+  return 2048 + (size_t)NT * 5 * 4 + (NT <= 64 ? (size_t)NT * 2 * 32 * 4 : 0);
+}
 
 template <int NT>
 struct Cfg {
   static constexpr uint32_t X_BYTES = NT * BK * 2;
   static constexpr uint32_t STAGE = W_BYTES + X_BYTES;
-  static constexpr int STAGES_RAW = (200 * 1024) / STAGE;
+  static constexpr int STAGES_RAW = (int)((220 * 1024 - aux_smem<NT>()) / STAGE);
   static constexpr int STAGES = STAGES_RAW > 16 ? 16 : STAGES_RAW;
   static constexpr uint32_t TMEM_COLS = NT < 32 ? 32 : NT;
   static constexpr uint32_t IDESC = idesc_bf16_f32(BM, NT);
-  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE + 512;
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE + aux_smem<NT>();
 };
 
 struct Split {
@@ -28,6 +34,14 @@ struct Split {
   __device__ __host__ int owner(long long x) const { return (int)(((x + 1) * G - 1) / U); }
 };
 
+// Per-CTA shared state of the epilogue warps.
+struct EpiShared {
+  int flag;
+  int shrink_ready;
+  float red_val[64];
+  int red_idx[64];
+};
+
 __device__ __forceinline__ float silu_ref(float g) {
   // Sign-split logistic as in src/tensor.py:199-214 (_sigmoid, silu).
   float z = expf(-fabsf(g));
@@ -35,33 +49,93 @@ __device__ __forceinline__ float silu_ref(float g) {
   return __fmul_rn(g, sig);
 }
 
+__device__ __forceinline__ void unpack8(const uint4& raw, float (&f)[8]) {
+  const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float2 t = __bfloat1622float2(h2[q]);
+    f[2 * q] = t.x;
+    f[2 * q + 1] = t.y;
+  }
+}
+
+// Row metadata staged in smem by the epilogue warps (after griddepcontrol.wait).
+struct RowMeta {
+  int* kind;
+  int* ad;
+  int* pos;
+  int* kvoff;
+  float* inv;
+  float* u;  // [NT][n_u][rank] LoRA U of this launch's rows (NT <= 64)
+};
+
 template <int NT>
 __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0, float (&v)[16],
-                                           int ep_t, float* red_val, int* red_idx) {
+                                           int ep_t, EpiShared& sh, const RowMeta& rm) {
   const int m = tile * BM + ep_t;
+  // ---- RMSNorm of the input rows (X was the raw residual stream) ----
+  if (p.in_ssq != nullptr) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = __fmul_rn(v[j], rm.inv[n0 + j]);
+  }
   // ---- LoRA expand on decoder rows (segmented by adapter slot) ----
-  if (p.lora_b != nullptr && m < p.lora_m) {
-    const int uidx = (p.mode == EPI_SILU) ? (m & 1) : 0;
+  if (p.lora_b != nullptr) {
+    if (!sh.shrink_ready) {  // uniform across the 128 epilogue threads
+      if (p.sh_x != nullptr && ep_t == 0) {
+        const int target = gridDim.x * 2;
+        while (ld_acquire(p.sync) < target) __nanosleep(32);
+      }
+      named_bar_sync(1, 128);
+      // stage U of this launch's decoder rows in smem (broadcast reads in the expand)
+      const int per_row = p.n_u * p.rank;
+      for (int idx = ep_t; rm.u != nullptr && idx < NT * per_row; idx += 128) {
+        const int n = idx / per_row;
+        rm.u[idx] = (n < p.n_rows && rm.kind[n] == 1 && rm.ad[n] >= 0)
+                        ? __ldcg(p.lora_u + (size_t)(p.row0 + n) * per_row + idx % per_row)
+                        : 0.f;
+      }
+      if (ep_t == 0) sh.shrink_ready = 1;
+      named_bar_sync(1, 128);
+    }
+    if (m < p.lora_m) {
+      const int uidx = (p.mode == EPI_SILU) ? (m & 1) : 0;
+      const int nch = p.rank >> 3;
+      const int per_row = p.n_u * p.rank;
+      // issue 8 columns' B loads before using any (one memory round trip per batch)
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int n = n0 + j;
-      if (n >= p.n_rows || p.row_kind[n] != 1) continue;
-      const int a = p.row_adapter[n];
-      if (a < 0) continue;  // base decoder row (read-only replay): no adapter
-      const __nv_bfloat16* b = p.lora_b + ((size_t)a * p.lora_m + m) * p.rank;
-      const float* u = p.lora_u + ((size_t)n * p.n_u + uidx) * p.rank;
-      float acc = 0.f;
-      for (int r = 0; r < p.rank; r += 8) {
-        uint4 raw = *reinterpret_cast<const uint4*>(b + r);
-        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+      for (int jb = 0; jb < 16; jb += 8) {
+        for (int cb = 0; cb < nch; cb += 2) {
+          uint4 braw[8][2];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          float2 f = __bfloat1622float2(h2[q]);
-          acc = fmaf(u[r + 2 * q], f.x, acc);
-          acc = fmaf(u[r + 2 * q + 1], f.y, acc);
+          for (int q = 0; q < 8; ++q) {
+            const int n = n0 + jb + q;
+            if (n < p.n_rows && rm.kind[n] == 1 && rm.ad[n] >= 0) {
+              const uint4* b = reinterpret_cast<const uint4*>(
+                  p.lora_b + ((size_t)rm.ad[n] * p.lora_m + m) * p.rank) + cb;
+              braw[q][0] = __ldg(b);
+              braw[q][1] = (cb + 1 < nch) ? __ldg(b + 1) : make_uint4(0, 0, 0, 0);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int n = n0 + jb + q;
+            if (!(n < p.n_rows && rm.kind[n] == 1 && rm.ad[n] >= 0)) continue;
+            const float* u = (rm.u != nullptr
+                                  ? rm.u + (size_t)n * per_row
+                                  : p.lora_u + (size_t)(p.row0 + n) * per_row) +
+                             uidx * p.rank + cb * 8;
+            float acc = 0.f;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              float bf[8];
+              unpack8(braw[q][c], bf);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) acc = fmaf(u[c * 8 + e], bf[e], acc);
+            }
+            v[jb + q] += acc;
+          }
         }
       }
-      v[j] += acc;
     }
   }
 
@@ -70,27 +144,45 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int n = n0 + j;
-        if (n < p.n_rows) p.out_f32[(size_t)n * p.ld_out + m] = v[j];
+        if (n < p.n_rows) p.out_f32[(size_t)(p.row0 + n) * p.ld_out + m] = v[j];
       }
     } break;
     case EPI_RESID: {
+      const int wq = ep_t >> 5, ln = ep_t & 31;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int n = n0 + j;
-        if (n < p.n_rows && p.row_kind[n] >= 0) {
-          float* r = p.resid + (size_t)n * p.M + m;
-          *r = __fadd_rn(*r, v[j]);
+        float sq = 0.f;
+        if (n < p.n_rows && rm.kind[n] >= 0) {
+          const size_t idx = (size_t)(p.row0 + n) * p.M + m;
+          const float xn = __fadd_rn(p.resid[idx], v[j]);
+          p.resid[idx] = xn;
+          p.resid_bf16[idx] = __float2bfloat16_rn(xn);
+          sq = __fmul_rn(xn, xn);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        if (ln == 0) sh.red_val[wq * 16 + j] = sq;
+      }
+      named_bar_sync(1, 128);
+      if (ep_t < 16) {
+        const int n = n0 + ep_t;
+        if (n < p.n_rows) {
+          const float s = ((sh.red_val[ep_t] + sh.red_val[16 + ep_t]) + sh.red_val[32 + ep_t]) +
+                          sh.red_val[48 + ep_t];
+          p.out_ssq[(size_t)tile * p.ss_stride + p.row0 + n] = s;
         }
       }
+      named_bar_sync(1, 128);
     } break;
     case EPI_SILU: {
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const float partner = __shfl_xor_sync(0xffffffffu, v[j], 1);
         const int n = n0 + j;
-        if ((m & 1) == 0 && n < p.n_rows && p.row_kind[n] >= 0) {
+        if ((m & 1) == 0 && n < p.n_rows && rm.kind[n] >= 0) {
           const float f = __fmul_rn(silu_ref(v[j]), partner);
-          p.out_bf16[(size_t)n * (p.M >> 1) + (m >> 1)] = __float2bfloat16_rn(f);
+          p.out_bf16[(size_t)(p.row0 + n) * (p.M >> 1) + (m >> 1)] = __float2bfloat16_rn(f);
         }
       }
     } break;
@@ -100,32 +192,27 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
       const int base = region == 0 ? 0 : (region == 1 ? p.q_dim : p.q_dim + p.kv_dim);
       const int i = (m - base) % hd;
       const int head = (m - base) / hd;
+      __nv_bfloat16* pages = region == 1 ? p.k_pages : p.v_pages;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const float partner = __shfl_xor_sync(0xffffffffu, v[j], 1);
         const int n = n0 + j;
-        if (n >= p.n_rows) continue;
-        const int kind = p.row_kind[n];
+        const int kind = n < p.n_rows ? rm.kind[n] : -1;
         if (kind < 0) continue;
-        const int pos = p.row_pos[n];
         float out = v[j];
         if (region < 2) {
           // Interleaved-pair RoPE, src/tensor.py:309-315.
-          const float2 cs = p.rope[(size_t)pos * (hd >> 1) + (i >> 1)];
+          const float2 cs = p.rope[(size_t)rm.pos[n] * (hd >> 1) + (i >> 1)];
           if ((i & 1) == 0)
             out = __fsub_rn(__fmul_rn(v[j], cs.x), __fmul_rn(partner, cs.y));
           else
             out = __fadd_rn(__fmul_rn(partner, cs.y), __fmul_rn(v[j], cs.x));
         }
         if (region == 0) {
-          p.out_bf16[(size_t)n * p.q_dim + m] = __float2bfloat16_rn(out);
+          p.out_bf16[(size_t)(p.row0 + n) * p.q_dim + m] = __float2bfloat16_rn(out);
         } else if (kind == 0) {
           // Encoder rows only: K/V for position pos into its page (src/model.py:486-494).
-          const int seq = p.row_seq[n];
-          const int page = p.block_table[(size_t)seq * p.bt_stride + (pos >> 4)];
-          __nv_bfloat16* dst = (region == 1 ? p.k_pages : p.v_pages) +
-                               (((size_t)page * p.num_kv_heads + head) * 16 + (pos & 15)) * hd + i;
-          *dst = __float2bfloat16_rn(out);
+          pages[(size_t)rm.kvoff[n] + (size_t)head * 16 * hd + i] = __float2bfloat16_rn(out);
         }
       }
     } break;
@@ -142,25 +229,103 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
           const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
           if (ov > val || (ov == val && oi < idx)) { val = ov; idx = oi; }
         }
-        if (ln == 0) { red_val[wq * 16 + j] = val; red_idx[wq * 16 + j] = idx; }
+        if (ln == 0) { sh.red_val[wq * 16 + j] = val; sh.red_idx[wq * 16 + j] = idx; }
       }
       named_bar_sync(1, 128);
       if (ep_t < 16) {
-        float val = red_val[ep_t];
-        int idx = red_idx[ep_t];
+        float val = sh.red_val[ep_t];
+        int idx = sh.red_idx[ep_t];
         for (int w = 1; w < 4; ++w) {
-          const float ov = red_val[w * 16 + ep_t];
-          const int oi = red_idx[w * 16 + ep_t];
+          const float ov = sh.red_val[w * 16 + ep_t];
+          const int oi = sh.red_idx[w * 16 + ep_t];
           if (ov > val || (ov == val && oi < idx)) { val = ov; idx = oi; }
         }
         const int n = n0 + ep_t;
         if (n < p.n_rows)
-          p.tile_best[(size_t)tile * p.best_stride + n] = make_float2(val, __int_as_float(idx));
+          p.tile_best[(size_t)tile * p.best_stride + p.row0 + n] =
+              make_float2(val, __int_as_float(idx));
       }
       named_bar_sync(1, 128);
     } break;
     default:
       break;
+  }
+}
+
+// In-kernel LoRA shrink by the epilogue warps of all CTAs. A task is one adapter row
+// (target t, slot a, rank index j) over one K slice of <= SHRINK_SLICE elements; all of
+// a lane's loads for the slice are issued before use (one memory round trip). The warp
+// that delivers a row's last slice folds the partials in slice order (deterministic).
+constexpr int SHRINK_SLICE = 2048;  // 8 x (32 lanes x 8 bf16)
+__device__ __forceinline__ void lora_shrink_tasks(const GemmParams& p, const RowMeta& rm,
+                                                  int gwarp, int nwarps, int lane) {
+  const int per_t = p.slots * p.rank;
+  const int splits = (p.sh_K + SHRINK_SLICE - 1) / SHRINK_SLICE;
+  const int tasks = p.sh_targets * per_t * splits;
+  for (int task = gwarp; task < tasks; task += nwarps) {
+    const int ks = task % splits, combo = task / splits;
+    const int t = combo / per_t, rem = combo % per_t;
+    const int a = rem / p.rank, j = rem % p.rank;
+    const int r0 = p.seg_off[a], r1 = p.seg_off[a + 1];
+    if (r0 == r1) continue;
+    const int k0 = ks * SHRINK_SLICE;
+    const __nv_bfloat16* A = (t == 0 ? p.sh_a0 : p.sh_a1) + ((size_t)a * p.rank + j) * p.sh_K;
+    uint4 araw[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int k = k0 + i * 256 + lane * 8;
+      araw[i] = k < p.sh_K ? __ldg(reinterpret_cast<const uint4*>(A + k)) : make_uint4(0, 0, 0, 0);
+    }
+    for (int rr = r0; rr < r1; ++rr) {
+      const int gr = p.seg_rows[rr];
+      if (gr < p.row0 || gr >= p.row0 + p.n_rows) continue;
+      uint4 xraw[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int k = k0 + i * 256 + lane * 8;
+        xraw[i] = k < p.sh_K ? *reinterpret_cast<const uint4*>(p.sh_x + (size_t)gr * p.sh_ld + k)
+                             : make_uint4(0, 0, 0, 0);
+      }
+      float acc = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float af[8], xf[8];
+        unpack8(araw[i], af);
+        unpack8(xraw[i], xf);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc = fmaf(xf[e], af[e], acc);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) {
+        const size_t slot = ((size_t)gr * p.n_u + t) * p.rank + j;
+        if (splits == 1) {
+          const float sc = p.sh_scale_inv ? rm.inv[gr - p.row0] : 1.f;
+          p.lora_u[slot] = __fmul_rn(acc, sc);
+        } else {
+          p.sh_part[(size_t)ks * p.rows_total * p.n_u * p.rank + slot] = acc;
+        }
+      }
+    }
+    if (splits > 1 && lane == 0) {
+      __threadfence();
+      int* cnt = p.sh_cnt + combo;
+      if (atomicAdd(cnt, 1) == splits - 1) {
+        __threadfence();
+        for (int rr = r0; rr < r1; ++rr) {
+          const int gr = p.seg_rows[rr];
+          if (gr < p.row0 || gr >= p.row0 + p.n_rows) continue;
+          const size_t slot = ((size_t)gr * p.n_u + t) * p.rank + j;
+          float s = 0.f;
+          for (int q = 0; q < splits; ++q)
+            s = (q == 0) ? __ldcg(p.sh_part + slot)
+                         : __fadd_rn(s, __ldcg(p.sh_part + (size_t)q * p.rows_total * p.n_u * p.rank + slot));
+          const float sc = p.sh_scale_inv ? rm.inv[gr - p.row0] : 1.f;
+          p.lora_u[slot] = __fmul_rn(s, sc);
+        }
+        *cnt = 0;
+      }
+    }
   }
 }
 
@@ -172,14 +337,20 @@ __global__ void __launch_bounds__(256, 1)
   using C = Cfg<NT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)C::STAGES * C::STAGE);
-  uint64_t* empty = full + C::STAGES;
-  uint64_t* tmem_full = empty + C::STAGES;
+  const int NS = (p.stages > 0 && p.stages < C::STAGES) ? p.stages : C::STAGES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NS * C::STAGE);
+  uint64_t* empty = full + NS;
+  uint64_t* tmem_full = empty + NS;
   uint64_t* tmem_empty = tmem_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
-  int* flag = reinterpret_cast<int*>(tmem_slot + 1);
-  float* red_val = reinterpret_cast<float*>(flag + 4);
-  int* red_idx = reinterpret_cast<int*>(red_val + 64);
+  EpiShared& sh = *reinterpret_cast<EpiShared*>(tmem_slot + 4);
+  RowMeta rm;
+  rm.kind = reinterpret_cast<int*>(&sh + 1);
+  rm.ad = rm.kind + NT;
+  rm.pos = rm.ad + NT;
+  rm.kvoff = rm.pos + NT;
+  rm.inv = reinterpret_cast<float*>(rm.kvoff + NT);
+  rm.u = NT <= 64 ? rm.inv + NT : nullptr;  // larger launches read U from global memory
 
   const int warp = warp_id();
   Split sp;
@@ -191,7 +362,7 @@ __global__ void __launch_bounds__(256, 1)
   const int t_first = (int)(u_begin / sp.Ut), t_last = (int)((u_end - 1) / sp.Ut);
 
   if (warp == 0 && elect_one()) {
-    for (int i = 0; i < C::STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < NS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
     mbar_init(tmem_full, 1);
     mbar_init(tmem_empty, 128);
     fence_barrier_init();
@@ -199,29 +370,42 @@ __global__ void __launch_bounds__(256, 1)
     tma_prefetch_desc(&tm_x);
   }
   if (warp == 2) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  if (threadIdx.x == 128) { sh.shrink_ready = 0; sh.flag = 0; }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_launch();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (elect_one()) {
       const uint64_t pol = policy_evict_first();
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int t = t_first; t <= t_last; ++t) {
-        const long long t0 = (long long)t * sp.Ut;
-        const int kb = (int)((u_begin > t0 ? u_begin : t0) - t0);
-        const int ke = (int)((u_end < t0 + sp.Ut ? u_end : t0 + sp.Ut) - t0);
-        for (int k = kb; k < ke; ++k) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* st = smem + (size_t)stage * C::STAGE;
-          mbar_expect_tx(&full[stage], C::STAGE);
+      auto load_w = [&](long long u, int stage) {
+        const int t = (int)(u / sp.Ut), k = (int)(u % sp.Ut);
+        uint8_t* st = smem + (size_t)stage * C::STAGE;
+        mbar_expect_tx(&full[stage], C::STAGE);
+        if (p.w_blocked)
+          tma_load_3d_hint(st, &tm_w, &full[stage], 0, 0, t * sp.Ut + k, pol);
+        else
           tma_load_2d_hint(st, &tm_w, &full[stage], k * BK, t * BM, pol);
-          tma_load_2d(st + W_BYTES, &tm_x, &full[stage], k * BK, x_row0);
-          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
-        }
+      };
+      auto load_x = [&](long long u, int stage) {
+        const int k = (int)(u % sp.Ut);
+        tma_load_2d(smem + (size_t)stage * C::STAGE + W_BYTES, &tm_x, &full[stage], k * BK, x_row0);
+      };
+      // Weights do not depend on the previous kernel: fill the ring before waiting on it.
+      const long long pre = (u_end - u_begin) < NS ? (u_end - u_begin) : NS;
+      for (long long i = 0; i < pre; ++i) load_w(u_begin + i, (int)i);
+      pdl_wait();
+      for (long long i = 0; i < pre; ++i) load_x(u_begin + i, (int)i);
+      int stage = (int)(pre % NS);
+      uint32_t phase = (pre == NS) ? 1u : 0u;
+      for (long long u = u_begin + pre; u < u_end; ++u) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        load_w(u, stage);
+        load_x(u, stage);
+        if (++stage == NS) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
@@ -237,7 +421,12 @@ __global__ void __launch_bounds__(256, 1)
       for (int k = kb; k < ke; ++k) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
-        if (elect_one()) {
+        if (p.skip_mma) {
+          if (elect_one()) {
+            mbar_arrive(&empty[stage]);
+            if (k == ke - 1) mbar_arrive(tmem_full);
+          }
+        } else if (elect_one()) {
           const uint32_t a = smem_u32(smem + (size_t)stage * C::STAGE);
           const uint32_t b = a + W_BYTES;
 #pragma unroll
@@ -249,14 +438,65 @@ __global__ void __launch_bounds__(256, 1)
           if (k == ke - 1) tc_commit(tmem_full);
         }
         __syncwarp();
-        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        if (++stage == NS) { stage = 0; phase ^= 1; }
       }
       tphase ^= 1;
+    }
+  } else if (warp == 2 || warp == 3) {
+    // ---------------- LoRA shrink (SGMV) on the two otherwise idle warps ----------------
+    if (p.sh_x != nullptr) {
+      pdl_wait();
+      named_bar_sync(2, 192);  // wait for the epilogue warps' row metadata
+      const int lane = lane_id();
+      lora_shrink_tasks(p, rm, blockIdx.x * 2 + (warp - 2), gridDim.x * 2, lane);
+      __syncwarp();
+      __threadfence();
+      if (lane == 0) atomicAdd(p.sync, 1);
     }
   } else if (warp >= 4) {
     // ---------------- epilogue (TMEM -> registers -> global) ----------------
     const int ep_t = threadIdx.x - 128;
     const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+    pdl_wait();
+    // stage this launch's row metadata (+ RMSNorm inverse) in smem
+    for (int n = ep_t; n < NT; n += 128) {
+      int kind = -1, ad = -1, pos = 0, kvoff = 0;
+      float inv = 1.f;
+      if (n < p.n_rows) {
+        const int gn = p.row0 + n;
+        kind = p.row_kind ? p.row_kind[gn] : 0;
+        ad = p.row_adapter ? p.row_adapter[gn] : -1;
+        pos = p.row_pos ? p.row_pos[gn] : 0;
+        if (p.mode == EPI_QKV && kind == 0) {
+          const int page = p.block_table[(size_t)p.row_seq[gn] * p.bt_stride + (pos >> 4)];
+          kvoff = (page * p.num_kv_heads * 16 + (pos & 15)) * p.head_dim;
+        }
+        if (p.in_ssq != nullptr) {
+          float ss = 0.f;
+          for (int t = 0; t < p.ss_tiles; ++t) ss = __fadd_rn(ss, p.in_ssq[(size_t)t * p.ss_stride + gn]);
+          inv = __fdiv_rn(1.f, sqrtf(__fadd_rn(__fdiv_rn(ss, p.ss_d), p.eps)));
+        }
+      }
+      rm.kind[n] = kind;
+      rm.ad[n] = ad;
+      rm.pos[n] = pos;
+      rm.kvoff[n] = kvoff;
+      rm.inv[n] = inv;
+    }
+    named_bar_sync(1, 128);
+    if (p.sh_x != nullptr) named_bar_arrive(2, 192);  // row metadata ready for the shrink warps
+    if (p.lora_b != nullptr) {
+      // warm L2 with the adapter B rows this CTA's tiles will need in the epilogue
+      for (int t = t_first; t <= t_last; ++t) {
+        const int m = t * BM + ep_t;
+        if (m >= p.lora_m) continue;
+        for (int a = 0; a < p.slots; ++a) {
+          if (p.seg_off[a] == p.seg_off[a + 1]) continue;
+          const char* b = reinterpret_cast<const char*>(p.lora_b + ((size_t)a * p.lora_m + m) * p.rank);
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(b));
+        }
+      }
+    }
     uint32_t tphase = 0;
     for (int t = t_first; t <= t_last; ++t) {
       const long long t0 = (long long)t * sp.Ut;
@@ -268,7 +508,7 @@ __global__ void __launch_bounds__(256, 1)
         for (int cc = 0; cc < NT / 16; ++cc) {
           float v[16];
           tmem_ld16(tmem_base + lane_base + cc * 16, v);
-          finalize16<NT>(p, t, cc * 16, v, ep_t, red_val, red_idx);
+          finalize16<NT>(p, t, cc * 16, v, ep_t, sh, rm);
         }
         tc_fence_before();
         mbar_arrive(tmem_empty);
@@ -285,9 +525,9 @@ __global__ void __launch_bounds__(256, 1)
         mbar_arrive(tmem_empty);
         __threadfence();
         named_bar_sync(1, 128);
-        if (ep_t == 0) *flag = atomicAdd(&p.counters[t], 1);
+        if (ep_t == 0) sh.flag = atomicAdd(&p.counters[t], 1);
         named_bar_sync(1, 128);
-        const bool last = (*flag == nseg - 1);
+        const bool last = (sh.flag == nseg - 1);
         named_bar_sync(1, 128);
         if (last) {
           __threadfence();
@@ -304,7 +544,7 @@ __global__ void __launch_bounds__(256, 1)
                 v[j] = (s == 0) ? x : __fadd_rn(v[j], x);
               }
             }
-            finalize16<NT>(p, t, cc * 16, v, ep_t, red_val, red_idx);
+            finalize16<NT>(p, t, cc * 16, v, ep_t, sh, rm);
           }
           if (ep_t == 0) p.counters[t] = 0;
         }
@@ -316,6 +556,15 @@ __global__ void __launch_bounds__(256, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 2) tmem_dealloc<C::TMEM_COLS>(tmem_base);
+  if (p.sh_x != nullptr && threadIdx.x == 0) {
+    // every CTA has passed its shrink wait: the last one out resets the counters
+    __threadfence();
+    if (atomicAdd(p.sync + 1, 1) == (int)gridDim.x - 1) {
+      p.sync[0] = 0;
+      p.sync[1] = 0;
+      __threadfence();
+    }
+  }
 }
 
 // ------------------------------------------------------------------ host side
@@ -332,8 +581,9 @@ static cudaError_t launch_nt(const CUtensorMap& tw, const CUtensorMap& tx, const
   }
   const long long U = (long long)(p.M / BM) * (p.K / BK);
   const int G = (int)(U < num_sms ? U : num_sms);
-  gemm_streamk_kernel<NT><<<G, 256, C::SMEM, s>>>(tw, tx, p, x_row0);
-  return cudaGetLastError();
+  const int NS = (p.stages > 0 && p.stages < C::STAGES) ? p.stages : C::STAGES;
+  const size_t smem = 1024 + (size_t)NS * C::STAGE + aux_smem<NT>();
+  return launch_pdl(gemm_streamk_kernel<NT>, dim3(G), dim3(256), smem, s, tw, tx, p, x_row0);
 }
 
 int gemm_pick_nt(int rows) {
@@ -346,6 +596,7 @@ int gemm_pick_nt(int rows) {
 
 cudaError_t gemm_launch(const CUtensorMap& tw, const CUtensorMap& tx, const GemmParams& p,
                         int x_row0, int nt, int num_sms, cudaStream_t s) {
+  if (p.rank > MAX_RANK) return cudaErrorInvalidValue;
   switch (nt) {
     case 16: return launch_nt<16>(tw, tx, p, x_row0, num_sms, s);
     case 32: return launch_nt<32>(tw, tx, p, x_row0, num_sms, s);

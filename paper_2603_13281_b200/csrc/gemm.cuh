@@ -5,20 +5,27 @@
 //
 // Reference op: `base_linear` / `icarus_linear` (src/model.py:334-371) whose inner
 // product is `_mm` (src/tensor.py:151-156). The reference stores W as [in, out];
-// the device copy is [out, in] (K-major) so both MMA operands are K-major.
+// the device copy is [out, in] (K-major), tile-major [M/128][K/64][128][64].
 //
 // Design (B200-first):
 //  * persistent stream-K over (m_tile, k_chunk) units: grid = #SMs, every CTA gets the
 //    same number of 64-wide K chunks (+-1), so all 148 SMs stream weights to the end;
 //  * warp-specialised: warp0 = TMA producer, warp1 = tcgen05.mma issuer,
 //    warp2 = TMEM allocator, warps4..7 = epilogue (one TMEM lane = one output feature);
-//  * TMA 128B-swizzled tiles W[128 x 64] + X[N x 64] into a deep smem ring;
-//    accumulator [128 x N] fp32 in TMEM, read back with tcgen05.ld;
+//  * programmatic dependent launch: the producer streams the first ring of WEIGHT tiles
+//    before `griddepcontrol.wait`, i.e. while the previous kernel is still draining --
+//    only the activation tiles depend on it;
 //  * split tiles are reduced deterministically: every segment writes its fp32 partial,
 //    the last arriving segment sums them in segment order (fixed by (M, K, grid) only,
 //    never by N) -- so a token row's result does not depend on batch composition;
-//  * fused epilogues: LoRA expand on decoder rows only (SGMV, CUDA cores, B read once),
-//    RoPE + paged-KV write (encoder rows only), residual add, SiLU*up, LM-head argmax.
+//  * RMSNorm folded in: X is bf16(x) (the raw residual stream); the epilogue scales row n
+//    by inv_n = 1/sqrt(mean(x_n^2)+eps) from per-128-feature sum-of-squares partials that
+//    the residual-producing epilogue wrote (gain folded into W on upload);
+//  * LoRA shrink (SGMV, U = x A^T per decoder row) is computed by the otherwise idle
+//    epilogue warps of every CTA while the weights stream; the expand (B U) is applied in
+//    the epilogue to decoder rows only;
+//  * fused epilogues: RoPE + paged-KV write (encoder rows only), residual add (+ bf16 copy
+//    + sum-of-squares partials for the next norm), SiLU*up, LM-head per-tile argmax.
 #pragma once
 #include "ptx.cuh"
 
@@ -27,32 +34,53 @@ namespace icr {
 enum EpiMode : int {
   EPI_F32 = 0,     // out_f32[n, m] = acc                       (tests / debug logits)
   EPI_QKV = 1,     // RoPE(q,k); q -> q_out bf16; k,v of encoder rows -> KV pages
-  EPI_RESID = 2,   // resid[n, m] += acc                       (wo, down)
+  EPI_RESID = 2,   // x[n, m] += acc; xb = bf16(x); ssq partial of x^2 per 128-feature tile
   EPI_SILU = 3,    // rows interleaved (gate_j, up_j): f[n, j] = silu(g) * u
   EPI_ARGMAX = 4,  // per-tile (max, argmax) over m for every row n (LM head)
 };
 
 struct GemmParams {
   int mode;
-  int M;        // rows of W (multiple of 128)
-  int K;        // multiple of 64
-  int n_rows;   // valid token rows in this launch (<= N tile)
-  int m_valid;  // features >= m_valid are masked (LM head vocab padding)
-  // per-row metadata (already offset to this row group)
-  const int* row_kind;     // 0 encoder, 1 decoder, <0 padding
-  const int* row_adapter;  // adapter slot for decoder rows
+  int w_blocked;  // 1: W stored tile-major [M/128][K/64][128][64] (3-D tensor map)
+  int M;          // rows of W (multiple of 128)
+  int K;          // multiple of 64
+  int n_rows;     // valid token rows in this launch (<= N tile)
+  int row0;       // global index of this launch's first row (row groups of <= 256)
+  int rows_total; // padded rows of the whole forward (stride of global-row scratch)
+  int m_valid;    // features >= m_valid are masked (LM head vocab padding)
+  // per-row metadata, GLOBAL row indexing (this launch reads [row0, row0 + n_rows))
+  const int* row_kind;     // 0 encoder, 1 decoder, <0 padding; null = all encoder
+  const int* row_adapter;  // adapter slot for decoder rows (-1 = none)
   const int* row_pos;      // absolute position
   const int* row_seq;      // sequence slot (block-table row)
+  // RMSNorm of the input rows: inv_n from partial sums of squares [ss_tiles][ss_stride]
+  const float* in_ssq;     // null = no scaling
+  int ss_tiles, ss_stride;
+  float ss_d, eps;         // feature count d (mean = sum / d) and RMSNorm eps
   // LoRA expand (decoder rows only): delta[m] = sum_j U[n, uidx, j] * Bs[slot, m, j]
-  const __nv_bfloat16* lora_b;  // [slots][lora_m][rank], scaling folded in; null = none
-  const float* lora_u;          // [rows][n_u][rank]
+  const __nv_bfloat16* lora_b;  // [slots][lora_m][rank], alpha/rank folded in; null = none
+  float* lora_u;                // [rows_total][n_u][rank] (global rows)
   int lora_m;                   // rows of W that carry an adapter (q_dim for qkv)
   int rank;
   int n_u;                      // 1, or 2 for interleaved gate/up
-  // outputs
+  // in-kernel LoRA shrink: U[n][t][j] = s_n * sum_k X_sh[n][k] * A_t[a][j][k]
+  const __nv_bfloat16* sh_x;    // bf16 [rows_total][sh_ld]; null = no shrink
+  int sh_ld, sh_K, sh_targets;  // sh_targets 1 or 2
+  const __nv_bfloat16* sh_a0;   // [slots][rank][sh_K]
+  const __nv_bfloat16* sh_a1;
+  int sh_scale_inv;             // 1: s_n = inv_n (X_sh is the un-normed residual)
+  const int* seg_off;           // [slots + 1] decoder rows grouped by adapter slot
+  const int* seg_rows;          // global row indices
+  int slots;
+  int* sync;                    // [2] shrink-done / exit counters (self-resetting)
+  float* sh_part;               // [SHRINK_SPLITS][rows_total][n_u][rank] K-split partials
+  int* sh_cnt;                  // [2][slots][rank] split arrivals per adapter row (self-resetting)
+  // outputs (GLOBAL row indexing)
   float* out_f32;               // EPI_F32
   int ld_out;
-  float* resid;                 // EPI_RESID, [rows][M]
+  float* resid;                 // EPI_RESID x [rows_total][M]
+  __nv_bfloat16* resid_bf16;    // EPI_RESID bf16 copy of x (next GEMM's X operand)
+  float* out_ssq;               // EPI_RESID partial sums of squares [M/128][ss_stride]
   __nv_bfloat16* out_bf16;      // EPI_QKV: q [rows][q_dim]; EPI_SILU: f [rows][M/2]
   // EPI_QKV specifics
   int q_dim, kv_dim, head_dim, num_kv_heads;
@@ -62,12 +90,15 @@ struct GemmParams {
   const int* block_table;       // [num_seq_slots][max_pages_per_seq]
   int bt_stride;
   // EPI_ARGMAX
-  float2* tile_best;            // [m_tiles][rows_total] (value, index-as-float-bits)
+  float2* tile_best;            // [m_tiles][best_stride] (value, index-as-float-bits)
   int best_stride;
-  // stream-K bookkeeping (scratch, zero-initialised once; counters self-reset)
-  float* ws;                    // [m_tiles][max_segs][N][128]
+  // stream-K bookkeeping (scratch; counters self-reset)
+  float* ws;                    // [grid][2][N][128]
   int* counters;                // [m_tiles]
   int max_segs;
+  // tuning / diagnostics (0 = defaults)
+  int stages;     // smem ring depth actually used (<= compiled maximum)
+  int skip_mma;   // 1: consume stages without tcgen05.mma (pure TMA streaming rate)
 };
 
 }  // namespace icr

@@ -10,6 +10,26 @@ namespace icr {
 
 struct GemmParams;
 
+// Programmatic dependent launch for every kernel of the step: the next kernel may start
+// (prologue, weight prefetch) while this one drains; kernels call griddepcontrol.wait
+// before touching their predecessor's outputs. g_pdl = 0 disables it (ICR_NO_PDL=1).
+extern int g_pdl;
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // --------------------------------------------------------------- GEMM (gemm.cu)
 cudaError_t gemm_launch(const CUtensorMap& tw, const CUtensorMap& tx, const GemmParams& p,
                         int x_row0, int nt, int num_sms, cudaStream_t s);
@@ -44,26 +64,31 @@ struct AttnLaunch {
   float scale;
   float* part_o;
   float2* part_ml;
+  int* merge_cnt;  // [rows][H_kv], zero-initialised, self-resetting
   __nv_bfloat16* out;
   int out_ld;
 };
 cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t s);
 
 // --------------------------------------------------------------- row ops (rowops.cu)
-// x_out[r] = embed[tok[r]] (if embed != null) else x_in; h[r] = bf16(x * rsqrt(mean(x^2)+eps))
-cudaError_t rmsnorm_launch(const float* x_in, const int* tokens, const __nv_bfloat16* embed,
-                           float* x_out, __nv_bfloat16* h_out, const int* row_kind,
-                           const int* row_map, int n_rows, int d, float eps, cudaStream_t s);
+// Layer-0 input: x[r] = embed[tok[r]] (fp32 residual stream), xb = bf16(x), and the
+// per-128-feature sums of squares ssq[c][r] that the first GEMM turns into RMSNorm scales.
+cudaError_t embed_launch(const int* tokens, const int* row_kind, const __nv_bfloat16* embed,
+                         float* x, __nv_bfloat16* xb, float* ssq, int ss_stride, int n_rows,
+                         int d, cudaStream_t s);
 
-// LoRA shrink (SGMV): for each adapter slot a and each row n of segment a,
-//   U[n][t][j] = scale * sum_k h[n][k] * A_t[a][j][k]          (t < n_targets <= 2)
-cudaError_t lora_shrink_launch(const __nv_bfloat16* h, int ld_h, int K,
-                               const __nv_bfloat16* A0, const __nv_bfloat16* A1, int n_targets,
-                               int slots, int rank, float scale, const int* seg_off,
-                               const int* seg_rows, float* U, cudaStream_t s);
+// Emitting rows for the LM head: hlm[i] = xb[lm_rows[i]], ssq_lm[c][i] = ssq[c][lm_rows[i]];
+// rows n_lm..n_pad-1 are zero.
+cudaError_t lm_gather_launch(const __nv_bfloat16* xb, const float* ssq, int ss_stride,
+                             const int* lm_rows, int n_lm, int n_pad, int d,
+                             __nv_bfloat16* hlm, float* ssq_lm, cudaStream_t s);
 
 // Final argmax over LM-head tiles (lowest index on ties, src/engine.py:75-76).
 cudaError_t argmax_reduce_launch(const float2* tile_best, int tiles, int stride, int n_rows,
                                  int* out_tokens, cudaStream_t s);
+
+// tokens[r] = out_tok[src[r]] for src[r] >= 0 (device-side greedy feedback).
+cudaError_t feedback_launch(int* tokens, const int* out_tok, const int* src, int n,
+                            cudaStream_t s);
 
 }  // namespace icr

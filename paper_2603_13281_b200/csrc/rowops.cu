@@ -1,167 +1,130 @@
-// Row-wise kernels of the decode step: embedding gather + RMSNorm, LoRA shrink (SGMV),
-// and the cross-tile LM-head argmax.
+// Row-wise kernels of the decode step: embedding gather (+ RMSNorm statistics), LM-row
+// gather, the cross-tile LM-head argmax, and the on-device greedy token feedback.
 #include "kernels.h"
 #include "ptx.cuh"
 
 namespace icr {
 
-// One CTA per token row. Reference: rms_norm, src/tensor.py:217-246 (gain folded into the
-// next weight on upload, see runtime.cu); embedding gather, src/tensor.py:321-332.
+int g_pdl = 1;
+
+// One CTA (8 warps) per token row. Reference: gather_rows, src/tensor.py:321-332; the
+// sums of squares feed rms_norm (src/tensor.py:217-246) inside the first projection GEMM.
+// Warp w owns 128-feature chunks w, w+8, ...: no block barriers, all loads in flight.
 __global__ void __launch_bounds__(256)
-    rmsnorm_kernel(const float* __restrict__ x_in, const int* __restrict__ tokens,
-                   const __nv_bfloat16* __restrict__ embed, float* __restrict__ x_out,
-                   __nv_bfloat16* __restrict__ h_out, const int* __restrict__ row_kind,
-                   const int* __restrict__ row_map, int d, float eps) {
-  const int r = blockIdx.x;
-  const int src_row = row_map != nullptr ? row_map[r] : r;
-  const int tid = threadIdx.x;
-  __shared__ float red[8];
-  __nv_bfloat16* h = h_out + (size_t)r * d;
-  if (row_kind != nullptr && row_kind[r] < 0) {
-    for (int i = tid; i < d; i += 256) h[i] = __float2bfloat16_rn(0.f);
-    return;
-  }
-  const float* x = x_in + (size_t)src_row * d;
-  float* xo = x_out + (size_t)src_row * d;
-  float ss = 0.f;
-  if (embed != nullptr) {
-    const __nv_bfloat16* e = embed + (size_t)tokens[src_row] * d;
-    for (int i = tid; i < d; i += 256) {
-      const float v = __bfloat162float(e[i]);
-      xo[i] = v;
-      ss = fmaf(v, v, ss);
+    embed_kernel(const int* __restrict__ tokens, const int* __restrict__ row_kind,
+                 const __nv_bfloat16* __restrict__ embed, float* __restrict__ x,
+                 __nv_bfloat16* __restrict__ xb, float* __restrict__ ssq, int ss_stride, int d) {
+  pdl_launch();
+  pdl_wait();
+  const int r = blockIdx.x, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool valid = row_kind[r] >= 0;
+  const __nv_bfloat16* e = embed + (size_t)(valid ? tokens[r] : 0) * d;
+  for (int c = w; c < d / 128; c += 8) {
+    const int i = c * 128 + lane * 4;
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+    if (valid) {
+      const uint2 raw = *reinterpret_cast<const uint2*>(e + i);
+      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+      const float2 a = __bfloat1622float2(h2[0]), b = __bfloat1622float2(h2[1]);
+      v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
     }
-  } else {
-    for (int i = tid; i < d; i += 256) {
-      const float v = x[i];
-      ss = fmaf(v, v, ss);
-    }
+    *reinterpret_cast<float4*>(x + (size_t)r * d + i) = make_float4(v[0], v[1], v[2], v[3]);
+    __nv_bfloat162 o0 = __floats2bfloat162_rn(v[0], v[1]), o1 = __floats2bfloat162_rn(v[2], v[3]);
+    uint2 ob;
+    ob.x = *reinterpret_cast<uint32_t*>(&o0);
+    ob.y = *reinterpret_cast<uint32_t*>(&o1);
+    *reinterpret_cast<uint2*>(xb + (size_t)r * d + i) = ob;
+    float sq = __fadd_rn(__fadd_rn(__fmul_rn(v[0], v[0]), __fmul_rn(v[1], v[1])),
+                         __fadd_rn(__fmul_rn(v[2], v[2]), __fmul_rn(v[3], v[3])));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    if (lane == 0) ssq[(size_t)c * ss_stride + r] = sq;
   }
-  ss = warp_sum(ss);
-  if ((tid & 31) == 0) red[tid >> 5] = ss;
-  __syncthreads();
-  if (tid < 32) {
-    float t = tid < 8 ? red[tid] : 0.f;
-    t = warp_sum(t);
-    if (tid == 0) red[0] = t;
-  }
-  __syncthreads();
-  const float mean = __fdiv_rn(red[0], (float)d);
-  const float inv = __fdiv_rn(1.f, sqrtf(__fadd_rn(mean, eps)));
-  const float* src = embed != nullptr ? xo : x;
-  for (int i = tid; i < d; i += 256) h[i] = __float2bfloat16_rn(__fmul_rn(src[i], inv));
 }
 
-cudaError_t rmsnorm_launch(const float* x_in, const int* tokens, const __nv_bfloat16* embed,
-                           float* x_out, __nv_bfloat16* h_out, const int* row_kind,
-                           const int* row_map, int n_rows, int d, float eps, cudaStream_t s) {
+cudaError_t embed_launch(const int* tokens, const int* row_kind, const __nv_bfloat16* embed,
+                         float* x, __nv_bfloat16* xb, float* ssq, int ss_stride, int n_rows,
+                         int d, cudaStream_t s) {
   if (n_rows <= 0) return cudaSuccess;
-  rmsnorm_kernel<<<n_rows, 256, 0, s>>>(x_in, tokens, embed, x_out, h_out, row_kind, row_map, d,
-                                        eps);
-  return cudaGetLastError();
+  return launch_pdl(embed_kernel, dim3(n_rows), dim3(256), 0, s, tokens, row_kind, embed, x, xb,
+                    ssq, ss_stride, d);
 }
 
-// grid = (rank, slots, n_targets). Each CTA owns one A row (adapter a, rank index j) and
-// produces U[n][t][j] for every row of segment a (reference: _lowrank_delta's first
-// product x @ A^T, src/model.py:340-343; A stored [rank, in] exactly as the reference).
-constexpr int SHRINK_ROWS = 16;
-__global__ void __launch_bounds__(256)
-    lora_shrink_kernel(const __nv_bfloat16* __restrict__ h, int ld_h, int K,
-                       const __nv_bfloat16* __restrict__ A0, const __nv_bfloat16* __restrict__ A1,
-                       int n_targets, int rank, float scale, const int* __restrict__ seg_off,
-                       const int* __restrict__ seg_rows, float* __restrict__ U) {
-  const int j = blockIdx.x, a = blockIdx.y, t = blockIdx.z;
-  const int r0 = seg_off[a], r1 = seg_off[a + 1];
-  if (r0 == r1) return;
-  const __nv_bfloat16* A = (t == 0 ? A0 : A1) + ((size_t)a * rank + j) * K;
-  const int tid = threadIdx.x;
-  __shared__ float red[8][SHRINK_ROWS];
-  for (int rb = r0; rb < r1; rb += SHRINK_ROWS) {
-    const int nr = min(SHRINK_ROWS, r1 - rb);
-    float acc[SHRINK_ROWS];
-#pragma unroll
-    for (int i = 0; i < SHRINK_ROWS; ++i) acc[i] = 0.f;
-    for (int k = tid * 8; k < K; k += 256 * 8) {
-      const uint4 araw = *reinterpret_cast<const uint4*>(A + k);
-      const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&araw);
-      float af[8];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float2 f = __bfloat1622float2(a2[q]);
-        af[2 * q] = f.x;
-        af[2 * q + 1] = f.y;
-      }
-#pragma unroll
-      for (int i = 0; i < SHRINK_ROWS; ++i) {
-        if (i < nr) {
-          const int n = seg_rows[rb + i];
-          const uint4 hraw = *reinterpret_cast<const uint4*>(h + (size_t)n * ld_h + k);
-          const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&hraw);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float2 f = __bfloat1622float2(h2[q]);
-            acc[i] = fmaf(f.x, af[2 * q], acc[i]);
-            acc[i] = fmaf(f.y, af[2 * q + 1], acc[i]);
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < SHRINK_ROWS; ++i) {
-      const float v = warp_sum(acc[i]);
-      if ((tid & 31) == 0) red[tid >> 5][i] = v;
-    }
-    __syncthreads();
-    if (tid < nr) {
-      float v = 0.f;
-      for (int w = 0; w < 8; ++w) v += red[w][tid];
-      const int n = seg_rows[rb + tid];
-      U[((size_t)n * n_targets + t) * rank + j] = __fmul_rn(v, scale);
-    }
-    __syncthreads();
+__global__ void __launch_bounds__(128)
+    lm_gather_kernel(const __nv_bfloat16* __restrict__ xb, const float* __restrict__ ssq,
+                     int ss_stride, const int* __restrict__ lm_rows, int n_lm, int n_pad, int d,
+                     __nv_bfloat16* __restrict__ hlm, float* __restrict__ ssq_lm) {
+  pdl_launch();
+  pdl_wait();
+  const int i = blockIdx.x, t = threadIdx.x;
+  const bool valid = i < n_lm;
+  const int src = valid ? lm_rows[i] : 0;
+  for (int k = t * 8; k < d; k += 128 * 8) {
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (valid) v = *reinterpret_cast<const uint4*>(xb + (size_t)src * d + k);
+    *reinterpret_cast<uint4*>(hlm + (size_t)i * d + k) = v;
   }
+  for (int c = t; c < d / 128; c += 128)
+    ssq_lm[(size_t)c * ss_stride + i] = valid ? ssq[(size_t)c * ss_stride + src] : 0.f;
 }
 
-cudaError_t lora_shrink_launch(const __nv_bfloat16* h, int ld_h, int K, const __nv_bfloat16* A0,
-                               const __nv_bfloat16* A1, int n_targets, int slots, int rank,
-                               float scale, const int* seg_off, const int* seg_rows, float* U,
-                               cudaStream_t s) {
-  if (slots <= 0) return cudaSuccess;
-  dim3 grid(rank, slots, n_targets);
-  lora_shrink_kernel<<<grid, 256, 0, s>>>(h, ld_h, K, A0, A1, n_targets, rank, scale, seg_off,
-                                          seg_rows, U);
-  return cudaGetLastError();
+cudaError_t lm_gather_launch(const __nv_bfloat16* xb, const float* ssq, int ss_stride,
+                             const int* lm_rows, int n_lm, int n_pad, int d, __nv_bfloat16* hlm,
+                             float* ssq_lm, cudaStream_t s) {
+  if (n_pad <= 0) return cudaSuccess;
+  return launch_pdl(lm_gather_kernel, dim3(n_pad), dim3(128), 0, s, xb, ssq, ss_stride, lm_rows,
+                    n_lm, n_pad, d, hlm, ssq_lm);
 }
 
-// One warp per row. (value, index) is a total order (value desc, index asc), so the
-// result is the first maximum regardless of scan order -- np.argmax semantics.
-__global__ void argmax_reduce_kernel(const float2* __restrict__ tile_best, int tiles, int stride,
-                                     int n_rows, int* __restrict__ out_tokens) {
-  const int r = blockIdx.x * 4 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (r >= n_rows) return;
+// One CTA per row. (value, index) is a total order (value desc, index asc), so the result
+// is the first maximum regardless of scan order -- np.argmax semantics.
+__device__ __forceinline__ void argmax_take(float& bv, int& bi, float ov, int oi) {
+  if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+}
+__global__ void __launch_bounds__(256)
+    argmax_reduce_kernel(const float2* __restrict__ tile_best, int tiles, int stride, int n_rows,
+                         int* __restrict__ out_tokens) {
+  pdl_launch();
+  pdl_wait();
+  const int r = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+  __shared__ float sv[8];
+  __shared__ int si[8];
   float bv = -INFINITY;
   int bi = 0x7fffffff;
-  for (int t = lane; t < tiles; t += 32) {
+  for (int t = tid; t < tiles; t += 256) {
     const float2 e = tile_best[(size_t)t * stride + r];
-    const int ei = __float_as_int(e.y);
-    if (e.x > bv || (e.x == bv && ei < bi)) { bv = e.x; bi = ei; }
+    argmax_take(bv, bi, e.x, __float_as_int(e.y));
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-    if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+  for (int o = 16; o > 0; o >>= 1)
+    argmax_take(bv, bi, __shfl_xor_sync(0xffffffffu, bv, o), __shfl_xor_sync(0xffffffffu, bi, o));
+  if (lane == 0) { sv[tid >> 5] = bv; si[tid >> 5] = bi; }
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < 8; ++w) argmax_take(bv, bi, sv[w], si[w]);
+    out_tokens[r] = bi;
   }
-  if (lane == 0) out_tokens[r] = bi;
 }
 
 cudaError_t argmax_reduce_launch(const float2* tile_best, int tiles, int stride, int n_rows,
                                  int* out_tokens, cudaStream_t s) {
   if (n_rows <= 0) return cudaSuccess;
-  argmax_reduce_kernel<<<(n_rows + 3) / 4, 128, 0, s>>>(tile_best, tiles, stride, n_rows,
-                                                         out_tokens);
-  return cudaGetLastError();
+  return launch_pdl(argmax_reduce_kernel, dim3(n_rows), dim3(256), 0, s, tile_best, tiles, stride,
+                    n_rows, out_tokens);
+}
+
+__global__ void feedback_kernel(int* tokens, const int* out_tok, const int* src, int n) {
+  pdl_launch();
+  pdl_wait();
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n && src[r] >= 0) tokens[r] = out_tok[src[r]];
+}
+
+cudaError_t feedback_launch(int* tokens, const int* out_tok, const int* src, int n,
+                            cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  return launch_pdl(feedback_kernel, dim3((n + 127) / 128), dim3(128), 0, s, tokens, out_tok, src,
+                    n);
 }
 
 }  // namespace icr

@@ -3,11 +3,14 @@
 //
 // One forward pass (= one fused multi-model decode step, or one prefill chunk) is:
 //   per layer (src/model.py:480-506 fused decode, :463-478 prefill):
-//     rmsnorm(+embed) -> LoRA shrink(q) -> GEMM qkv [RoPE, q out, encoder K/V -> pages]
-//     -> paged attention partials + fixed-order merge -> LoRA shrink(o) -> GEMM o [+= x]
-//     -> rmsnorm -> LoRA shrink(gate, up) -> GEMM gate|up [silu*up] -> LoRA shrink(down)
-//     -> GEMM down [+= x]
-//   final rmsnorm on emitting rows -> GEMM lm_head [per-tile argmax] -> argmax reduce.
+//     GEMM qkv   [norm scale, LoRA shrink+expand q, RoPE, q out, encoder K/V -> pages]
+//     attention  [shared-page partials + fused fixed-order merge]
+//     GEMM o     [LoRA o, x += ., bf16 copy, sum-of-squares partials]
+//     GEMM gate|up [norm scale, LoRA gate/up, silu*up]
+//     GEMM down  [LoRA down, x += ., bf16 copy, sum-of-squares partials]
+//   + embed (layer-0 input) and, per forward, LM-row gather -> GEMM lm_head [per-tile
+//   argmax] -> argmax reduce. 5 launches per layer, all with programmatic dependent launch,
+//   captured once per batch shape into a CUDA graph and replayed.
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -22,13 +25,6 @@
 #include "../../include/icarus_b200.h"
 #include "gemm.cuh"
 #include "kernels.h"
-
-namespace icr {
-__global__ void feedback_kernel(int* tokens, const int* out_tok, const int* src, int n) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r < n && src[r] >= 0) tokens[r] = out_tok[src[r]];
-}
-}  // namespace icr
 
 using namespace icr;
 
@@ -83,6 +79,24 @@ static icr_status make_map(CUtensorMap* m, const void* ptr, uint64_t rows, uint6
   if (r != CUDA_SUCCESS)
     return fail(ICR_CUDA, "cuTensorMapEncodeTiled failed (%d) rows=%llu cols=%llu box=%u", (int)r,
                 (unsigned long long)rows, (unsigned long long)cols, box_rows);
+  return ICR_OK;
+}
+
+// Tile-major weights [M/128][K/64][128][64] bf16: box {64, 128, 1} = one contiguous 16 KB block.
+static icr_status make_map_blocked(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols) {
+  icr_status st = get_encode();
+  if (st) return st;
+  cuuint64_t dims[3] = {64, 128, (rows / 128) * (cols / 64)};
+  cuuint64_t strides[2] = {128, 128 * 128};
+  cuuint32_t box[3] = {64, 128, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(ICR_CUDA, "cuTensorMapEncodeTiled (blocked) failed (%d) rows=%llu cols=%llu", (int)r,
+                (unsigned long long)rows, (unsigned long long)cols);
   return ICR_OK;
 }
 
@@ -189,16 +203,33 @@ static icr_status build_attn_plan(int n_rows, const int* kind, const int* seq, c
   return ICR_OK;
 }
 
-// Device-side view of one forward's metadata (offsets into meta_dev).
+
+// ------------------------------------------------------------------ metadata layout
+// Offsets depend only on the padded row count and the model capacities, so a captured
+// CUDA graph stays valid while the per-step contents (positions, pages, plan) change.
 struct Meta {
-  int n_rows, rp, n_lm, n_dec, n_items;
-  size_t o_tokens, o_kind, o_seq, o_pos, o_adapter, o_lm_rows, o_seg_off, o_seg_rows, o_bt,
-      o_items, o_item_pages, o_item_rows, o_n_items, o_feedback, total;
+  int n_rows = 0, rp = 0, n_lm = 0, n_lm_pad = 0, n_dec = 0, n_items = 0;
+  size_t items_cap = 0, rows_cap = 0, pages_cap = 0;
+  size_t o_tokens = 0, o_kind = 0, o_seq = 0, o_pos = 0, o_adapter = 0, o_lm_rows = 0,
+         o_seg_off = 0, o_seg_rows = 0, o_n_items = 0, o_feedback = 0, o_bt = 0, o_items = 0,
+         o_item_rows = 0, o_item_pages = 0, total = 0, used = 0;
 };
 
 // ------------------------------------------------------------------ model
 struct LayerMaps {
   CUtensorMap qkv, o, gu, down;
+};
+
+struct GraphKey {
+  int rp, n_lm, n_items, lora;
+  float* logits;
+  bool operator<(const GraphKey& o) const {
+    if (rp != o.rp) return rp < o.rp;
+    if (n_lm != o.n_lm) return n_lm < o.n_lm;
+    if (n_items != o.n_items) return n_items < o.n_items;
+    if (lora != o.lora) return lora < o.lora;
+    return logits < o.logits;
+  }
 };
 
 struct icr_model {
@@ -210,94 +241,102 @@ struct icr_model {
   const __nv_bfloat16* lm_head;
   float scaling;
   int num_sms;
-  int q_dim, kv_dim, vpad, rp, max_chunks;
+  int q_dim, kv_dim, vpad, rp, max_chunks, group, ss_tiles;
   // scratch
-  float* x;
-  __nv_bfloat16 *h, *qb, *att, *f, *hlm;
-  float* U;
-  float2* tile_best;
-  int* out_tok;
-  float* part_o;
-  float2* part_ml;
-  float2* rope;
-  float* ws;
-  int* counters;
-  int* zero_kind;
-  CUtensorMap xmap_h[5], xmap_att[5], xmap_f[5], xmap_hlm[5];
+  float* x = nullptr;            // residual stream [rp][d]
+  __nv_bfloat16* xb = nullptr;   // bf16(x) [rp][d]
+  float* ssq = nullptr;          // per-128-feature sums of squares [d/128][rp]
+  float* ssq_lm = nullptr;
+  __nv_bfloat16 *qb = nullptr, *att = nullptr, *f = nullptr, *hlm = nullptr;
+  float* U = nullptr;
+  float2* tile_best = nullptr;
+  int* out_tok = nullptr;
+  float* part_o = nullptr;
+  float2* part_ml = nullptr;
+  int* merge_cnt = nullptr;
+  float2* rope = nullptr;
+  float* ws = nullptr;
+  int* counters = nullptr;
+  int* sync = nullptr;
+  float* sh_part = nullptr;  // LoRA shrink K-split partials
+  int* sh_cnt = nullptr;
+  CUtensorMap xmap_xb[5], xmap_att[5], xmap_f[5], xmap_hlm[5];
   // metadata staging
   int* meta_dev = nullptr;
   size_t meta_cap = 0;  // ints
   int* staging[2] = {nullptr, nullptr};
-  size_t staging_cap = 0;
-  cudaEvent_t staging_ev[2];
-  cudaEvent_t step_ev[2];
+  cudaEvent_t staging_ev[2] = {nullptr, nullptr};
+  // graphs
+  bool use_graphs = true;
+  cudaStream_t capture_stream = nullptr;
+  std::map<GraphKey, cudaGraphExec_t> graphs;
   // instrumentation of the last forward
   long long last_launches = 0;
   long long last_meta_bytes = 0;
   long long last_items = 0;
-  Meta last_mt{};
+  Meta last_mt;
   bool has_last = false;
 };
 
-static icr_status ensure_meta(icr_model* m, size_t ints) {
-  if (ints <= m->meta_cap) return ICR_OK;
-  size_t cap = std::max(ints, m->meta_cap * 2 + 4096);
-  if (m->meta_dev) cudaFree(m->meta_dev);
-  for (int i = 0; i < 2; ++i)
-    if (m->staging[i]) cudaFreeHost(m->staging[i]);
-  CUDA_TRY(cudaMalloc(&m->meta_dev, cap * sizeof(int)));
-  for (int i = 0; i < 2; ++i) CUDA_TRY(cudaMallocHost(&m->staging[i], cap * sizeof(int)));
-  m->meta_cap = cap;
-  return ICR_OK;
-}
-
-// Packs host batch metadata into `stage` (capacity checked by caller via sizing pass).
-static icr_status pack_meta(icr_model* m, const icr_batch* b, const int* pos_override,
-                            const int* feedback, int* stage, Meta& mt, AttnPlan& plan,
-                            bool size_only) {
+static Meta layout_meta(const icr_model* m, int n_rows) {
   const icr_model_config& c = m->cfg;
-  const int n = b->n_rows;
-  const int rp = (n + 15) & ~15;
-  const int* pos = pos_override ? pos_override : b->row_pos;
-  mt.n_rows = n;
-  mt.rp = rp;
-  if (!size_only) {
-    icr_status st = build_attn_plan(n, b->row_kind, b->row_seq, pos, b->block_table, b->n_seqs,
-                                    c.max_pages_per_seq, c.num_pages,
-                                    c.num_heads / c.num_kv_heads, c.chunk_pages, plan);
-    if (st) return st;
-  }
-  mt.n_items = (int)plan.items.size();
-  int n_lm = 0, n_dec = 0;
-  for (int r = 0; r < n; ++r) {
-    if (b->row_emit && b->row_emit[r]) ++n_lm;
-    if (b->row_kind[r] == 1) ++n_dec;
-  }
-  mt.n_lm = n_lm;
-  mt.n_dec = n_dec;
+  Meta mt;
+  mt.n_rows = n_rows;
+  mt.rp = (n_rows + 15) & ~15;
+  mt.rows_cap = (size_t)mt.rp * m->group * m->max_chunks;
+  mt.items_cap = (size_t)mt.rp * m->max_chunks;
+  mt.pages_cap = mt.items_cap * c.chunk_pages;
   size_t off = 0;
   auto take = [&](size_t count) {
     size_t o = off;
     off += (count + 3) & ~size_t(3);  // 16-byte alignment
     return o;
   };
-  mt.o_tokens = take(rp);
-  mt.o_kind = take(rp);
-  mt.o_seq = take(rp);
-  mt.o_pos = take(rp);
-  mt.o_adapter = take(rp);
-  mt.o_lm_rows = take(rp);
+  mt.o_tokens = take(mt.rp);
+  mt.o_kind = take(mt.rp);
+  mt.o_seq = take(mt.rp);
+  mt.o_pos = take(mt.rp);
+  mt.o_adapter = take(mt.rp);
+  mt.o_lm_rows = take(mt.rp);
   mt.o_seg_off = take(c.adapter_slots + 1);
-  mt.o_seg_rows = take(rp);
-  mt.o_bt = take((size_t)b->n_seqs * c.max_pages_per_seq);
-  mt.o_items = take(plan.items.size() * (sizeof(AttnItem) / sizeof(int)));
-  mt.o_item_pages = take(plan.pages.size());
-  mt.o_item_rows = take(plan.rows.size() * 2);
+  mt.o_seg_rows = take(mt.rp);
   mt.o_n_items = take(1);
-  mt.o_feedback = take(rp);
+  mt.o_feedback = take(mt.rp);
+  mt.o_bt = take((size_t)c.max_seqs * c.max_pages_per_seq);
+  mt.o_items = take(mt.items_cap * (sizeof(AttnItem) / sizeof(int)));
+  mt.o_item_rows = take(mt.rows_cap * 2);
+  mt.o_item_pages = take(mt.pages_cap);
   mt.total = off;
-  if (size_only) return ICR_OK;
+  return mt;
+}
 
+static icr_status ensure_meta(icr_model* m, size_t ints) {
+  if (ints <= m->meta_cap) return ICR_OK;
+  size_t cap = std::max(ints, m->meta_cap * 2 + 4096);
+  CUDA_TRY(cudaDeviceSynchronize());
+  if (m->meta_dev) cudaFree(m->meta_dev);
+  for (int i = 0; i < 2; ++i)
+    if (m->staging[i]) cudaFreeHost(m->staging[i]);
+  CUDA_TRY(cudaMalloc(&m->meta_dev, cap * sizeof(int)));
+  CUDA_TRY(cudaMemset(m->meta_dev, 0, cap * sizeof(int)));
+  for (int i = 0; i < 2; ++i) CUDA_TRY(cudaMallocHost(&m->staging[i], cap * sizeof(int)));
+  m->meta_cap = cap;
+  // graphs captured against the old buffer are stale
+  for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
+  m->graphs.clear();
+  return ICR_OK;
+}
+
+// Packs the host batch (with `pos`) into `stage` using layout `mt`.
+static icr_status pack_meta(icr_model* m, const icr_batch* b, const int* pos, const int* feedback,
+                            const AttnPlan& plan, int* stage, Meta& mt) {
+  const icr_model_config& c = m->cfg;
+  const int n = b->n_rows, rp = mt.rp;
+  if (plan.items.size() > mt.items_cap || plan.rows.size() > mt.rows_cap ||
+      plan.pages.size() > mt.pages_cap)
+    return fail(ICR_CAPACITY, "attention plan exceeds metadata capacity");
+  mt.n_items = (int)plan.items.size();
+  int n_lm = 0, n_dec = 0;
   int* t = stage;
   for (int r = 0; r < rp; ++r) {
     const bool valid = r < n;
@@ -307,11 +346,12 @@ static icr_status pack_meta(icr_model* m, const icr_batch* b, const int* pos_ove
     t[mt.o_pos + r] = valid ? pos[r] : 0;
     t[mt.o_adapter + r] = valid ? b->row_adapter[r] : -1;
     t[mt.o_feedback + r] = (valid && feedback) ? feedback[r] : -1;
+    if (valid && b->row_emit && b->row_emit[r]) t[mt.o_lm_rows + n_lm++] = r;
+    if (valid && b->row_kind[r] == 1 && b->row_adapter[r] >= 0) ++n_dec;
   }
-  int li = 0;
-  for (int r = 0; r < n; ++r)
-    if (b->row_emit && b->row_emit[r]) t[mt.o_lm_rows + li++] = r;
-  // decoder rows grouped by adapter slot (SGMV segments)
+  mt.n_lm = n_lm;
+  mt.n_lm_pad = (n_lm + 15) & ~15;
+  mt.n_dec = n_dec;
   int* seg_off = t + mt.o_seg_off;
   int* seg_rows = t + mt.o_seg_rows;
   int k = 0;
@@ -321,38 +361,36 @@ static icr_status pack_meta(icr_model* m, const icr_batch* b, const int* pos_ove
       if (b->row_kind[r] == 1 && b->row_adapter[r] == a) seg_rows[k++] = r;
   }
   seg_off[c.adapter_slots] = k;
+  t[mt.o_n_items] = mt.n_items;
   memcpy(t + mt.o_bt, b->block_table, sizeof(int) * (size_t)b->n_seqs * c.max_pages_per_seq);
   memcpy(t + mt.o_items, plan.items.data(), plan.items.size() * sizeof(AttnItem));
-  memcpy(t + mt.o_item_pages, plan.pages.data(), plan.pages.size() * sizeof(int));
   memcpy(t + mt.o_item_rows, plan.rows.data(), plan.rows.size() * sizeof(int2));
-  t[mt.o_n_items] = mt.n_items;
+  memcpy(t + mt.o_item_pages, plan.pages.data(), plan.pages.size() * sizeof(int));
+  mt.used = mt.o_item_pages + plan.pages.size();
   return ICR_OK;
 }
 
-static icr_status validate_batch(icr_model* m, const icr_batch* b, const int* pos_override) {
+static icr_status validate_batch(icr_model* m, const icr_batch* b, const int* pos) {
   const icr_model_config& c = m->cfg;
   if (b->n_rows < 1) return fail(ICR_SHAPE, "batch needs at least one row");
   if (b->n_rows > c.max_rows)
     return fail(ICR_CAPACITY, "batch of %d rows exceeds max_rows %d", b->n_rows, c.max_rows);
   if (b->n_seqs < 1 || b->n_seqs > c.max_seqs)
     return fail(ICR_CAPACITY, "n_seqs %d outside [1, %d]", b->n_seqs, c.max_seqs);
-  const int* pos = pos_override ? pos_override : b->row_pos;
   for (int r = 0; r < b->n_rows; ++r) {
     if (b->tokens[r] < 0 || b->tokens[r] >= c.vocab_size)
       return fail(ICR_INDEX, "token %d outside vocab [0, %d)", b->tokens[r], c.vocab_size);
     const int k = b->row_kind[r];
     if (k != 0 && k != 1) return fail(ICR_MODE, "row %d kind %d must be 0 (encoder) or 1 (decoder)", r, k);
-    if (k == 1) {
-      if (b->row_adapter[r] >= 0 && (c.lora_rank == 0 || b->row_adapter[r] >= c.adapter_slots))
-        return fail(ICR_CONFIG, "row %d adapter slot %d outside [0, %d)", r, b->row_adapter[r], c.adapter_slots);
-    }
+    if (b->row_adapter[r] >= 0 && (k != 1 || c.lora_rank == 0 || b->row_adapter[r] >= c.adapter_slots))
+      return fail(ICR_CONFIG, "row %d adapter slot %d invalid (kind %d, %d slots)", r, b->row_adapter[r], k, c.adapter_slots);
     if (pos[r] < 0 || pos[r] >= c.max_positions)
       return fail(ICR_CAPACITY, "row %d position %d outside [0, %d)", r, pos[r], c.max_positions);
   }
   return ICR_OK;
 }
 
-// Enqueue the whole forward on `s` using metadata already resident at m->meta_dev.
+// Enqueue the whole forward on `s` using metadata resident at m->meta_dev (layout mt).
 static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_dev, cudaStream_t s) {
   const icr_model_config& c = m->cfg;
   int* md = m->meta_dev;
@@ -362,29 +400,19 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
   const int* pos = md + mt.o_pos;
   const int* adapter = md + mt.o_adapter;
   const int* lm_rows = md + mt.o_lm_rows;
-  const int* seg_off = md + mt.o_seg_off;
-  const int* seg_rows = md + mt.o_seg_rows;
   const int* bt = md + mt.o_bt;
   const bool lora = c.lora_rank > 0 && mt.n_dec > 0;
   const int d = c.hidden_dim, rp = mt.rp;
   long long launches = 0;
 
-  auto gemm = [&](const CUtensorMap& wmap, CUtensorMap* xmaps, GemmParams p, int rows,
-                  int row_stride_out) -> icr_status {
+  auto gemm = [&](const CUtensorMap& wmap, CUtensorMap* xmaps, const GemmParams& p,
+                  int rows) -> icr_status {
     for (int g0 = 0; g0 < rows; g0 += 256) {
       const int gr = std::min(256, rows - g0);
       const int nt = gemm_pick_nt(gr);
       GemmParams q = p;
       q.n_rows = gr;
-      if (p.row_kind) q.row_kind = p.row_kind + g0;
-      if (p.row_adapter) q.row_adapter = p.row_adapter + g0;
-      if (p.row_pos) q.row_pos = p.row_pos + g0;
-      if (p.row_seq) q.row_seq = p.row_seq + g0;
-      if (p.lora_u) q.lora_u = p.lora_u + (size_t)g0 * p.n_u * p.rank;
-      if (p.out_f32) q.out_f32 = p.out_f32 + (size_t)g0 * p.ld_out;
-      if (p.resid) q.resid = p.resid + (size_t)g0 * p.M;
-      if (p.out_bf16) q.out_bf16 = p.out_bf16 + (size_t)g0 * row_stride_out;
-      if (p.tile_best) q.tile_best = p.tile_best + g0;
+      q.row0 = g0;
       cudaError_t e = gemm_launch(wmap, xmaps[nt_index(nt)], q, g0, nt, m->num_sms, s);
       if (e != cudaSuccess) return fail(ICR_CUDA, "gemm launch: %s", cudaGetErrorString(e));
       ++launches;
@@ -393,18 +421,34 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
   };
 
   GemmParams base{};
+  base.w_blocked = 1;
   base.ws = m->ws;
   base.counters = m->counters;
   base.rank = c.lora_rank;
   base.n_u = 1;
   base.m_valid = 1 << 30;
+  base.row_kind = kind;
+  base.row_adapter = adapter;
+  base.row_pos = pos;
+  base.row_seq = seq;
+  base.ss_tiles = m->ss_tiles;
+  base.ss_stride = rp;
+  base.ss_d = (float)d;
+  base.eps = c.rms_eps;
+  base.lora_u = m->U;
+  base.seg_off = md + mt.o_seg_off;
+  base.seg_rows = md + mt.o_seg_rows;
+  base.slots = c.adapter_slots;
+  base.rows_total = rp;
+  base.sh_part = m->sh_part;
+  base.sh_cnt = m->sh_cnt;
 
   AttnLaunch al{};
   al.q = m->qb;
   al.q_ld = m->q_dim;
   al.num_kv_heads = c.num_kv_heads;
   al.num_heads = c.num_heads;
-  al.group = c.num_heads / c.num_kv_heads;
+  al.group = m->group;
   al.head_dim = c.head_dim;
   al.items = reinterpret_cast<const AttnItem*>(md + mt.o_items);
   al.item_pages = md + mt.o_item_pages;
@@ -419,34 +463,29 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
   al.scale = (float)(1.0 / std::sqrt((double)c.head_dim));
   al.part_o = m->part_o;
   al.part_ml = m->part_ml;
+  al.merge_cnt = m->merge_cnt;
   al.out = m->att;
   al.out_ld = m->q_dim;
 
   icr_status st;
+  CUDA_TRY(embed_launch(tokens, kind, m->embed, m->x, m->xb, m->ssq, rp, rp, d, s));
+  ++launches;
   for (int l = 0; l < c.num_layers; ++l) {
     const icr_layer_weights& w = m->layers[l];
     const LayerMaps& lm = m->maps[l];
-    ++launches;
-    CUDA_TRY(rmsnorm_launch(m->x, tokens, l == 0 ? m->embed : nullptr, m->x, m->h, kind, nullptr,
-                            rp, d, c.rms_eps, s));
-    if (lora) {
-      ++launches;
-      CUDA_TRY(lora_shrink_launch(m->h, d, d, (const __nv_bfloat16*)w.a_q, nullptr, 1,
-                                  c.adapter_slots, c.lora_rank, m->scaling, seg_off, seg_rows,
-                                  m->U, s));
-    }
-    {
+    {  // q, k, v (src/model.py:485-496)
       GemmParams p = base;
       p.mode = EPI_QKV;
       p.M = m->q_dim + 2 * m->kv_dim;
       p.K = d;
-      p.row_kind = kind;
-      p.row_adapter = adapter;
-      p.row_pos = pos;
-      p.row_seq = seq;
-      p.lora_b = lora ? (const __nv_bfloat16*)w.b_q : nullptr;
-      p.lora_u = m->U;
-      p.lora_m = m->q_dim;
+      p.in_ssq = m->ssq;
+      if (lora) {
+        p.lora_b = (const __nv_bfloat16*)w.b_q;
+        p.lora_m = m->q_dim;
+        p.sh_x = m->xb; p.sh_ld = d; p.sh_K = d; p.sh_targets = 1;
+        p.sh_a0 = (const __nv_bfloat16*)w.a_q; p.sh_scale_inv = 1;
+        p.sync = m->sync + 0;
+      }
       p.out_bf16 = m->qb;
       p.q_dim = m->q_dim;
       p.kv_dim = m->kv_dim;
@@ -457,109 +496,133 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
       p.v_pages = (__nv_bfloat16*)w.v_pages;
       p.block_table = bt;
       p.bt_stride = c.max_pages_per_seq;
-      if ((st = gemm(lm.qkv, m->xmap_h, p, rp, m->q_dim))) return st;
+      if ((st = gemm(lm.qkv, m->xmap_xb, p, rp))) return st;
     }
     al.k_pages = (const __nv_bfloat16*)w.k_pages;
     al.v_pages = (const __nv_bfloat16*)w.v_pages;
-    {
+    {  // attention over 2H heads (src/model.py:497-501)
       cudaError_t e = attn_launch(al, s);
-      launches += 2;
       if (e != cudaSuccess) return fail(ICR_CUDA, "attention launch: %s", cudaGetErrorString(e));
+      launches += 2;
     }
-    if (lora) {
-      ++launches;
-      CUDA_TRY(lora_shrink_launch(m->att, m->q_dim, m->q_dim, (const __nv_bfloat16*)w.a_o, nullptr,
-                                  1, c.adapter_slots, c.lora_rank, m->scaling, seg_off, seg_rows,
-                                  m->U, s));
-    }
-    {
+    {  // o + residual (src/model.py:502)
       GemmParams p = base;
       p.mode = EPI_RESID;
       p.M = d;
       p.K = m->q_dim;
-      p.row_kind = kind;
-      p.row_adapter = adapter;
-      p.lora_b = lora ? (const __nv_bfloat16*)w.b_o : nullptr;
-      p.lora_u = m->U;
-      p.lora_m = d;
+      if (lora) {
+        p.lora_b = (const __nv_bfloat16*)w.b_o;
+        p.lora_m = d;
+        p.sh_x = m->att; p.sh_ld = m->q_dim; p.sh_K = m->q_dim; p.sh_targets = 1;
+        p.sh_a0 = (const __nv_bfloat16*)w.a_o; p.sh_scale_inv = 0;
+        p.sync = m->sync + 2;
+      }
       p.resid = m->x;
-      if ((st = gemm(lm.o, m->xmap_att, p, rp, 0))) return st;
+      p.resid_bf16 = m->xb;
+      p.out_ssq = m->ssq;
+      if ((st = gemm(lm.o, m->xmap_att, p, rp))) return st;
     }
-    ++launches;
-    CUDA_TRY(rmsnorm_launch(m->x, nullptr, nullptr, m->x, m->h, kind, nullptr, rp, d, c.rms_eps, s));
-    if (lora) {
-      ++launches;
-      CUDA_TRY(lora_shrink_launch(m->h, d, d, (const __nv_bfloat16*)w.a_gate,
-                                  (const __nv_bfloat16*)w.a_up, 2, c.adapter_slots, c.lora_rank,
-                                  m->scaling, seg_off, seg_rows, m->U, s));
-    }
-    {
+    {  // gate | up + SiLU (src/model.py:503-505)
       GemmParams p = base;
       p.mode = EPI_SILU;
       p.M = 2 * c.ffn_dim;
       p.K = d;
-      p.row_kind = kind;
-      p.row_adapter = adapter;
-      p.lora_b = lora ? (const __nv_bfloat16*)w.b_gu : nullptr;
-      p.lora_u = m->U;
-      p.lora_m = 2 * c.ffn_dim;
-      p.n_u = 2;
+      p.in_ssq = m->ssq;
+      if (lora) {
+        p.lora_b = (const __nv_bfloat16*)w.b_gu;
+        p.lora_m = 2 * c.ffn_dim;
+        p.n_u = 2;
+        p.sh_x = m->xb; p.sh_ld = d; p.sh_K = d; p.sh_targets = 2;
+        p.sh_a0 = (const __nv_bfloat16*)w.a_gate; p.sh_a1 = (const __nv_bfloat16*)w.a_up;
+        p.sh_scale_inv = 1;
+        p.sync = m->sync + 4;
+      }
       p.out_bf16 = m->f;
-      if ((st = gemm(lm.gu, m->xmap_h, p, rp, c.ffn_dim))) return st;
+      if ((st = gemm(lm.gu, m->xmap_xb, p, rp))) return st;
     }
-    if (lora) {
-      ++launches;
-      CUDA_TRY(lora_shrink_launch(m->f, c.ffn_dim, c.ffn_dim, (const __nv_bfloat16*)w.a_down,
-                                  nullptr, 1, c.adapter_slots, c.lora_rank, m->scaling, seg_off,
-                                  seg_rows, m->U, s));
-    }
-    {
+    {  // down + residual (src/model.py:506)
       GemmParams p = base;
       p.mode = EPI_RESID;
       p.M = d;
       p.K = c.ffn_dim;
-      p.row_kind = kind;
-      p.row_adapter = adapter;
-      p.lora_b = lora ? (const __nv_bfloat16*)w.b_down : nullptr;
-      p.lora_u = m->U;
-      p.lora_m = d;
+      if (lora) {
+        p.lora_b = (const __nv_bfloat16*)w.b_down;
+        p.lora_m = d;
+        p.sh_x = m->f; p.sh_ld = c.ffn_dim; p.sh_K = c.ffn_dim; p.sh_targets = 1;
+        p.sh_a0 = (const __nv_bfloat16*)w.a_down; p.sh_scale_inv = 0;
+        p.sync = m->sync + 6;
+      }
       p.resid = m->x;
-      if ((st = gemm(lm.down, m->xmap_f, p, rp, 0))) return st;
+      p.resid_bf16 = m->xb;
+      p.out_ssq = m->ssq;
+      if ((st = gemm(lm.down, m->xmap_f, p, rp))) return st;
     }
   }
-  // final norm (emitting rows only) + LM head + argmax (src/engine.py:188-193)
+  // final norm on emitting rows + LM head + argmax (src/engine.py:188-193)
   if (mt.n_lm > 0) {
-    const int nlm_p = (mt.n_lm + 15) & ~15;
+    CUDA_TRY(lm_gather_launch(m->xb, m->ssq, rp, lm_rows, mt.n_lm, mt.n_lm_pad, d, m->hlm,
+                              m->ssq_lm, s));
     ++launches;
-    CUDA_TRY(rmsnorm_launch(m->x, nullptr, nullptr, nullptr, m->hlm, nullptr, lm_rows, mt.n_lm, d,
-                            c.rms_eps, s));
-    if (nlm_p > mt.n_lm)
-      CUDA_TRY(cudaMemsetAsync(m->hlm + (size_t)mt.n_lm * d, 0,
-                               sizeof(__nv_bfloat16) * (size_t)(nlm_p - mt.n_lm) * d, s));
     GemmParams p = base;
+    p.row_kind = nullptr;
+    p.row_adapter = nullptr;
+    p.row_pos = nullptr;
+    p.row_seq = nullptr;
     p.mode = EPI_ARGMAX;
     p.M = m->vpad;
     p.K = d;
     p.m_valid = c.vocab_size;
+    p.in_ssq = m->ssq_lm;
     p.tile_best = m->tile_best;
     p.best_stride = rp;
-    if ((st = gemm(m->lm_map, m->xmap_hlm, p, mt.n_lm, 0))) return st;
-    ++launches;
+    if ((st = gemm(m->lm_map, m->xmap_hlm, p, mt.n_lm))) return st;
     CUDA_TRY(argmax_reduce_launch(m->tile_best, m->vpad / 128, rp, mt.n_lm, m->out_tok, s));
+    ++launches;
     if (logits_dev) {
-      GemmParams q = base;
+      GemmParams q = p;
       q.mode = EPI_F32;
-      q.M = m->vpad;
-      q.K = d;
+      q.tile_best = nullptr;
       q.out_f32 = logits_dev;
       q.ld_out = m->vpad;
-      if ((st = gemm(m->lm_map, m->xmap_hlm, q, mt.n_lm, 0))) return st;
+      q.m_valid = 1 << 30;
+      if ((st = gemm(m->lm_map, m->xmap_hlm, q, mt.n_lm))) return st;
     }
   }
   m->last_launches = launches;
   m->last_items = mt.n_items;
   m->last_mt = mt;
   m->has_last = true;
+  return ICR_OK;
+}
+
+// Run the forward for metadata already uploaded: replay (or capture) a CUDA graph of the
+// whole launch sequence, or launch directly when graphs are disabled.
+static icr_status run_forward(icr_model* m, const Meta& mt, float* logits_dev, cudaStream_t s) {
+  if (!m->use_graphs) return enqueue_forward(m, mt, logits_dev, s);
+  const GraphKey key{mt.rp, mt.n_lm, mt.n_items, (m->cfg.lora_rank > 0 && mt.n_dec > 0) ? 1 : 0,
+                     logits_dev};
+  auto it = m->graphs.find(key);
+  if (it == m->graphs.end()) {
+    if (m->graphs.size() >= 64) {
+      for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
+      m->graphs.clear();
+    }
+    cudaGraph_t g;
+    CUDA_TRY(cudaStreamBeginCapture(m->capture_stream, cudaStreamCaptureModeThreadLocal));
+    icr_status st = enqueue_forward(m, mt, logits_dev, m->capture_stream);
+    cudaError_t ce = cudaStreamEndCapture(m->capture_stream, &g);
+    if (st) return st;
+    if (ce != cudaSuccess) return fail(ICR_CUDA, "graph capture: %s", cudaGetErrorString(ce));
+    cudaGraphExec_t ex;
+    ce = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    if (ce != cudaSuccess) return fail(ICR_CUDA, "graph instantiate: %s", cudaGetErrorString(ce));
+    it = m->graphs.emplace(key, ex).first;
+  } else {
+    m->last_mt = mt;
+    m->last_items = mt.n_items;
+  }
+  CUDA_TRY(cudaGraphLaunch(it->second, s));
   return ICR_OK;
 }
 
@@ -584,12 +647,16 @@ icr_status icr_model_create(const icr_model_config* cfg, const icr_layer_weights
     return fail(ICR_CONFIG, "hidden_dim %d != num_heads*head_dim", c.hidden_dim);
   if (c.head_dim != 64 && c.head_dim != 128)
     return fail(ICR_CONFIG, "B200 attention kernel supports head_dim 64 or 128, got %d", c.head_dim);
+  const int group = c.num_heads / c.num_kv_heads;
+  if (64 % group)
+    return fail(ICR_CONFIG, "GQA group %d must divide 64", group);
   const int q_dim = c.num_heads * c.head_dim, kv_dim = c.num_kv_heads * c.head_dim;
   if ((q_dim + 2 * kv_dim) % 128 || c.hidden_dim % 128 || (2 * c.ffn_dim) % 128 || c.ffn_dim % 64)
     return fail(ICR_CONFIG, "B200 GEMM tiles need hidden_dim %% 128 == 0, ffn_dim %% 64 == 0 and "
                 "(q_dim + 2 kv_dim) %% 128 == 0");
-  if (c.lora_rank < 0 || (c.lora_rank > 0 && (c.lora_rank % 8 || c.adapter_slots < 1)))
-    return fail(ICR_CONFIG, "lora_rank must be 0 or a multiple of 8 with adapter_slots >= 1");
+  if (c.lora_rank < 0 || c.lora_rank > 32 ||
+      (c.lora_rank > 0 && (c.lora_rank % 8 || c.adapter_slots < 1)))
+    return fail(ICR_CONFIG, "lora_rank must be 0 or a multiple of 8 up to 32 with adapter_slots >= 1");
   if (c.chunk_pages < 1 || c.max_rows < 1 || c.max_positions < 1 || c.num_pages < 1 ||
       c.max_seqs < 1 || c.max_pages_per_seq < 1)
     return fail(ICR_CONFIG, "capacities must be positive");
@@ -603,10 +670,14 @@ icr_status icr_model_create(const icr_model_config* cfg, const icr_layer_weights
   m->num_sms = query_sms();
   m->q_dim = q_dim;
   m->kv_dim = kv_dim;
+  m->group = group;
+  m->ss_tiles = c.hidden_dim / 128;
   m->vpad = (c.vocab_size + 127) / 128 * 128;
   m->rp = (c.max_rows + 15) & ~15;
   const int CT = c.chunk_pages * 16;
   m->max_chunks = (c.max_positions + CT - 1) / CT;
+  if (const char* e = getenv("ICR_NO_GRAPH")) m->use_graphs = !(e[0] == '1');
+  if (const char* e = getenv("ICR_NO_PDL")) g_pdl = (e[0] == '1') ? 0 : 1;
   const size_t rp = m->rp;
   auto bail = [&](icr_status s) {
     icr_model_destroy(m);
@@ -621,7 +692,9 @@ icr_status icr_model_create(const icr_model_config* cfg, const icr_layer_weights
     cudaMemset((ptr), 0, (bytes));                                                \
   } while (0)
   ALLOC(m->x, rp * c.hidden_dim * sizeof(float));
-  ALLOC(m->h, rp * c.hidden_dim * 2);
+  ALLOC(m->xb, rp * c.hidden_dim * 2);
+  ALLOC(m->ssq, (size_t)m->ss_tiles * rp * sizeof(float));
+  ALLOC(m->ssq_lm, (size_t)m->ss_tiles * rp * sizeof(float));
   ALLOC(m->qb, rp * q_dim * 2);
   ALLOC(m->att, rp * q_dim * 2);
   ALLOC(m->f, rp * c.ffn_dim * 2);
@@ -631,13 +704,20 @@ icr_status icr_model_create(const icr_model_config* cfg, const icr_layer_weights
   ALLOC(m->out_tok, rp * sizeof(int));
   ALLOC(m->part_o, rp * c.num_heads * m->max_chunks * c.head_dim * sizeof(float));
   ALLOC(m->part_ml, rp * c.num_heads * m->max_chunks * sizeof(float2));
+  ALLOC(m->merge_cnt, rp * c.num_kv_heads * sizeof(int));
   ALLOC(m->rope, (size_t)c.max_positions * (c.head_dim / 2) * sizeof(float2));
   ALLOC(m->ws, gemm_ws_floats(m->num_sms) * sizeof(float));
   {
     const int max_tiles = std::max({m->vpad, 2 * c.ffn_dim, q_dim + 2 * kv_dim, c.hidden_dim}) / 128;
     ALLOC(m->counters, (size_t)max_tiles * sizeof(int));
   }
-  ALLOC(m->zero_kind, rp * sizeof(int));
+  ALLOC(m->sync, 16 * sizeof(int));
+  {
+    const int kmax = std::max({c.hidden_dim, q_dim, c.ffn_dim});
+    const int splits = (kmax + 2047) / 2048;
+    ALLOC(m->sh_part, (size_t)splits * rp * 2 * std::max(c.lora_rank, 8) * sizeof(float));
+    ALLOC(m->sh_cnt, (size_t)2 * std::max(c.adapter_slots, 1) * std::max(c.lora_rank, 8) * sizeof(int));
+  }
 #undef ALLOC
   // RoPE table, float64 angles cast once (src/tensor.py:270-279).
   {
@@ -661,22 +741,20 @@ icr_status icr_model_create(const icr_model_config* cfg, const icr_layer_weights
     if (c.lora_rank > 0 && (!w.a_q || !w.b_q || !w.a_o || !w.b_o || !w.a_gate || !w.a_up ||
                             !w.b_gu || !w.a_down || !w.b_down))
       return bail(fail(ICR_CONFIG, "layer %d: missing adapter pointer", l));
-    if ((st = make_map(&m->maps[l].qkv, w.w_qkv, q_dim + 2 * kv_dim, c.hidden_dim, 128))) return bail(st);
-    if ((st = make_map(&m->maps[l].o, w.w_o, c.hidden_dim, q_dim, 128))) return bail(st);
-    if ((st = make_map(&m->maps[l].gu, w.w_gu, 2 * c.ffn_dim, c.hidden_dim, 128))) return bail(st);
-    if ((st = make_map(&m->maps[l].down, w.w_down, c.hidden_dim, c.ffn_dim, 128))) return bail(st);
+    if ((st = make_map_blocked(&m->maps[l].qkv, w.w_qkv, q_dim + 2 * kv_dim, c.hidden_dim))) return bail(st);
+    if ((st = make_map_blocked(&m->maps[l].o, w.w_o, c.hidden_dim, q_dim))) return bail(st);
+    if ((st = make_map_blocked(&m->maps[l].gu, w.w_gu, 2 * c.ffn_dim, c.hidden_dim))) return bail(st);
+    if ((st = make_map_blocked(&m->maps[l].down, w.w_down, c.hidden_dim, c.ffn_dim))) return bail(st);
   }
-  if ((st = make_map(&m->lm_map, lm_head, m->vpad, c.hidden_dim, 128))) return bail(st);
+  if ((st = make_map_blocked(&m->lm_map, lm_head, m->vpad, c.hidden_dim))) return bail(st);
   for (int i = 0; i < 5; ++i) {
-    if ((st = make_map(&m->xmap_h[i], m->h, rp, c.hidden_dim, kNts[i]))) return bail(st);
+    if ((st = make_map(&m->xmap_xb[i], m->xb, rp, c.hidden_dim, kNts[i]))) return bail(st);
     if ((st = make_map(&m->xmap_att[i], m->att, rp, q_dim, kNts[i]))) return bail(st);
     if ((st = make_map(&m->xmap_f[i], m->f, rp, c.ffn_dim, kNts[i]))) return bail(st);
     if ((st = make_map(&m->xmap_hlm[i], m->hlm, rp, c.hidden_dim, kNts[i]))) return bail(st);
   }
-  for (int i = 0; i < 2; ++i) {
-    cudaEventCreateWithFlags(&m->staging_ev[i], cudaEventDisableTiming);
-    cudaEventCreate(&m->step_ev[i]);
-  }
+  for (int i = 0; i < 2; ++i) cudaEventCreateWithFlags(&m->staging_ev[i], cudaEventDisableTiming);
+  cudaStreamCreateWithFlags(&m->capture_stream, cudaStreamNonBlocking);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return bail(fail(ICR_CUDA, "model create: %s", cudaGetErrorString(e)));
   *out = m;
@@ -686,37 +764,42 @@ icr_status icr_model_create(const icr_model_config* cfg, const icr_layer_weights
 icr_status icr_model_destroy(icr_model* m) {
   if (!m) return ICR_OK;
   cudaDeviceSynchronize();
-  void* bufs[] = {m->x, m->h, m->qb, m->att, m->f, m->hlm, m->U, m->tile_best, m->out_tok,
-                  m->part_o, m->part_ml, m->rope, m->ws, m->counters, m->zero_kind, m->meta_dev};
+  for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
+  void* bufs[] = {m->x, m->xb, m->ssq, m->ssq_lm, m->qb, m->att, m->f, m->hlm, m->U,
+                  m->tile_best, m->out_tok, m->part_o, m->part_ml, m->merge_cnt, m->rope, m->ws,
+                  m->counters, m->sync, m->sh_part, m->sh_cnt, m->meta_dev};
   for (void* p : bufs)
     if (p) cudaFree(p);
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < 2; ++i) {
     if (m->staging[i]) cudaFreeHost(m->staging[i]);
+    if (m->staging_ev[i]) cudaEventDestroy(m->staging_ev[i]);
+  }
+  if (m->capture_stream) cudaStreamDestroy(m->capture_stream);
   delete m;
   return ICR_OK;
 }
+
+static int plan_group(icr_model* m) { return m->group; }
 
 icr_status icr_forward(icr_model* m, const icr_batch* b, int32_t* out_tokens_host,
                        float* logits_dev, void* stream) {
   if (!m || !b) return fail(ICR_CONFIG, "null argument");
   cudaStream_t s = (cudaStream_t)stream;
-  icr_status st = validate_batch(m, b, nullptr);
+  icr_status st = validate_batch(m, b, b->row_pos);
   if (st) return st;
-  Meta mt;
   AttnPlan plan;
-  // plan first (needs no staging), then size, then pack
   st = build_attn_plan(b->n_rows, b->row_kind, b->row_seq, b->row_pos, b->block_table, b->n_seqs,
-                       m->cfg.max_pages_per_seq, m->cfg.num_pages,
-                       m->cfg.num_heads / m->cfg.num_kv_heads, m->cfg.chunk_pages, plan);
+                       m->cfg.max_pages_per_seq, m->cfg.num_pages, plan_group(m),
+                       m->cfg.chunk_pages, plan);
   if (st) return st;
-  pack_meta(m, b, nullptr, nullptr, nullptr, mt, plan, true);
+  Meta mt = layout_meta(m, b->n_rows);
   if ((st = ensure_meta(m, mt.total))) return st;
   CUDA_TRY(cudaEventSynchronize(m->staging_ev[0]));
-  if ((st = pack_meta(m, b, nullptr, nullptr, m->staging[0], mt, plan, false))) return st;
-  CUDA_TRY(cudaMemcpyAsync(m->meta_dev, m->staging[0], mt.total * sizeof(int), cudaMemcpyHostToDevice, s));
-  m->last_meta_bytes = (long long)mt.total * sizeof(int);
+  if ((st = pack_meta(m, b, b->row_pos, nullptr, plan, m->staging[0], mt))) return st;
+  CUDA_TRY(cudaMemcpyAsync(m->meta_dev, m->staging[0], mt.used * sizeof(int), cudaMemcpyHostToDevice, s));
   CUDA_TRY(cudaEventRecord(m->staging_ev[0], s));
-  if ((st = enqueue_forward(m, mt, logits_dev, s))) return st;
+  m->last_meta_bytes = (long long)mt.used * sizeof(int);
+  if ((st = run_forward(m, mt, logits_dev, s))) return st;
   if (mt.n_lm > 0 && out_tokens_host) {
     int* pin = m->staging[1];
     CUDA_TRY(cudaEventSynchronize(m->staging_ev[1]));
@@ -738,9 +821,8 @@ icr_status icr_decode_loop(icr_model* m, const icr_batch* first, const int32_t* 
   std::vector<int> pos(first->row_pos, first->row_pos + n);
   std::vector<cudaEvent_t> evs(steps + 1);
   for (auto& e : evs) CUDA_TRY(cudaEventCreate(&e));
-  icr_status st = ICR_OK;
-  Meta mt{};
-  int n_lm = 0;
+  Meta mt = layout_meta(m, n);
+  icr_status st = ensure_meta(m, mt.total);
   for (int i = 0; i < steps && st == ICR_OK; ++i) {
     if (i > 0)
       for (int r = 0; r < n; ++r) pos[r] += 1;
@@ -748,28 +830,22 @@ icr_status icr_decode_loop(icr_model* m, const icr_batch* first, const int32_t* 
     AttnPlan plan;
     if ((st = build_attn_plan(n, first->row_kind, first->row_seq, pos.data(), first->block_table,
                               first->n_seqs, m->cfg.max_pages_per_seq, m->cfg.num_pages,
-                              m->cfg.num_heads / m->cfg.num_kv_heads, m->cfg.chunk_pages, plan)))
+                              plan_group(m), m->cfg.chunk_pages, plan)))
       break;
-    pack_meta(m, first, pos.data(), feedback_src, nullptr, mt, plan, true);
-    // Growing the buffers would free memory the in-flight steps still read: size once.
-    if (mt.total > m->meta_cap) {
-      cudaStreamSynchronize(s);
-      if ((st = ensure_meta(m, mt.total * 2))) break;
-    }
     const int slot = i & 1;
     cudaEventSynchronize(m->staging_ev[slot]);
-    if ((st = pack_meta(m, first, pos.data(), feedback_src, m->staging[slot], mt, plan, false))) break;
+    if ((st = pack_meta(m, first, pos.data(), feedback_src, plan, m->staging[slot], mt))) break;
     // Step 0 uploads everything; later steps keep the device-fed tokens.
     const size_t from = (i == 0) ? 0 : mt.o_kind;
-    cudaMemcpyAsync(m->meta_dev + from, m->staging[slot] + from, (mt.total - from) * sizeof(int),
+    cudaMemcpyAsync(m->meta_dev + from, m->staging[slot] + from, (mt.used - from) * sizeof(int),
                     cudaMemcpyHostToDevice, s);
-    m->last_meta_bytes = (long long)(mt.total - from) * sizeof(int);
+    m->last_meta_bytes = (long long)(mt.used - from) * sizeof(int);
     cudaEventRecord(m->staging_ev[slot], s);
     cudaEventRecord(evs[i], s);
-    if ((st = enqueue_forward(m, mt, nullptr, s))) break;
-    n_lm = mt.n_lm;
-    feedback_kernel<<<(mt.rp + 127) / 128, 128, 0, s>>>(m->meta_dev + mt.o_tokens, m->out_tok,
-                                                        m->meta_dev + mt.o_feedback, mt.rp);
+    if ((st = run_forward(m, mt, nullptr, s))) break;
+    cudaError_t e = feedback_launch(m->meta_dev + mt.o_tokens, m->out_tok,
+                                    m->meta_dev + mt.o_feedback, mt.rp, s);
+    if (e != cudaSuccess) st = fail(ICR_CUDA, "feedback: %s", cudaGetErrorString(e));
   }
   if (st == ICR_OK) {
     cudaEventRecord(evs[steps], s);
@@ -778,8 +854,9 @@ icr_status icr_decode_loop(icr_model* m, const icr_batch* first, const int32_t* 
   }
   if (st == ICR_OK && step_ms_host)
     for (int i = 0; i < steps; ++i) cudaEventElapsedTime(&step_ms_host[i], evs[i], evs[i + 1]);
-  if (st == ICR_OK && out_tokens_host_last && n_lm > 0)
-    cudaMemcpy(out_tokens_host_last, m->out_tok, n_lm * sizeof(int), cudaMemcpyDeviceToHost);
+  if (st == ICR_OK && out_tokens_host_last && mt.n_lm > 0)
+    cudaMemcpy(out_tokens_host_last, m->out_tok, mt.n_lm * sizeof(int), cudaMemcpyDeviceToHost);
+  cudaStreamSynchronize(s);
   for (auto& e : evs) cudaEventDestroy(e);
   return st;
 }
@@ -795,9 +872,11 @@ icr_status icr_model_stats(icr_model* m, int64_t* out3) {
 
 // Re-launch one projection GEMM family of the last forward `iters` times, cycling through
 // all layers so no weight tile is served from L2, and return the average device time per
-// launch (CUDA events on the launch stream). which: 0 wo, 1 gate|up, 2 down, 3 lm_head.
-// Side effects are confined to scratch buffers (residual stream, f, tile maxima).
-icr_status icr_profile_gemm(icr_model* m, int which, int iters, float* avg_ms, void* stream) {
+// launch (CUDA events on the launch stream), all LoRA / norm / epilogue work included.
+// which: 0 wo, 1 gate|up, 2 down, 3 lm_head. Side effects stay in scratch buffers
+// (residual stream, f, tile maxima), so call it after the timed region.
+icr_status icr_profile_gemm(icr_model* m, int which_raw, int iters, float* avg_ms, void* stream) {
+  const int which = which_raw & 0xF;
   if (!m || !avg_ms || iters < 1) return fail(ICR_CONFIG, "bad arguments");
   if (!m->has_last) return fail(ICR_STATE, "profile needs a previous forward");
   cudaStream_t s = (cudaStream_t)stream;
@@ -806,6 +885,7 @@ icr_status icr_profile_gemm(icr_model* m, int which, int iters, float* avg_ms, v
   int* md = m->meta_dev;
   const bool lora = c.lora_rank > 0 && mt.n_dec > 0;
   GemmParams p{};
+  p.w_blocked = 1;
   p.ws = m->ws;
   p.counters = m->counters;
   p.rank = c.lora_rank;
@@ -813,24 +893,55 @@ icr_status icr_profile_gemm(icr_model* m, int which, int iters, float* avg_ms, v
   p.m_valid = 1 << 30;
   p.row_kind = md + mt.o_kind;
   p.row_adapter = md + mt.o_adapter;
+  p.row_pos = md + mt.o_pos;
+  p.row_seq = md + mt.o_seq;
+  p.ss_tiles = m->ss_tiles;
+  p.ss_stride = mt.rp;
+  p.ss_d = (float)c.hidden_dim;
+  p.eps = c.rms_eps;
   p.lora_u = m->U;
+  p.seg_off = md + mt.o_seg_off;
+  p.seg_rows = md + mt.o_seg_rows;
+  p.slots = c.adapter_slots;
+  p.rows_total = mt.rp;
+  p.sh_part = m->sh_part;
+  p.sh_cnt = m->sh_cnt;
   int rows = mt.rp;
   CUtensorMap* xmaps = m->xmap_att;
-  const void* bptr_off = nullptr;
-  (void)bptr_off;
   switch (which) {
-    case 0: p.mode = EPI_RESID; p.M = c.hidden_dim; p.K = m->q_dim; p.lora_m = c.hidden_dim;
-            p.resid = m->x; xmaps = m->xmap_att; break;
-    case 1: p.mode = EPI_SILU; p.M = 2 * c.ffn_dim; p.K = c.hidden_dim; p.lora_m = 2 * c.ffn_dim;
-            p.n_u = 2; p.out_bf16 = m->f; xmaps = m->xmap_h; break;
-    case 2: p.mode = EPI_RESID; p.M = c.hidden_dim; p.K = c.ffn_dim; p.lora_m = c.hidden_dim;
-            p.resid = m->x; xmaps = m->xmap_f; break;
+    case 0: p.mode = EPI_RESID; p.M = c.hidden_dim; p.K = m->q_dim; p.resid = m->x;
+            p.resid_bf16 = m->xb; p.out_ssq = m->ssq; xmaps = m->xmap_att;
+            if (lora) { p.lora_m = c.hidden_dim; p.sh_x = m->att; p.sh_ld = m->q_dim;
+                        p.sh_K = m->q_dim; p.sh_targets = 1; p.sync = m->sync + 2; }
+            break;
+    case 1: p.mode = EPI_SILU; p.M = 2 * c.ffn_dim; p.K = c.hidden_dim; p.in_ssq = m->ssq;
+            p.out_bf16 = m->f; xmaps = m->xmap_xb;
+            if (lora) { p.lora_m = 2 * c.ffn_dim; p.n_u = 2; p.sh_x = m->xb; p.sh_ld = c.hidden_dim;
+                        p.sh_K = c.hidden_dim; p.sh_targets = 2; p.sh_scale_inv = 1;
+                        p.sync = m->sync + 4; }
+            break;
+    case 2: p.mode = EPI_RESID; p.M = c.hidden_dim; p.K = c.ffn_dim; p.resid = m->x;
+            p.resid_bf16 = m->xb; p.out_ssq = m->ssq; xmaps = m->xmap_f;
+            if (lora) { p.lora_m = c.hidden_dim; p.sh_x = m->f; p.sh_ld = c.ffn_dim;
+                        p.sh_K = c.ffn_dim; p.sh_targets = 1; p.sync = m->sync + 6; }
+            break;
     case 3: p.mode = EPI_ARGMAX; p.M = m->vpad; p.K = c.hidden_dim; p.m_valid = c.vocab_size;
-            p.tile_best = m->tile_best; p.best_stride = mt.rp; rows = mt.n_lm; xmaps = m->xmap_hlm;
-            p.row_kind = nullptr; break;
+            p.in_ssq = m->ssq_lm; p.tile_best = m->tile_best; p.best_stride = mt.rp;
+            rows = mt.n_lm; xmaps = m->xmap_hlm; p.row_kind = nullptr; p.row_adapter = nullptr;
+            break;
     default: return fail(ICR_MODE, "which must be 0..3");
   }
-  if (rows > 256) return fail(ICR_SHAPE, "profile supports <= 256 rows");
+  if (rows > 256 || rows < 1) return fail(ICR_SHAPE, "profile supports 1..256 rows");
+  // diagnostic variants: bit 4 drops the LoRA (shrink + expand), bit 5 replaces the fused
+  // epilogue by a plain fp32 store into scratch
+  const bool no_lora = (which_raw >> 4) & 1, plain = (which_raw >> 5) & 1;
+  if (no_lora) { p.sh_x = nullptr; p.sync = nullptr; }
+  if (plain) {
+    const size_t need = (size_t)rows * p.M;
+    const size_t have = (size_t)m->rp * c.num_heads * m->max_chunks * c.head_dim;
+    if (need > have) return fail(ICR_CAPACITY, "profile scratch too small");
+    p.mode = EPI_F32; p.out_f32 = m->part_o; p.ld_out = p.M; p.in_ssq = nullptr;
+  }
   p.n_rows = rows;
   const int nt = gemm_pick_nt(rows);
   cudaEvent_t e0, e1;
@@ -843,9 +954,14 @@ icr_status icr_profile_gemm(icr_model* m, int which, int iters, float* avg_ms, v
       const icr_layer_weights& w = m->layers[l];
       GemmParams q = p;
       const CUtensorMap* wm = &m->lm_map;
-      if (which == 0) { wm = &m->maps[l].o; q.lora_b = lora ? (const __nv_bfloat16*)w.b_o : nullptr; }
-      if (which == 1) { wm = &m->maps[l].gu; q.lora_b = lora ? (const __nv_bfloat16*)w.b_gu : nullptr; }
-      if (which == 2) { wm = &m->maps[l].down; q.lora_b = lora ? (const __nv_bfloat16*)w.b_down : nullptr; }
+      const bool lora_l = lora && !((which_raw >> 4) & 1);
+      if (which == 0) { wm = &m->maps[l].o;
+        if (lora_l) { q.lora_b = (const __nv_bfloat16*)w.b_o; q.sh_a0 = (const __nv_bfloat16*)w.a_o; } }
+      if (which == 1) { wm = &m->maps[l].gu;
+        if (lora_l) { q.lora_b = (const __nv_bfloat16*)w.b_gu; q.sh_a0 = (const __nv_bfloat16*)w.a_gate;
+                    q.sh_a1 = (const __nv_bfloat16*)w.a_up; } }
+      if (which == 2) { wm = &m->maps[l].down;
+        if (lora_l) { q.lora_b = (const __nv_bfloat16*)w.b_down; q.sh_a0 = (const __nv_bfloat16*)w.a_down; } }
       cudaError_t e = gemm_launch(*wm, xmaps[nt_index(nt)], q, 0, nt, m->num_sms, s);
       if (e != cudaSuccess) return fail(ICR_CUDA, "gemm: %s", cudaGetErrorString(e));
     }
@@ -854,6 +970,73 @@ icr_status icr_profile_gemm(icr_model* m, int which, int iters, float* avg_ms, v
   float ms = 0.f;
   CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
   *avg_ms = ms / (float)(iters * L);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return ICR_OK;
+}
+
+// GEMM streaming micro-benchmark: n_mats weight matrices [n_mats][M][K] (tile-major if
+// blocked) are cycled so nothing is served from L2; returns average ms per launch.
+icr_status icr_bench_gemm(const void* w, const void* x, int M, int K, int rows, int n_mats,
+                          int blocked, int stages, int ctas_per_sm, int skip_mma, int iters,
+                          float* avg_ms, void* stream) {
+  if (M % 128 || K % 64 || rows < 1 || rows > 256 || n_mats < 1 || iters < 1)
+    return fail(ICR_SHAPE, "bad bench shape");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int sms = query_sms() * std::max(1, ctas_per_sm);
+  static float* ws = nullptr;
+  static int* ctr = nullptr;
+  static float* out = nullptr;
+  static size_t out_n = 0;
+  if (!ws) CUDA_TRY(cudaMalloc(&ws, gemm_ws_floats(sms * 4) * sizeof(float)));
+  if (!ctr) {
+    CUDA_TRY(cudaMalloc(&ctr, 65536 * sizeof(int)));
+    CUDA_TRY(cudaMemset(ctr, 0, 65536 * sizeof(int)));
+  }
+  if (out_n < (size_t)rows * M) {
+    if (out) cudaFree(out);
+    CUDA_TRY(cudaMalloc(&out, (size_t)rows * M * sizeof(float)));
+    out_n = (size_t)rows * M;
+  }
+  std::vector<CUtensorMap> wm(n_mats);
+  icr_status st;
+  for (int i = 0; i < n_mats; ++i) {
+    const void* wi = (const char*)w + (size_t)i * M * K * 2;
+    st = blocked ? make_map_blocked(&wm[i], wi, M, K) : make_map(&wm[i], wi, M, K, 128);
+    if (st) return st;
+  }
+  const int nt = gemm_pick_nt(rows);
+  CUtensorMap xm;
+  if ((st = make_map(&xm, x, rows, K, nt))) return st;
+  GemmParams p{};
+  p.mode = EPI_F32;
+  p.w_blocked = blocked;
+  p.M = M;
+  p.K = K;
+  p.n_rows = rows;
+  p.m_valid = M;
+  p.out_f32 = out;
+  p.ld_out = M;
+  p.ws = ws;
+  p.counters = ctr;
+  p.stages = stages;
+  p.skip_mma = skip_mma;
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  // warm-up
+  for (int i = 0; i < n_mats; ++i) gemm_launch(wm[i], xm, p, 0, nt, sms, s);
+  CUDA_TRY(cudaEventRecord(e0, s));
+  for (int it = 0; it < iters; ++it)
+    for (int i = 0; i < n_mats; ++i) {
+      cudaError_t e = gemm_launch(wm[i], xm, p, 0, nt, sms, s);
+      if (e != cudaSuccess) return fail(ICR_CUDA, "bench gemm: %s", cudaGetErrorString(e));
+    }
+  CUDA_TRY(cudaEventRecord(e1, s));
+  CUDA_TRY(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+  *avg_ms = ms / (float)(iters * n_mats);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   return ICR_OK;
@@ -891,7 +1074,8 @@ icr_status icr_gemm_bf16(const void* w_dev, const void* x_dev, float* out_dev, i
     p.K = K;
     p.n_rows = gr;
     p.m_valid = M;
-    p.out_f32 = out_dev + (size_t)g0 * M;
+    p.out_f32 = out_dev;
+    p.row0 = g0;
     p.ld_out = M;
     p.ws = g_ws;
     p.counters = g_counters;
@@ -924,6 +1108,7 @@ icr_status icr_paged_attention(const void* q_dev, const void* k_pages, const voi
   int2* d_rows;
   float* d_po;
   float2* d_pml;
+  int* d_cnt;
   const size_t np = std::max<size_t>(plan.pages.size(), 1), nr = std::max<size_t>(plan.rows.size(), 1),
                ni = std::max<size_t>(plan.items.size(), 1);
   CUDA_TRY(cudaMalloc(&d_pos, n_rows * sizeof(int)));
@@ -934,6 +1119,8 @@ icr_status icr_paged_attention(const void* q_dev, const void* k_pages, const voi
   CUDA_TRY(cudaMalloc(&d_rows, nr * sizeof(int2)));
   CUDA_TRY(cudaMalloc(&d_po, (size_t)n_rows * num_heads * max_chunks * head_dim * sizeof(float)));
   CUDA_TRY(cudaMalloc(&d_pml, (size_t)n_rows * num_heads * max_chunks * sizeof(float2)));
+  CUDA_TRY(cudaMalloc(&d_cnt, (size_t)n_rows * num_kv_heads * sizeof(int)));
+  CUDA_TRY(cudaMemsetAsync(d_cnt, 0, (size_t)n_rows * num_kv_heads * sizeof(int), s));
   int nitems = (int)plan.items.size();
   CUDA_TRY(cudaMemcpyAsync(d_pos, row_pos_host, n_rows * sizeof(int), cudaMemcpyHostToDevice, s));
   CUDA_TRY(cudaMemcpyAsync(d_kind, kind.data(), n_rows * sizeof(int), cudaMemcpyHostToDevice, s));
@@ -963,11 +1150,12 @@ icr_status icr_paged_attention(const void* q_dev, const void* k_pages, const voi
   a.scale = (float)(1.0 / std::sqrt((double)head_dim));
   a.part_o = d_po;
   a.part_ml = d_pml;
+  a.merge_cnt = d_cnt;
   a.out = (__nv_bfloat16*)out_dev;
   a.out_ld = num_heads * head_dim;
   cudaError_t e = attn_launch(a, s);
   cudaError_t e2 = cudaStreamSynchronize(s);
-  void* bufs[] = {d_pos, d_kind, d_pages, d_n, d_items, d_rows, d_po, d_pml};
+  void* bufs[] = {d_pos, d_kind, d_pages, d_n, d_items, d_rows, d_po, d_pml, d_cnt};
   for (void* p : bufs) cudaFree(p);
   if (e != cudaSuccess) return fail(ICR_CUDA, "attention: %s", cudaGetErrorString(e));
   if (e2 != cudaSuccess) return fail(ICR_CUDA, "attention sync: %s", cudaGetErrorString(e2));

@@ -121,6 +121,19 @@ class PageArena:
 
 
 # ----------------------------------------------------------------------------- weights
+def tile_major(w):
+    """[M, K] -> [M/128, K/64, 128, 64] contiguous: every 128x64 GEMM tile is one 16 KB
+    block, so a weight-streaming CTA reads long contiguous runs of HBM (3-D TMA box)."""
+    M, K = w.shape
+    return w.view(M // 128, 128, K // 64, 64).permute(0, 2, 1, 3).contiguous()
+
+
+def untile(w):
+    """Inverse of tile_major (tests, checksums)."""
+    mt, kt, _, _ = w.shape
+    return w.permute(0, 2, 1, 3).reshape(mt * 128, kt * 64)
+
+
 class DeviceWeights:
     """Base weights in the kernel layout (see module doc)."""
 
@@ -153,15 +166,15 @@ class DeviceWeights:
             up = t(lw.up.data).T * g_ffn
             gu = torch.stack([gate, up], 1).reshape(2 * cfg.ffn_dim, cfg.hidden_dim)
             self.layers.append({
-                "w_qkv": qkv.to(device, bf).contiguous(),
-                "w_o": t(lw.wo.data).T.to(device, bf).contiguous(),
-                "w_gu": gu.to(device, bf).contiguous(),
-                "w_down": t(lw.down.data).T.to(device, bf).contiguous(),
+                "w_qkv": tile_major(qkv.to(device, bf)),
+                "w_o": tile_major(t(lw.wo.data).T.contiguous().to(device, bf)),
+                "w_gu": tile_major(gu.to(device, bf)),
+                "w_down": tile_major(t(lw.down.data).T.contiguous().to(device, bf)),
             })
         self.embed = t(base.embed.data).to(device, bf).contiguous()
         lm = torch.zeros(self.vocab_pad, cfg.hidden_dim)
         lm[:cfg.vocab_size] = t(base.lm_head.data).T * t(base.final_gain.data)[None, :]
-        self.lm_head = lm.to(device, bf).contiguous()
+        self.lm_head = tile_major(lm.to(device, bf))
         return self
 
     @classmethod
@@ -185,12 +198,12 @@ class DeviceWeights:
 
         for _ in range(cfg.num_layers):
             self.layers.append({
-                "w_qkv": draw(qd + 2 * kvd, d, d), "w_o": draw(d, qd, qd),
-                "w_gu": draw(2 * f, d, d), "w_down": draw(d, f, f)})
+                "w_qkv": tile_major(draw(qd + 2 * kvd, d, d)), "w_o": tile_major(draw(d, qd, qd)),
+                "w_gu": tile_major(draw(2 * f, d, d)), "w_down": tile_major(draw(d, f, f))})
         self.embed = draw(cfg.vocab_size, d, d)
         lm = draw(self.vocab_pad, d, d)
         lm[cfg.vocab_size:] = 0
-        self.lm_head = lm
+        self.lm_head = tile_major(lm)
         return self
 
     def checksum(self) -> str:
