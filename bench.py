@@ -256,6 +256,11 @@ def run_b200(args) -> None:
 
     # ---------------- roofline of the dominant kernel (gate|up GEMM) ----------------
     import ctypes as C
+    kind_ms = (C.c_float * 10)()
+    _lib.check(rt._lib.icr_profile_step(rt._handle, kind_ms, _lib.stream_handle()))
+    names = ("embed", "qkv", "attention", "o", "gate_up", "down", "lm_gather", "lm_head", "argmax")
+    step_breakdown = {n: round(kind_ms[i], 4) for i, n in enumerate(names)}
+    step_breakdown["total_serial"] = round(kind_ms[9], 4)
     avg = C.c_float()
     per_kind = {}
     for which, name in ((0, "o"), (2, "down"), (3, "lm_head"), (1, "gate_up")):
@@ -304,6 +309,7 @@ def run_b200(args) -> None:
                      "algorithmic_bytes_per_launch": gu_bytes,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",
                      "gemm_launch_us": per_kind},
+        "step_breakdown_ms": step_breakdown,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         res = cpu_baseline_sample(1, 2, 0)

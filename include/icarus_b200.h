@@ -141,6 +141,11 @@ icr_status icr_decode_loop(icr_model* m, const icr_batch* first, const int32_t* 
  * icr_forward / icr_decode_loop step. */
 icr_status icr_model_stats(icr_model* m, int64_t* out3);
 
+/* Per-kernel-kind device time of the last forward, replayed without the graph with an
+ * event after every launch: kind_ms[0..8] = embed, qkv, attention, o, gate|up, down,
+ * LM gather, LM head, argmax; kind_ms[9] = total (ms). Recomputes identical K/V. */
+icr_status icr_profile_step(icr_model* m, float* kind_ms, void* stream);
+
 /* Average device time of one projection-GEMM launch (which: 0 wo, 1 gate|up, 2 down,
  * 3 lm_head) re-run `iters` times over all layers with the last forward's rows. */
 icr_status icr_profile_gemm(icr_model* m, int which, int iters, float* avg_ms, void* stream);

@@ -12,6 +12,8 @@
 // kernel folds chunks 0..last in fixed order. Partials depend only on the row's own query, the chunk's keys and the row's position, never on which other rows share the
 // CTA -- the batch-invariance the reference gets from its per-head loop (2H == H||H,
 // tests/test_model.py:225-239) and that makes prefill / decode KV bytes identical.
+#include <algorithm>
+
 #include "kernels.h"
 #include "ptx.cuh"
 
@@ -59,22 +61,29 @@ __device__ __forceinline__ uint32_t swz(int row, int chunk) {
   return (uint32_t)(row * HD * 2 + ((chunk ^ (row & 7)) << 4));
 }
 
-constexpr int PAGE_STAGES = 6;  // K/V pages in flight per CTA
+constexpr int PAGE_STAGES = 8;  // K/V pages in flight per CTA (two per pipeline step)
 
 template <int HD>
 constexpr size_t attn_smem() { return (size_t)64 * HD * 2 + (size_t)PAGE_STAGES * 2 * 16 * HD * 2; }
 
+// 8 warps: warp w owns query rows [16*(w&3), +16) and the chunk's pages of parity (w>>2).
+// The two page-parity halves keep separate online-softmax states and are combined at the
+// end in a fixed order (even pages first), so a row's partial depends only on its own query,
+// the chunk's keys and its position.
 template <int HD>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(256, 2)
     attn_partial_kernel(const __nv_bfloat16* __restrict__ q, int q_ld,
                         const __nv_bfloat16* __restrict__ k_pages,
                         const __nv_bfloat16* __restrict__ v_pages, int num_kv_heads, int group,
                         const AttnItem* __restrict__ items, const int* __restrict__ item_pages,
                         const int2* __restrict__ item_rows, const int* __restrict__ row_pos,
                         int num_heads, int max_chunks, float scale, float* __restrict__ part_o,
-                        float2* __restrict__ part_ml, const int* __restrict__ n_items_dev) {
+                        float2* __restrict__ part_ml, const int* __restrict__ n_items_dev,
+                        const uint8_t* __restrict__ pf_base, long long pf_bytes) {
   constexpr int CH = HD / 8;  // 16-byte chunks per row
   extern __shared__ __align__(128) uint8_t attn_smem_raw[];
+  // attention moves few bytes: use the idle HBM to pull the o-projection weights into L2
+  prefetch_slice_l2(pf_base, pf_bytes, blockIdx.y * gridDim.x + blockIdx.x, gridDim.x * gridDim.y);
   __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(attn_smem_raw);
   __nv_bfloat16* sKV = sQ + 64 * HD;  // [stage][K | V][16][HD]
 
@@ -85,28 +94,32 @@ __global__ void __launch_bounds__(128)
   const AttnItem it = items[item_id];
   const int g = blockIdx.y;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rg = warp & 3, kg = warp >> 2;
 
-  auto load_page = [&](int pi, int buf) {
+  auto load_page = [&](int pi) {
+    const int buf = pi % PAGE_STAGES;
     const int page = item_pages[it.page_off + pi];
     const size_t off = ((size_t)page * num_kv_heads + g) * 16 * HD;
     const uint8_t* ks = reinterpret_cast<const uint8_t*>(k_pages + off);
     const uint8_t* vs = reinterpret_cast<const uint8_t*>(v_pages + off);
     const uint32_t kd = smem_u32(sKV + (size_t)buf * 32 * HD), vd = kd + 16 * HD * 2;
-    for (int idx = tid; idx < 16 * CH; idx += 128) {
+    for (int idx = tid; idx < 16 * CH; idx += 256) {
       const int row = idx / CH, ch = idx % CH;
       cp_async16(kd + swz<HD>(row, ch), ks + idx * 16);
       cp_async16(vd + swz<HD>(row, ch), vs + idx * 16);
     }
   };
-  // K/V ring prologue: pages 0 .. PAGE_STAGES-2 in flight before touching Q
+  const int n_steps = (it.n_pages + 1) / 2;
+  // ring prologue: steps 0 .. PAGE_STAGES/2 - 2 (two pages each) in flight before Q
 #pragma unroll
-  for (int s = 0; s < PAGE_STAGES - 1; ++s) {
-    if (s < it.n_pages) load_page(s, s);
+  for (int st = 0; st < PAGE_STAGES / 2 - 1; ++st) {
+    if (2 * st < it.n_pages) load_page(2 * st);
+    if (2 * st + 1 < it.n_pages) load_page(2 * st + 1);
     cp_async_commit();
   }
 
   // ---- stage Q rows (swizzled) ----
-  for (int idx = tid; idx < 64 * CH; idx += 128) {
+  for (int idx = tid; idx < 64 * CH; idx += 256) {
     const int row = idx / CH, ch = idx % CH;
     uint4 val = make_uint4(0, 0, 0, 0);
     if (row < it.n_rows) {
@@ -118,18 +131,18 @@ __global__ void __launch_bounds__(128)
   }
   __syncthreads();
 
-  // ---- per-warp query fragments ----
-  const int r_lo = warp * 16 + (lane >> 2);  // rows r_lo and r_lo + 8 of the item
+  const int r_lo = rg * 16 + (lane >> 2);  // rows r_lo and r_lo + 8 of the item
+  const bool active = rg * 16 < it.n_rows;
   int pos_lo = -1, pos_hi = -1;
   if (r_lo < it.n_rows) pos_lo = row_pos[item_rows[it.row_off + r_lo].x];
   if (r_lo + 8 < it.n_rows) pos_hi = row_pos[item_rows[it.row_off + r_lo + 8].x];
 
   uint32_t qa[HD / 16][4];
-  {
+  if (active) {
     const uint32_t qbase = smem_u32(sQ);
 #pragma unroll
     for (int kk = 0; kk < HD / 16; ++kk) {
-      const int row = warp * 16 + (lane & 15);
+      const int row = rg * 16 + (lane & 15);
       const int ch = kk * 2 + (lane >> 4);
       ldsm_x4(qbase + swz<HD>(row, ch), qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3]);
     }
@@ -140,105 +153,130 @@ __global__ void __launch_bounds__(128)
   for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
   float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;
 
-  for (int pi = 0; pi < it.n_pages; ++pi) {
-    const int buf = pi % PAGE_STAGES;
+  for (int st = 0; st < n_steps; ++st) {
     {
-      const int nxt = pi + PAGE_STAGES - 1;
-      if (nxt < it.n_pages) load_page(nxt, nxt % PAGE_STAGES);
+      const int nxt = st + PAGE_STAGES / 2 - 1;
+      if (2 * nxt < it.n_pages) load_page(2 * nxt);
+      if (2 * nxt + 1 < it.n_pages) load_page(2 * nxt + 1);
       cp_async_commit();
     }
-    cp_async_wait<PAGE_STAGES - 1>();
+    cp_async_wait<PAGE_STAGES / 2 - 1>();
     __syncthreads();
-
-    // S = Q K^T for 16 keys (two n8 tiles)
-    float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-    const uint32_t kbase = smem_u32(sKV + (size_t)buf * 32 * HD);
+    const int pi = 2 * st + kg;
+    if (active && pi < it.n_pages) {
+      const int buf = pi % PAGE_STAGES;
+      // S = Q K^T for 16 keys (two n8 tiles)
+      float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      const uint32_t kbase = smem_u32(sKV + (size_t)buf * 32 * HD);
 #pragma unroll
-    for (int kk = 0; kk < HD / 16; ++kk) {
-      // x4: matrices (keys0-7, dims lo), (keys0-7, dims hi), (keys8-15, lo), (keys8-15, hi)
-      const int key = (lane & 7) + ((lane >> 4) << 3);
-      const int ch = kk * 2 + ((lane >> 3) & 1);
-      uint32_t b0, b1, b2, b3;
-      ldsm_x4(kbase + swz<HD>(key, ch), b0, b1, b2, b3);
-      mma_bf16_16816(s[0], qa[kk], b0, b1);
-      mma_bf16_16816(s[1], qa[kk], b2, b3);
-    }
-    // scale, mask, online softmax (src/model.py:415-423, src/tensor.py:249-267)
-    const int kpos0 = it.chunk_start + pi * 16;
-    float mx_lo = m_lo, mx_hi = m_hi;
-#pragma unroll
-    for (int nt = 0; nt < 2; ++nt) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int kp = kpos0 + nt * 8 + (lane & 3) * 2 + e;
-        float a = __fmul_rn(s[nt][e], scale);
-        float b = __fmul_rn(s[nt][2 + e], scale);
-        a = (kp <= pos_lo) ? a : -INFINITY;
-        b = (kp <= pos_hi) ? b : -INFINITY;
-        s[nt][e] = a;
-        s[nt][2 + e] = b;
-        mx_lo = fmaxf(mx_lo, a);
-        mx_hi = fmaxf(mx_hi, b);
+      for (int kk = 0; kk < HD / 16; ++kk) {
+        const int key = (lane & 7) + ((lane >> 4) << 3);
+        const int ch = kk * 2 + ((lane >> 3) & 1);
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(kbase + swz<HD>(key, ch), b0, b1, b2, b3);
+        mma_bf16_16816(s[0], qa[kk], b0, b1);
+        mma_bf16_16816(s[1], qa[kk], b2, b3);
       }
-    }
-    mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, 1));
-    mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, 2));
-    mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 1));
-    mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 2));
-    const float corr_lo = (mx_lo == -INFINITY) ? 1.f : expf(m_lo - mx_lo);
-    const float corr_hi = (mx_hi == -INFINITY) ? 1.f : expf(m_hi - mx_hi);
-    float sum_lo = 0.f, sum_hi = 0.f;
+      // scale, mask, online softmax (src/model.py:415-423, src/tensor.py:249-267)
+      const int kpos0 = it.chunk_start + pi * 16;
+      float mx_lo = m_lo, mx_hi = m_hi;
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt) {
+      for (int nt = 0; nt < 2; ++nt) {
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const float a = (s[nt][e] == -INFINITY) ? 0.f : expf(s[nt][e] - mx_lo);
-        const float b = (s[nt][2 + e] == -INFINITY) ? 0.f : expf(s[nt][2 + e] - mx_hi);
-        s[nt][e] = a;
-        s[nt][2 + e] = b;
-        sum_lo += a;
-        sum_hi += b;
+        for (int e = 0; e < 2; ++e) {
+          const int kp = kpos0 + nt * 8 + (lane & 3) * 2 + e;
+          float a = __fmul_rn(s[nt][e], scale);
+          float b = __fmul_rn(s[nt][2 + e], scale);
+          a = (kp <= pos_lo) ? a : -INFINITY;
+          b = (kp <= pos_hi) ? b : -INFINITY;
+          s[nt][e] = a;
+          s[nt][2 + e] = b;
+          mx_lo = fmaxf(mx_lo, a);
+          mx_hi = fmaxf(mx_hi, b);
+        }
       }
-    }
-    sum_lo += __shfl_xor_sync(0xffffffffu, sum_lo, 1);
-    sum_lo += __shfl_xor_sync(0xffffffffu, sum_lo, 2);
-    sum_hi += __shfl_xor_sync(0xffffffffu, sum_hi, 1);
-    sum_hi += __shfl_xor_sync(0xffffffffu, sum_hi, 2);
-    l_lo = l_lo * corr_lo + sum_lo;
-    l_hi = l_hi * corr_hi + sum_hi;
-    m_lo = mx_lo;
-    m_hi = mx_hi;
+      mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, 1));
+      mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, 2));
+      mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 1));
+      mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 2));
+      const float corr_lo = (mx_lo == -INFINITY) ? 1.f : expf(m_lo - mx_lo);
+      const float corr_hi = (mx_hi == -INFINITY) ? 1.f : expf(m_hi - mx_hi);
+      float sum_lo = 0.f, sum_hi = 0.f;
 #pragma unroll
-    for (int i = 0; i < HD / 8; ++i) {
-      o[i][0] *= corr_lo; o[i][1] *= corr_lo;
-      o[i][2] *= corr_hi; o[i][3] *= corr_hi;
-    }
-    // O += P V
-    uint32_t pa[4];
-    pa[0] = pack_bf16(s[0][0], s[0][1]);
-    pa[1] = pack_bf16(s[0][2], s[0][3]);
-    pa[2] = pack_bf16(s[1][0], s[1][1]);
-    pa[3] = pack_bf16(s[1][2], s[1][3]);
-    const uint32_t vbase = kbase + 16 * HD * 2;
+      for (int nt = 0; nt < 2; ++nt) {
 #pragma unroll
-    for (int dt = 0; dt < HD / 16; ++dt) {
-      // x4.trans: (keys0-7, dims d0..d0+7), (keys8-15, d0..), (keys0-7, d0+8..), (keys8-15, d0+8..)
-      const int key = (lane & 7) + (((lane >> 3) & 1) << 3);
-      const int ch = dt * 2 + (lane >> 4);
-      uint32_t b0, b1, b2, b3;
-      ldsm_x4_t(vbase + swz<HD>(key, ch), b0, b1, b2, b3);
-      mma_bf16_16816(o[dt * 2], pa, b0, b1);
-      mma_bf16_16816(o[dt * 2 + 1], pa, b2, b3);
+        for (int e = 0; e < 2; ++e) {
+          const float a = (s[nt][e] == -INFINITY) ? 0.f : expf(s[nt][e] - mx_lo);
+          const float b = (s[nt][2 + e] == -INFINITY) ? 0.f : expf(s[nt][2 + e] - mx_hi);
+          s[nt][e] = a;
+          s[nt][2 + e] = b;
+          sum_lo += a;
+          sum_hi += b;
+        }
+      }
+      sum_lo += __shfl_xor_sync(0xffffffffu, sum_lo, 1);
+      sum_lo += __shfl_xor_sync(0xffffffffu, sum_lo, 2);
+      sum_hi += __shfl_xor_sync(0xffffffffu, sum_hi, 1);
+      sum_hi += __shfl_xor_sync(0xffffffffu, sum_hi, 2);
+      l_lo = l_lo * corr_lo + sum_lo;
+      l_hi = l_hi * corr_hi + sum_hi;
+      m_lo = mx_lo;
+      m_hi = mx_hi;
+#pragma unroll
+      for (int i = 0; i < HD / 8; ++i) {
+        o[i][0] *= corr_lo; o[i][1] *= corr_lo;
+        o[i][2] *= corr_hi; o[i][3] *= corr_hi;
+      }
+      // O += P V
+      uint32_t pa[4];
+      pa[0] = pack_bf16(s[0][0], s[0][1]);
+      pa[1] = pack_bf16(s[0][2], s[0][3]);
+      pa[2] = pack_bf16(s[1][0], s[1][1]);
+      pa[3] = pack_bf16(s[1][2], s[1][3]);
+      const uint32_t vbase = kbase + 16 * HD * 2;
+#pragma unroll
+      for (int dt = 0; dt < HD / 16; ++dt) {
+        const int key = (lane & 7) + (((lane >> 3) & 1) << 3);
+        const int ch = dt * 2 + (lane >> 4);
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4_t(vbase + swz<HD>(key, ch), b0, b1, b2, b3);
+        mma_bf16_16816(o[dt * 2], pa, b0, b1);
+        mma_bf16_16816(o[dt * 2 + 1], pa, b2, b3);
+      }
     }
     __syncthreads();
   }
+  cp_async_wait<0>();
+  __syncthreads();
 
-  // ---- write partials ----
+  // ---- combine the odd-page state into the even-page state (fixed order) ----
+  float* so = reinterpret_cast<float*>(sKV);        // [64 rows][HD] from the odd-page warps
+  float2* sml = reinterpret_cast<float2*>(so + 64 * HD);
+  if (kg == 1 && active) {
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int r = r_lo + half * 8;
+#pragma unroll
+      for (int i = 0; i < HD / 8; ++i) {
+        const int col = i * 8 + (lane & 3) * 2;
+        *reinterpret_cast<float2*>(so + r * HD + col) =
+            half == 0 ? make_float2(o[i][0], o[i][1]) : make_float2(o[i][2], o[i][3]);
+      }
+      if ((lane & 3) == 0) sml[r] = half == 0 ? make_float2(m_lo, l_lo) : make_float2(m_hi, l_hi);
+    }
+  }
+  __syncthreads();
+  if (kg == 1 || !active) return;
   const int chunk = it.chunk_idx;
 #pragma unroll
   for (int half = 0; half < 2; ++half) {
     const int r = r_lo + half * 8;
     if (r >= it.n_rows) continue;
+    const float m0 = half == 0 ? m_lo : m_hi, l0 = half == 0 ? l_lo : l_hi;
+    const float2 ml1 = sml[r];
+    const float M = fmaxf(m0, ml1.x);
+    const float w0 = (m0 == -INFINITY) ? 0.f : expf(m0 - M);
+    const float w1 = (ml1.x == -INFINITY) ? 0.f : expf(ml1.x - M);
     const int2 rr = item_rows[it.row_off + r];
     const int head = g * group + rr.y;
     const size_t slot = ((size_t)rr.x * num_heads + head) * max_chunks + chunk;
@@ -246,41 +284,54 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
     for (int i = 0; i < HD / 8; ++i) {
       const int col = i * 8 + (lane & 3) * 2;
+      const float2 o1 = *reinterpret_cast<const float2*>(so + r * HD + col);
+      const float a0 = half == 0 ? o[i][0] : o[i][2], a1 = half == 0 ? o[i][1] : o[i][3];
       *reinterpret_cast<float2*>(dst + col) =
-          half == 0 ? make_float2(o[i][0], o[i][1]) : make_float2(o[i][2], o[i][3]);
+          make_float2(fmaf(o1.x, w1, a0 * w0), fmaf(o1.y, w1, a1 * w0));
     }
-    if ((lane & 3) == 0)
-      part_ml[slot] = half == 0 ? make_float2(m_lo, l_lo) : make_float2(m_hi, l_hi);
+    if ((lane & 3) == 0) part_ml[slot] = make_float2(M, fmaf(ml1.y, w1, l0 * w0));
   }
 }
 
 // Fixed-order merge of chunk partials: one CTA per (row, KV group), one thread per
-// (head-in-group, dim). Chunks 0..last are folded in index order, so the result is
-// independent of how the chunks were grouped into work items.
+// (head-in-group, dim); per head the chunk weights exp(m_c - M) and L are computed once
+// (sequentially, chunk order) and shared through smem.
 template <int HD>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(512)
     attn_merge_kernel(const float* __restrict__ part_o, const float2* __restrict__ part_ml,
                       const int* __restrict__ row_pos, const int* __restrict__ row_kind,
                       int num_heads, int group, int max_chunks, int chunk_tokens,
                       __nv_bfloat16* __restrict__ out, int out_ld) {
+  extern __shared__ float merge_smem[];  // [group][max_chunks] weights + [group] L
   pdl_launch();
   pdl_wait();
   const int r = blockIdx.x, g = blockIdx.y;
   if (row_kind[r] < 0) return;
   const int nch = row_pos[r] / chunk_tokens + 1;
-  for (int idx = threadIdx.x; idx < group * HD; idx += blockDim.x) {
-    const int head = g * group + idx / HD, d = idx % HD;
-    const size_t base = ((size_t)r * num_heads + head) * max_chunks;
+  float* wts = merge_smem;
+  float* Ls = merge_smem + group * max_chunks;
+  const int tid = threadIdx.x;
+  if (tid < group) {
+    const size_t base = ((size_t)r * num_heads + g * group + tid) * max_chunks;
     float M = -INFINITY;
     for (int c = 0; c < nch; ++c) M = fmaxf(M, part_ml[base + c].x);
-    float L = 0.f, O = 0.f;
+    float L = 0.f;
     for (int c = 0; c < nch; ++c) {
       const float2 ml = part_ml[base + c];
       const float w = expf(ml.x - M);
+      wts[tid * max_chunks + c] = w;
       L = fmaf(ml.y, w, L);
-      O = fmaf(part_o[(base + c) * HD + d], w, O);
     }
-    out[(size_t)r * out_ld + head * HD + d] = __float2bfloat16_rn(__fdiv_rn(O, L));
+    Ls[tid] = L;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < group * HD; idx += blockDim.x) {
+    const int hg = idx / HD, d = idx % HD;
+    const int head = g * group + hg;
+    const size_t base = ((size_t)r * num_heads + head) * max_chunks;
+    float O = 0.f;
+    for (int c = 0; c < nch; ++c) O = fmaf(part_o[(base + c) * HD + d], wts[hg * max_chunks + c], O);
+    out[(size_t)r * out_ld + head * HD + d] = __float2bfloat16_rn(__fdiv_rn(O, Ls[hg]));
   }
 }
 
@@ -295,12 +346,14 @@ static cudaError_t attn_launch_hd(const AttnLaunch& a, cudaStream_t s) {
     attr = true;
   }
   dim3 grid(a.n_items_cap, a.num_kv_heads);
-  cudaError_t e = launch_pdl(attn_partial_kernel<HD>, grid, dim3(128), attn_smem<HD>(), s, a.q,
+  cudaError_t e = launch_pdl(attn_partial_kernel<HD>, grid, dim3(256), attn_smem<HD>(), s, a.q,
                              a.q_ld, a.k_pages, a.v_pages, a.num_kv_heads, a.group, a.items,
                              a.item_pages, a.item_rows, a.row_pos, a.num_heads, a.max_chunks,
-                             a.scale, a.part_o, a.part_ml, a.n_items_dev);
+                             a.scale, a.part_o, a.part_ml, a.n_items_dev, a.pf_base, a.pf_bytes);
   if (e != cudaSuccess) return e;
-  return launch_pdl(attn_merge_kernel<HD>, dim3(a.n_rows, a.num_kv_heads), dim3(256), 0, s,
+  const int mthreads = std::min(512, ((a.group * HD + 31) / 32) * 32);
+  const size_t msmem = (size_t)a.group * (a.max_chunks + 1) * sizeof(float);
+  return launch_pdl(attn_merge_kernel<HD>, dim3(a.n_rows, a.num_kv_heads), dim3(mthreads), msmem, s,
                     a.part_o, a.part_ml, a.row_pos, a.row_kind, a.num_heads, a.group,
                     a.max_chunks, a.chunk_tokens, a.out, a.out_ld);
 }

@@ -11,9 +11,7 @@ constexpr uint32_t W_BYTES = BM * BK * 2;
 constexpr int MAX_RANK = 32;
 // barriers, reduction scratch, staged row metadata and the LoRA U rows of the launch
 template <int NT>
-constexpr size_t aux_smem() {
-  return 2048 + (size_t)NT * 5 * 4 + (NT <= 64 ? (size_t)NT * 2 * 32 * 4 : 0);
-}
+constexpr size_t aux_smem() { return 2048 + (size_t)NT * 5 * 4; }
 
 template <int NT>
 struct Cfg {
@@ -66,7 +64,6 @@ struct RowMeta {
   int* pos;
   int* kvoff;
   float* inv;
-  float* u;  // [NT][n_u][rank] LoRA U of this launch's rows (NT <= 64)
 };
 
 template <int NT>
@@ -78,67 +75,6 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] = __fmul_rn(v[j], rm.inv[n0 + j]);
   }
-  // ---- LoRA expand on decoder rows (segmented by adapter slot) ----
-  if (p.lora_b != nullptr) {
-    if (!sh.shrink_ready) {  // uniform across the 128 epilogue threads
-      if (p.sh_x != nullptr && ep_t == 0) {
-        const int target = gridDim.x * 2;
-        while (ld_acquire(p.sync) < target) __nanosleep(32);
-      }
-      named_bar_sync(1, 128);
-      // stage U of this launch's decoder rows in smem (broadcast reads in the expand)
-      const int per_row = p.n_u * p.rank;
-      for (int idx = ep_t; rm.u != nullptr && idx < NT * per_row; idx += 128) {
-        const int n = idx / per_row;
-        rm.u[idx] = (n < p.n_rows && rm.kind[n] == 1 && rm.ad[n] >= 0)
-                        ? __ldcg(p.lora_u + (size_t)(p.row0 + n) * per_row + idx % per_row)
-                        : 0.f;
-      }
-      if (ep_t == 0) sh.shrink_ready = 1;
-      named_bar_sync(1, 128);
-    }
-    if (m < p.lora_m) {
-      const int uidx = (p.mode == EPI_SILU) ? (m & 1) : 0;
-      const int nch = p.rank >> 3;
-      const int per_row = p.n_u * p.rank;
-      // issue 8 columns' B loads before using any (one memory round trip per batch)
-#pragma unroll
-      for (int jb = 0; jb < 16; jb += 8) {
-        for (int cb = 0; cb < nch; cb += 2) {
-          uint4 braw[8][2];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int n = n0 + jb + q;
-            if (n < p.n_rows && rm.kind[n] == 1 && rm.ad[n] >= 0) {
-              const uint4* b = reinterpret_cast<const uint4*>(
-                  p.lora_b + ((size_t)rm.ad[n] * p.lora_m + m) * p.rank) + cb;
-              braw[q][0] = __ldg(b);
-              braw[q][1] = (cb + 1 < nch) ? __ldg(b + 1) : make_uint4(0, 0, 0, 0);
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int n = n0 + jb + q;
-            if (!(n < p.n_rows && rm.kind[n] == 1 && rm.ad[n] >= 0)) continue;
-            const float* u = (rm.u != nullptr
-                                  ? rm.u + (size_t)n * per_row
-                                  : p.lora_u + (size_t)(p.row0 + n) * per_row) +
-                             uidx * p.rank + cb * 8;
-            float acc = 0.f;
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-              float bf[8];
-              unpack8(braw[q][c], bf);
-#pragma unroll
-              for (int e = 0; e < 8; ++e) acc = fmaf(u[c * 8 + e], bf[e], acc);
-            }
-            v[jb + q] += acc;
-          }
-        }
-      }
-    }
-  }
-
   switch (p.mode) {
     case EPI_F32: {
 #pragma unroll
@@ -257,8 +193,8 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
 // a lane's loads for the slice are issued before use (one memory round trip). The warp
 // that delivers a row's last slice folds the partials in slice order (deterministic).
 constexpr int SHRINK_SLICE = 2048;  // 8 x (32 lanes x 8 bf16)
-__device__ __forceinline__ void lora_shrink_tasks(const GemmParams& p, const RowMeta& rm,
-                                                  int gwarp, int nwarps, int lane) {
+__device__ __forceinline__ void lora_shrink_tasks(const GemmParams& p, int gwarp, int nwarps,
+                                                  int lane) {
   const int per_t = p.slots * p.rank;
   const int splits = (p.sh_K + SHRINK_SLICE - 1) / SHRINK_SLICE;
   const int tasks = p.sh_targets * per_t * splits;
@@ -298,13 +234,12 @@ __device__ __forceinline__ void lora_shrink_tasks(const GemmParams& p, const Row
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       if (lane == 0) {
-        const size_t slot = ((size_t)gr * p.n_u + t) * p.rank + j;
-        if (splits == 1) {
-          const float sc = p.sh_scale_inv ? rm.inv[gr - p.row0] : 1.f;
-          p.lora_u[slot] = __fmul_rn(acc, sc);
-        } else {
-          p.sh_part[(size_t)ks * p.rows_total * p.n_u * p.rank + slot] = acc;
-        }
+        const size_t slot = ((size_t)gr * 2 + t) * p.rank + j;
+        if (splits == 1)
+          p.ubd[(size_t)gr * p.ubd_ld + (size_t)t * p.slots * p.rank + a * p.rank + j] =
+              __float2bfloat16_rn(acc);
+        else
+          p.sh_part[(size_t)ks * p.rows_total * 2 * p.rank + slot] = acc;
       }
     }
     if (splits > 1 && lane == 0) {
@@ -315,13 +250,13 @@ __device__ __forceinline__ void lora_shrink_tasks(const GemmParams& p, const Row
         for (int rr = r0; rr < r1; ++rr) {
           const int gr = p.seg_rows[rr];
           if (gr < p.row0 || gr >= p.row0 + p.n_rows) continue;
-          const size_t slot = ((size_t)gr * p.n_u + t) * p.rank + j;
+          const size_t slot = ((size_t)gr * 2 + t) * p.rank + j;
           float s = 0.f;
           for (int q = 0; q < splits; ++q)
             s = (q == 0) ? __ldcg(p.sh_part + slot)
-                         : __fadd_rn(s, __ldcg(p.sh_part + (size_t)q * p.rows_total * p.n_u * p.rank + slot));
-          const float sc = p.sh_scale_inv ? rm.inv[gr - p.row0] : 1.f;
-          p.lora_u[slot] = __fmul_rn(s, sc);
+                         : __fadd_rn(s, __ldcg(p.sh_part + (size_t)q * p.rows_total * 2 * p.rank + slot));
+          p.ubd[(size_t)gr * p.ubd_ld + (size_t)t * p.slots * p.rank + a * p.rank + j] =
+              __float2bfloat16_rn(s);
         }
         *cnt = 0;
       }
@@ -332,7 +267,9 @@ __device__ __forceinline__ void lora_shrink_tasks(const GemmParams& p, const Row
 template <int NT>
 __global__ void __launch_bounds__(256, 1)
     gemm_streamk_kernel(const __grid_constant__ CUtensorMap tm_w,
-                        const __grid_constant__ CUtensorMap tm_x, const GemmParams p,
+                        const __grid_constant__ CUtensorMap tm_x,
+                        const __grid_constant__ CUtensorMap tm_lb,
+                        const __grid_constant__ CUtensorMap tm_lu, const GemmParams p,
                         int x_row0) {
   using C = Cfg<NT>;
   extern __shared__ uint8_t smem_raw[];
@@ -350,11 +287,12 @@ __global__ void __launch_bounds__(256, 1)
   rm.pos = rm.ad + NT;
   rm.kvoff = rm.pos + NT;
   rm.inv = reinterpret_cast<float*>(rm.kvoff + NT);
-  rm.u = NT <= 64 ? rm.inv + NT : nullptr;  // larger launches read U from global memory
 
   const int warp = warp_id();
+  const int Kb = p.K / BK;  // base K chunks per tile
+  const int Lc = p.lora_chunks;
   Split sp;
-  sp.Ut = p.K / BK;
+  sp.Ut = Kb + Lc;
   sp.U = (long long)(p.M / BM) * sp.Ut;
   sp.G = gridDim.x;
   const int c = blockIdx.x;
@@ -368,6 +306,7 @@ __global__ void __launch_bounds__(256, 1)
     fence_barrier_init();
     tma_prefetch_desc(&tm_w);
     tma_prefetch_desc(&tm_x);
+    if (Lc > 0) { tma_prefetch_desc(&tm_lb); tma_prefetch_desc(&tm_lu); }
   }
   if (warp == 2) tmem_alloc<C::TMEM_COLS>(tmem_slot);
   if (threadIdx.x == 128) { sh.shrink_ready = 0; sh.flag = 0; }
@@ -376,36 +315,107 @@ __global__ void __launch_bounds__(256, 1)
   tc_fence_after();
   pdl_launch();
   const uint32_t tmem_base = *tmem_slot;
+  auto stamp = [&](int slot) {
+    if (p.trace != nullptr) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      p.trace[(size_t)blockIdx.x * 8 + slot] = t;
+    }
+  };
+  if (threadIdx.x == 0) stamp(0);
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (elect_one()) {
       const uint64_t pol = policy_evict_first();
-      auto load_w = [&](long long u, int stage) {
-        const int t = (int)(u / sp.Ut), k = (int)(u % sp.Ut);
+      // Walk this CTA's units with running (tile, chunk) counters: no integer division on
+      // the per-16KB path (a single thread must issue a tile every ~0.3 us).
+      // LoRA chunk placement inside a tile (one rule for every CTA sharing the tile): the
+      // last Lc units of the portion owned by the CTA whose range contains the tile start,
+      // i.e. as late as possible in that CTA's range -- the shrink has finished by then.
+      struct Cursor {
+        int t, k;  // tile, position within the tile's Ut units
+        int ls;    // first LoRA unit within the tile
+      };
+      auto tile_ls = [&](int t) {
+        if (Lc == 0) return 0;
+        const long long t0 = (long long)t * sp.Ut;
+        const long long nxt = sp.ubegin(sp.owner(t0) + 1);
+        const long long e0 = (t0 + sp.Ut < nxt) ? t0 + sp.Ut : nxt;
+        const int portion = (int)(e0 - t0);
+        return portion >= Lc ? portion - Lc : 0;
+      };
+      auto chunk_of = [&](const Cursor& cu, int& ch) {
+        if (cu.k < cu.ls || Lc == 0) { ch = cu.k; return false; }
+        if (cu.k < cu.ls + Lc) { ch = cu.k - cu.ls; return true; }
+        ch = cu.k - Lc;
+        return false;
+      };
+      auto advance = [&](Cursor& cu) {
+        if (++cu.k == sp.Ut) { cu.k = 0; ++cu.t; cu.ls = tile_ls(cu.t); }
+      };
+      bool lora_ready = false;
+      auto load_w = [&](const Cursor& cu, int stage) {
+        int ch;
+        const bool lo = chunk_of(cu, ch);
         uint8_t* st = smem + (size_t)stage * C::STAGE;
         mbar_expect_tx(&full[stage], C::STAGE);
-        if (p.w_blocked)
-          tma_load_3d_hint(st, &tm_w, &full[stage], 0, 0, t * sp.Ut + k, pol);
+        if (lo)
+          tma_load_3d_hint(st, &tm_lb, &full[stage], 0, 0, cu.t * Lc + ch, pol);
+        else if (p.w_blocked)
+          tma_load_3d_hint(st, &tm_w, &full[stage], 0, 0, cu.t * Kb + ch, pol);
         else
-          tma_load_2d_hint(st, &tm_w, &full[stage], k * BK, t * BM, pol);
+          tma_load_2d_hint(st, &tm_w, &full[stage], ch * BK, cu.t * BM, pol);
       };
-      auto load_x = [&](long long u, int stage) {
-        const int k = (int)(u % sp.Ut);
-        tma_load_2d(smem + (size_t)stage * C::STAGE + W_BYTES, &tm_x, &full[stage], k * BK, x_row0);
+      auto load_x = [&](const Cursor& cu, int stage) {
+        int ch;
+        const bool lo = chunk_of(cu, ch);
+        uint8_t* dst = smem + (size_t)stage * C::STAGE + W_BYTES;
+        if (lo) {
+          if (!lora_ready) {  // U is produced by this grid's shrink warps
+            const int target = gridDim.x * 2;
+            stamp(2);
+            while (ld_acquire(p.sync) < target) __nanosleep(32);
+            stamp(3);
+            asm volatile("fence.proxy.async.global;\n" ::: "memory");
+            lora_ready = true;
+          }
+          tma_load_2d(dst, &tm_lu, &full[stage], ch * BK, x_row0);
+        } else {
+          tma_load_2d(dst, &tm_x, &full[stage], ch * BK, x_row0);
+        }
       };
+      Cursor start;
+      start.t = t_first;
+      start.k = (int)(u_begin - (long long)t_first * sp.Ut);
+      start.ls = tile_ls(t_first);
       // Weights do not depend on the previous kernel: fill the ring before waiting on it.
-      const long long pre = (u_end - u_begin) < NS ? (u_end - u_begin) : NS;
-      for (long long i = 0; i < pre; ++i) load_w(u_begin + i, (int)i);
+      const long long total = u_end - u_begin;
+      const int pre = (int)(total < NS ? total : NS);
+      Cursor cu = start;
+      for (int i = 0; i < pre; ++i) { load_w(cu, i); advance(cu); }
       pdl_wait();
-      for (long long i = 0; i < pre; ++i) load_x(u_begin + i, (int)i);
-      int stage = (int)(pre % NS);
+      cu = start;
+      for (int i = 0; i < pre; ++i) { load_x(cu, i); advance(cu); }
+      int stage = pre % NS;
       uint32_t phase = (pre == NS) ? 1u : 0u;
       for (long long u = u_begin + pre; u < u_end; ++u) {
         mbar_wait(&empty[stage], phase ^ 1);
-        load_w(u, stage);
-        load_x(u, stage);
+        load_w(cu, stage);
+        load_x(cu, stage);
+        advance(cu);
         if (++stage == NS) { stage = 0; phase ^= 1; }
+      }
+      stamp(4);
+      // all of this CTA's weight bytes are requested: keep HBM busy with the next weights
+      if (p.pf_w != nullptr) {
+        for (int c2 = c; c2 < p.pf_G; c2 += gridDim.x) {
+          const long long b = (long long)c2 * p.pf_units / p.pf_G;
+          const long long e = (long long)(c2 + 1) * p.pf_units / p.pf_G;
+          const long long s0 = b + p.pf_skip;
+          const long long s1 = (e < s0 + p.pf_max) ? e : s0 + p.pf_max;
+          for (long long u = s0; u < s1; ++u) bulk_prefetch_l2(p.pf_w + u * W_BYTES, W_BYTES);
+        }
       }
     }
   } else if (warp == 1) {
@@ -446,12 +456,13 @@ __global__ void __launch_bounds__(256, 1)
     // ---------------- LoRA shrink (SGMV) on the two otherwise idle warps ----------------
     if (p.sh_x != nullptr) {
       pdl_wait();
-      named_bar_sync(2, 192);  // wait for the epilogue warps' row metadata
       const int lane = lane_id();
-      lora_shrink_tasks(p, rm, blockIdx.x * 2 + (warp - 2), gridDim.x * 2, lane);
+      lora_shrink_tasks(p, blockIdx.x * 2 + (warp - 2), gridDim.x * 2, lane);
       __syncwarp();
       __threadfence();
+      asm volatile("fence.proxy.async.global;\n" ::: "memory");  // U is read by TMA
       if (lane == 0) atomicAdd(p.sync, 1);
+      if (lane == 0 && warp == 2) stamp(1);
     }
   } else if (warp >= 4) {
     // ---------------- epilogue (TMEM -> registers -> global) ----------------
@@ -484,19 +495,6 @@ __global__ void __launch_bounds__(256, 1)
       rm.inv[n] = inv;
     }
     named_bar_sync(1, 128);
-    if (p.sh_x != nullptr) named_bar_arrive(2, 192);  // row metadata ready for the shrink warps
-    if (p.lora_b != nullptr) {
-      // warm L2 with the adapter B rows this CTA's tiles will need in the epilogue
-      for (int t = t_first; t <= t_last; ++t) {
-        const int m = t * BM + ep_t;
-        if (m >= p.lora_m) continue;
-        for (int a = 0; a < p.slots; ++a) {
-          if (p.seg_off[a] == p.seg_off[a + 1]) continue;
-          const char* b = reinterpret_cast<const char*>(p.lora_b + ((size_t)a * p.lora_m + m) * p.rank);
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(b));
-        }
-      }
-    }
     uint32_t tphase = 0;
     for (int t = t_first; t <= t_last; ++t) {
       const long long t0 = (long long)t * sp.Ut;
@@ -555,6 +553,7 @@ __global__ void __launch_bounds__(256, 1)
 
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) stamp(5);
   if (warp == 2) tmem_dealloc<C::TMEM_COLS>(tmem_base);
   if (p.sh_x != nullptr && threadIdx.x == 0) {
     // every CTA has passed its shrink wait: the last one out resets the counters
@@ -569,8 +568,9 @@ __global__ void __launch_bounds__(256, 1)
 
 // ------------------------------------------------------------------ host side
 template <int NT>
-static cudaError_t launch_nt(const CUtensorMap& tw, const CUtensorMap& tx, const GemmParams& p,
-                             int x_row0, int num_sms, cudaStream_t s) {
+static cudaError_t launch_nt(const CUtensorMap& tw, const CUtensorMap& tx, const CUtensorMap& tlb,
+                             const CUtensorMap& tlu, const GemmParams& p, int x_row0, int num_sms,
+                             cudaStream_t s) {
   using C = Cfg<NT>;
   static bool attr = false;
   if (!attr) {
@@ -579,11 +579,12 @@ static cudaError_t launch_nt(const CUtensorMap& tw, const CUtensorMap& tx, const
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const long long U = (long long)(p.M / BM) * (p.K / BK);
+  const long long U = (long long)(p.M / BM) * (p.K / BK + p.lora_chunks);
   const int G = (int)(U < num_sms ? U : num_sms);
   const int NS = (p.stages > 0 && p.stages < C::STAGES) ? p.stages : C::STAGES;
   const size_t smem = 1024 + (size_t)NS * C::STAGE + aux_smem<NT>();
-  return launch_pdl(gemm_streamk_kernel<NT>, dim3(G), dim3(256), smem, s, tw, tx, p, x_row0);
+  return launch_pdl(gemm_streamk_kernel<NT>, dim3(G), dim3(256), smem, s, tw, tx, tlb, tlu, p,
+                    x_row0);
 }
 
 int gemm_pick_nt(int rows) {
@@ -594,19 +595,33 @@ int gemm_pick_nt(int rows) {
   return 256;
 }
 
-cudaError_t gemm_launch(const CUtensorMap& tw, const CUtensorMap& tx, const GemmParams& p,
-                        int x_row0, int nt, int num_sms, cudaStream_t s) {
+cudaError_t gemm_launch(const CUtensorMap& tw, const CUtensorMap& tx, const CUtensorMap* tlb,
+                        const CUtensorMap* tlu, const GemmParams& p, int x_row0, int nt,
+                        int num_sms, cudaStream_t s) {
   if (p.rank > MAX_RANK) return cudaErrorInvalidValue;
+  if (p.lora_chunks > 0 && (tlb == nullptr || tlu == nullptr)) return cudaErrorInvalidValue;
+  const CUtensorMap& lb = tlb ? *tlb : tw;
+  const CUtensorMap& lu = tlu ? *tlu : tx;
   switch (nt) {
-    case 16: return launch_nt<16>(tw, tx, p, x_row0, num_sms, s);
-    case 32: return launch_nt<32>(tw, tx, p, x_row0, num_sms, s);
-    case 64: return launch_nt<64>(tw, tx, p, x_row0, num_sms, s);
-    case 128: return launch_nt<128>(tw, tx, p, x_row0, num_sms, s);
-    case 256: return launch_nt<256>(tw, tx, p, x_row0, num_sms, s);
+    case 16: return launch_nt<16>(tw, tx, lb, lu, p, x_row0, num_sms, s);
+    case 32: return launch_nt<32>(tw, tx, lb, lu, p, x_row0, num_sms, s);
+    case 64: return launch_nt<64>(tw, tx, lb, lu, p, x_row0, num_sms, s);
+    case 128: return launch_nt<128>(tw, tx, lb, lu, p, x_row0, num_sms, s);
+    case 256: return launch_nt<256>(tw, tx, lb, lu, p, x_row0, num_sms, s);
     default: return cudaErrorInvalidValue;
   }
 }
 
 size_t gemm_ws_floats(int num_sms) { return (size_t)num_sms * 2 * 256 * BM; }
+
+int gemm_stages(int nt) {
+  switch (nt) {
+    case 16: return Cfg<16>::STAGES;
+    case 32: return Cfg<32>::STAGES;
+    case 64: return Cfg<64>::STAGES;
+    case 128: return Cfg<128>::STAGES;
+    default: return Cfg<256>::STAGES;
+  }
+}
 
 }  // namespace icr

@@ -57,23 +57,24 @@ struct GemmParams {
   const float* in_ssq;     // null = no scaling
   int ss_tiles, ss_stride;
   float ss_d, eps;         // feature count d (mean = sum / d) and RMSNorm eps
-  // LoRA expand (decoder rows only): delta[m] = sum_j U[n, uidx, j] * Bs[slot, m, j]
-  const __nv_bfloat16* lora_b;  // [slots][lora_m][rank], alpha/rank folded in; null = none
-  float* lora_u;                // [rows_total][n_u][rank] (global rows)
-  int lora_m;                   // rows of W that carry an adapter (q_dim for qkv)
-  int rank;
-  int n_u;                      // 1, or 2 for interleaved gate/up
-  // in-kernel LoRA shrink: U[n][t][j] = s_n * sum_k X_sh[n][k] * A_t[a][j][k]
+  // LoRA (decoder rows only), SGMV as extra tcgen05 K-chunks: each tile accumulates
+  // B_cat[m, :] . Ubd[n, :] over lora_chunks 64-wide chunks, where B_cat concatenates every
+  // slot's (alpha/r) * B along K (tile-major like W) and Ubd is block-diagonal: row n holds
+  // its adapter's U = X_n A^T in its own slot columns, zeros elsewhere (encoder rows: 0).
+  int lora_chunks;              // 0 = no LoRA in this launch
+  // in-kernel LoRA shrink (warps 2-3): Ubd[n][t*slots*rank + a*rank + j] = X_sh[n] . A_t[a][j]
   const __nv_bfloat16* sh_x;    // bf16 [rows_total][sh_ld]; null = no shrink
   int sh_ld, sh_K, sh_targets;  // sh_targets 1 or 2
   const __nv_bfloat16* sh_a0;   // [slots][rank][sh_K]
   const __nv_bfloat16* sh_a1;
-  int sh_scale_inv;             // 1: s_n = inv_n (X_sh is the un-normed residual)
+  int rank;
   const int* seg_off;           // [slots + 1] decoder rows grouped by adapter slot
   const int* seg_rows;          // global row indices
   int slots;
+  __nv_bfloat16* ubd;           // block-diagonal U [rows_total][ubd_ld] (bf16, TMA operand)
+  int ubd_ld;
   int* sync;                    // [2] shrink-done / exit counters (self-resetting)
-  float* sh_part;               // [SHRINK_SPLITS][rows_total][n_u][rank] K-split partials
+  float* sh_part;               // [SHRINK_SPLITS][rows_total][2][rank] K-split partials
   int* sh_cnt;                  // [2][slots][rank] split arrivals per adapter row (self-resetting)
   // outputs (GLOBAL row indexing)
   float* out_f32;               // EPI_F32
@@ -96,7 +97,14 @@ struct GemmParams {
   float* ws;                    // [grid][2][N][128]
   int* counters;                // [m_tiles]
   int max_segs;
+  // L2 prefetch of the NEXT projection's weights once this CTA has issued all its loads:
+  // next-kernel CTA c streams tile-major units [c*U'/G', (c+1)*U'/G'); its first pf_skip
+  // units come in through its own PDL pre-issue, the following <= pf_max are prefetched.
+  const uint8_t* pf_w;  // null = none
+  long long pf_units;   // U' of the next GEMM
+  int pf_G, pf_skip, pf_max;
   // tuning / diagnostics (0 = defaults)
+  unsigned long long* trace;  // per-CTA %globaltimer stamps [grid][8] (null = off)
   int stages;     // smem ring depth actually used (<= compiled maximum)
   int skip_mma;   // 1: consume stages without tcgen05.mma (pure TMA streaming rate)
 };

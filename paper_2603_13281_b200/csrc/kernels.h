@@ -31,9 +31,13 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 }
 
 // --------------------------------------------------------------- GEMM (gemm.cu)
-cudaError_t gemm_launch(const CUtensorMap& tw, const CUtensorMap& tx, const GemmParams& p,
-                        int x_row0, int nt, int num_sms, cudaStream_t s);
+// tlb / tlu: LoRA expand operands (B_cat tile-major 3-D map, block-diagonal U 2-D map);
+// may be null when p.lora_chunks == 0.
+cudaError_t gemm_launch(const CUtensorMap& tw, const CUtensorMap& tx, const CUtensorMap* tlb,
+                        const CUtensorMap* tlu, const GemmParams& p, int x_row0, int nt,
+                        int num_sms, cudaStream_t s);
 int gemm_pick_nt(int rows);
+int gemm_stages(int nt);
 size_t gemm_ws_floats(int num_sms);
 
 // --------------------------------------------------------------- attention (attention.cu)
@@ -64,7 +68,9 @@ struct AttnLaunch {
   float scale;
   float* part_o;
   float2* part_ml;
-  int* merge_cnt;  // [rows][H_kv], zero-initialised, self-resetting
+  int* merge_cnt;  // unused (kept for ABI of the test entry)
+  const uint8_t* pf_base;  // L2 prefetch of the next projection's weights (null = none)
+  long long pf_bytes;
   __nv_bfloat16* out;
   int out_ld;
 };
@@ -75,7 +81,18 @@ cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t s);
 // per-128-feature sums of squares ssq[c][r] that the first GEMM turns into RMSNorm scales.
 cudaError_t embed_launch(const int* tokens, const int* row_kind, const __nv_bfloat16* embed,
                          float* x, __nv_bfloat16* xb, float* ssq, int ss_stride, int n_rows,
-                         int d, cudaStream_t s);
+                         int d, const uint8_t* pf_base, long long pf_bytes, __nv_bfloat16* ubd,
+                         int ubd_ld, cudaStream_t s);
+
+// Each CTA of a latency-bound kernel prefetches its slice of [base, base + bytes) into L2.
+__device__ __forceinline__ void prefetch_slice_l2(const uint8_t* base, long long bytes, int part,
+                                                  int nparts) {
+  if (base == nullptr) return;
+  const long long units = bytes >> 14;  // 16 KB pieces
+  const long long b = (long long)part * units / nparts, e = (long long)(part + 1) * units / nparts;
+  for (long long u = b + threadIdx.x; u < e; u += blockDim.x)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], 16384;\n" ::"l"(base + (u << 14)) : "memory");
+}
 
 // Emitting rows for the LM head: hlm[i] = xb[lm_rows[i]], ssq_lm[c][i] = ssq[c][lm_rows[i]];
 // rows n_lm..n_pad-1 are zero.

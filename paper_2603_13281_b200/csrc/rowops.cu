@@ -13,10 +13,16 @@ int g_pdl = 1;
 __global__ void __launch_bounds__(256)
     embed_kernel(const int* __restrict__ tokens, const int* __restrict__ row_kind,
                  const __nv_bfloat16* __restrict__ embed, float* __restrict__ x,
-                 __nv_bfloat16* __restrict__ xb, float* __restrict__ ssq, int ss_stride, int d) {
+                 __nv_bfloat16* __restrict__ xb, float* __restrict__ ssq, int ss_stride, int d,
+                 const uint8_t* __restrict__ pf_base, long long pf_bytes,
+                 __nv_bfloat16* __restrict__ ubd, int ubd_ld) {
   pdl_launch();
+  prefetch_slice_l2(pf_base, pf_bytes, blockIdx.x, gridDim.x);
   pdl_wait();
   const int r = blockIdx.x, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // the block-diagonal LoRA U row starts the step all zero (the shrinks fill own slots)
+  for (int i = threadIdx.x * 8; i < ubd_ld; i += 256 * 8)
+    *reinterpret_cast<uint4*>(ubd + (size_t)r * ubd_ld + i) = make_uint4(0, 0, 0, 0);
   const bool valid = row_kind[r] >= 0;
   const __nv_bfloat16* e = embed + (size_t)(valid ? tokens[r] : 0) * d;
   for (int c = w; c < d / 128; c += 8) {
@@ -44,10 +50,11 @@ __global__ void __launch_bounds__(256)
 
 cudaError_t embed_launch(const int* tokens, const int* row_kind, const __nv_bfloat16* embed,
                          float* x, __nv_bfloat16* xb, float* ssq, int ss_stride, int n_rows,
-                         int d, cudaStream_t s) {
+                         int d, const uint8_t* pf_base, long long pf_bytes, __nv_bfloat16* ubd,
+                         int ubd_ld, cudaStream_t s) {
   if (n_rows <= 0) return cudaSuccess;
   return launch_pdl(embed_kernel, dim3(n_rows), dim3(256), 0, s, tokens, row_kind, embed, x, xb,
-                    ssq, ss_stride, d);
+                    ssq, ss_stride, d, pf_base, pf_bytes, ubd, ubd_ld);
 }
 
 __global__ void __launch_bounds__(128)

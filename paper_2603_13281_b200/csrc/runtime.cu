@@ -217,7 +217,8 @@ struct Meta {
 
 // ------------------------------------------------------------------ model
 struct LayerMaps {
-  CUtensorMap qkv, o, gu, down;
+  CUtensorMap qkv, o, gu, down;          // base weights (tile-major)
+  CUtensorMap lb_q, lb_o, lb_gu, lb_down;  // LoRA B_cat (tile-major), when lora_rank > 0
 };
 
 struct GraphKey {
@@ -248,7 +249,8 @@ struct icr_model {
   float* ssq = nullptr;          // per-128-feature sums of squares [d/128][rp]
   float* ssq_lm = nullptr;
   __nv_bfloat16 *qb = nullptr, *att = nullptr, *f = nullptr, *hlm = nullptr;
-  float* U = nullptr;
+  __nv_bfloat16* ubd = nullptr;  // block-diagonal LoRA U [rp][ubd_ld]
+  int ubd_ld = 0, lc1 = 0, lc2 = 0;  // U row stride; LoRA K chunks for 1 / 2 targets
   float2* tile_best = nullptr;
   int* out_tok = nullptr;
   float* part_o = nullptr;
@@ -260,7 +262,7 @@ struct icr_model {
   int* sync = nullptr;
   float* sh_part = nullptr;  // LoRA shrink K-split partials
   int* sh_cnt = nullptr;
-  CUtensorMap xmap_xb[5], xmap_att[5], xmap_f[5], xmap_hlm[5];
+  CUtensorMap xmap_xb[5], xmap_att[5], xmap_f[5], xmap_hlm[5], xmap_ubd[5];
   // metadata staging
   int* meta_dev = nullptr;
   size_t meta_cap = 0;  // ints
@@ -276,7 +278,22 @@ struct icr_model {
   long long last_items = 0;
   Meta last_mt;
   bool has_last = false;
+  // per-launch timing (icr_profile_step): events recorded after every launch when set
+  std::vector<cudaEvent_t>* timing = nullptr;
+  std::vector<int>* timing_kind = nullptr;
 };
+
+// kinds for icr_profile_step
+enum { TK_EMBED = 0, TK_QKV = 1, TK_ATTN = 2, TK_O = 3, TK_GU = 4, TK_DOWN = 5, TK_LMG = 6,
+       TK_LM = 7, TK_ARGMAX = 8 };
+static void mark(icr_model* m, cudaStream_t s, int kind) {
+  if (!m->timing) return;
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, s);
+  m->timing->push_back(e);
+  m->timing_kind->push_back(kind);
+}
 
 static Meta layout_meta(const icr_model* m, int n_rows) {
   const icr_model_config& c = m->cfg;
@@ -390,6 +407,23 @@ static icr_status validate_batch(icr_model* m, const icr_batch* b, const int* po
   return ICR_OK;
 }
 
+// L2 prefetch target for a GEMM tail: the next projection (tile-major) weights.
+static const int kPfMaxUnits = 24;  // per CTA: 24 x 16 KB x 148 CTAs ~= 57 MB of L2
+static void set_prefetch(const icr_model* m, GemmParams& p, const void* next_w, int next_M,
+                         int next_K, int rows) {
+  if (next_w == nullptr || rows > 256 || getenv("ICR_NO_PREFETCH")) return;
+  const long long U = (long long)(next_M / 128) * (next_K / 64);
+  const int G = (int)std::min<long long>(U, m->num_sms);
+  const int skip = gemm_stages(gemm_pick_nt(rows));
+  const long long per = U / G;
+  if (per <= skip) return;
+  p.pf_w = (const uint8_t*)next_w;
+  p.pf_units = U;
+  p.pf_G = G;
+  p.pf_skip = skip;
+  p.pf_max = (int)std::min<long long>(per - skip, kPfMaxUnits);
+}
+
 // Enqueue the whole forward on `s` using metadata resident at m->meta_dev (layout mt).
 static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_dev, cudaStream_t s) {
   const icr_model_config& c = m->cfg;
@@ -401,19 +435,24 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
   const int* adapter = md + mt.o_adapter;
   const int* lm_rows = md + mt.o_lm_rows;
   const int* bt = md + mt.o_bt;
-  const bool lora = c.lora_rank > 0 && mt.n_dec > 0;
+  // LoRA chunks are part of every launch of an adapter-carrying model (zero U for rows
+  // without an adapter), so stream-K split points -- and with them every encoder row's
+  // bits -- never depend on which rows the batch holds.
+  const bool lora = c.lora_rank > 0;
   const int d = c.hidden_dim, rp = mt.rp;
   long long launches = 0;
 
-  auto gemm = [&](const CUtensorMap& wmap, CUtensorMap* xmaps, const GemmParams& p,
-                  int rows) -> icr_status {
+  auto gemm = [&](const CUtensorMap& wmap, CUtensorMap* xmaps, const GemmParams& p, int rows,
+                  const CUtensorMap* lbmap = nullptr) -> icr_status {
     for (int g0 = 0; g0 < rows; g0 += 256) {
       const int gr = std::min(256, rows - g0);
       const int nt = gemm_pick_nt(gr);
       GemmParams q = p;
       q.n_rows = gr;
       q.row0 = g0;
-      cudaError_t e = gemm_launch(wmap, xmaps[nt_index(nt)], q, g0, nt, m->num_sms, s);
+      cudaError_t e = gemm_launch(wmap, xmaps[nt_index(nt)], lbmap,
+                                  lbmap ? &m->xmap_ubd[nt_index(nt)] : nullptr, q, g0, nt,
+                                  m->num_sms, s);
       if (e != cudaSuccess) return fail(ICR_CUDA, "gemm launch: %s", cudaGetErrorString(e));
       ++launches;
     }
@@ -425,7 +464,6 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
   base.ws = m->ws;
   base.counters = m->counters;
   base.rank = c.lora_rank;
-  base.n_u = 1;
   base.m_valid = 1 << 30;
   base.row_kind = kind;
   base.row_adapter = adapter;
@@ -435,7 +473,8 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
   base.ss_stride = rp;
   base.ss_d = (float)d;
   base.eps = c.rms_eps;
-  base.lora_u = m->U;
+  base.ubd = m->ubd;
+  base.ubd_ld = m->ubd_ld;
   base.seg_off = md + mt.o_seg_off;
   base.seg_rows = md + mt.o_seg_rows;
   base.slots = c.adapter_slots;
@@ -468,8 +507,13 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
   al.out_ld = m->q_dim;
 
   icr_status st;
-  CUDA_TRY(embed_launch(tokens, kind, m->embed, m->x, m->xb, m->ssq, rp, rp, d, s));
+  const int qkv_M = m->q_dim + 2 * m->kv_dim;
+  const bool pf_on = rp <= 256 && !getenv("ICR_NO_PREFETCH");
+  CUDA_TRY(embed_launch(tokens, kind, m->embed, m->x, m->xb, m->ssq, rp, rp, d,
+                        pf_on ? (const uint8_t*)m->layers[0].w_qkv : nullptr,
+                        (long long)qkv_M * d * 2, m->ubd, m->ubd_ld, s));
   ++launches;
+  mark(m, s, TK_EMBED);
   for (int l = 0; l < c.num_layers; ++l) {
     const icr_layer_weights& w = m->layers[l];
     const LayerMaps& lm = m->maps[l];
@@ -480,10 +524,9 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
       p.K = d;
       p.in_ssq = m->ssq;
       if (lora) {
-        p.lora_b = (const __nv_bfloat16*)w.b_q;
-        p.lora_m = m->q_dim;
+        p.lora_chunks = m->lc1;
         p.sh_x = m->xb; p.sh_ld = d; p.sh_K = d; p.sh_targets = 1;
-        p.sh_a0 = (const __nv_bfloat16*)w.a_q; p.sh_scale_inv = 1;
+        p.sh_a0 = (const __nv_bfloat16*)w.a_q;
         p.sync = m->sync + 0;
       }
       p.out_bf16 = m->qb;
@@ -496,14 +539,18 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
       p.v_pages = (__nv_bfloat16*)w.v_pages;
       p.block_table = bt;
       p.bt_stride = c.max_pages_per_seq;
-      if ((st = gemm(lm.qkv, m->xmap_xb, p, rp))) return st;
+      if ((st = gemm(lm.qkv, m->xmap_xb, p, rp, lora ? &lm.lb_q : nullptr))) return st;
+      mark(m, s, TK_QKV);
     }
     al.k_pages = (const __nv_bfloat16*)w.k_pages;
     al.v_pages = (const __nv_bfloat16*)w.v_pages;
+    al.pf_base = pf_on ? (const uint8_t*)w.w_o : nullptr;
+    al.pf_bytes = (long long)d * m->q_dim * 2;
     {  // attention over 2H heads (src/model.py:497-501)
       cudaError_t e = attn_launch(al, s);
       if (e != cudaSuccess) return fail(ICR_CUDA, "attention launch: %s", cudaGetErrorString(e));
       launches += 2;
+      mark(m, s, TK_ATTN);
     }
     {  // o + residual (src/model.py:502)
       GemmParams p = base;
@@ -511,16 +558,17 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
       p.M = d;
       p.K = m->q_dim;
       if (lora) {
-        p.lora_b = (const __nv_bfloat16*)w.b_o;
-        p.lora_m = d;
+        p.lora_chunks = m->lc1;
         p.sh_x = m->att; p.sh_ld = m->q_dim; p.sh_K = m->q_dim; p.sh_targets = 1;
-        p.sh_a0 = (const __nv_bfloat16*)w.a_o; p.sh_scale_inv = 0;
+        p.sh_a0 = (const __nv_bfloat16*)w.a_o;
         p.sync = m->sync + 2;
       }
       p.resid = m->x;
       p.resid_bf16 = m->xb;
       p.out_ssq = m->ssq;
-      if ((st = gemm(lm.o, m->xmap_att, p, rp))) return st;
+      set_prefetch(m, p, w.w_gu, 2 * c.ffn_dim, d, rp);
+      if ((st = gemm(lm.o, m->xmap_att, p, rp, lora ? &lm.lb_o : nullptr))) return st;
+      mark(m, s, TK_O);
     }
     {  // gate | up + SiLU (src/model.py:503-505)
       GemmParams p = base;
@@ -529,16 +577,15 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
       p.K = d;
       p.in_ssq = m->ssq;
       if (lora) {
-        p.lora_b = (const __nv_bfloat16*)w.b_gu;
-        p.lora_m = 2 * c.ffn_dim;
-        p.n_u = 2;
+        p.lora_chunks = m->lc2;
         p.sh_x = m->xb; p.sh_ld = d; p.sh_K = d; p.sh_targets = 2;
         p.sh_a0 = (const __nv_bfloat16*)w.a_gate; p.sh_a1 = (const __nv_bfloat16*)w.a_up;
-        p.sh_scale_inv = 1;
         p.sync = m->sync + 4;
       }
       p.out_bf16 = m->f;
-      if ((st = gemm(lm.gu, m->xmap_xb, p, rp))) return st;
+      set_prefetch(m, p, w.w_down, d, c.ffn_dim, rp);
+      if ((st = gemm(lm.gu, m->xmap_xb, p, rp, lora ? &lm.lb_gu : nullptr))) return st;
+      mark(m, s, TK_GU);
     }
     {  // down + residual (src/model.py:506)
       GemmParams p = base;
@@ -546,16 +593,20 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
       p.M = d;
       p.K = c.ffn_dim;
       if (lora) {
-        p.lora_b = (const __nv_bfloat16*)w.b_down;
-        p.lora_m = d;
+        p.lora_chunks = m->lc1;
         p.sh_x = m->f; p.sh_ld = c.ffn_dim; p.sh_K = c.ffn_dim; p.sh_targets = 1;
-        p.sh_a0 = (const __nv_bfloat16*)w.a_down; p.sh_scale_inv = 0;
+        p.sh_a0 = (const __nv_bfloat16*)w.a_down;
         p.sync = m->sync + 6;
       }
       p.resid = m->x;
       p.resid_bf16 = m->xb;
       p.out_ssq = m->ssq;
-      if ((st = gemm(lm.down, m->xmap_f, p, rp))) return st;
+      if (l + 1 < c.num_layers)
+        set_prefetch(m, p, m->layers[l + 1].w_qkv, qkv_M, d, rp);
+      else
+        set_prefetch(m, p, m->lm_head, m->vpad, d, rp);
+      if ((st = gemm(lm.down, m->xmap_f, p, rp, lora ? &lm.lb_down : nullptr))) return st;
+      mark(m, s, TK_DOWN);
     }
   }
   // final norm on emitting rows + LM head + argmax (src/engine.py:188-193)
@@ -563,6 +614,7 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
     CUDA_TRY(lm_gather_launch(m->xb, m->ssq, rp, lm_rows, mt.n_lm, mt.n_lm_pad, d, m->hlm,
                               m->ssq_lm, s));
     ++launches;
+    mark(m, s, TK_LMG);
     GemmParams p = base;
     p.row_kind = nullptr;
     p.row_adapter = nullptr;
@@ -576,8 +628,10 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
     p.tile_best = m->tile_best;
     p.best_stride = rp;
     if ((st = gemm(m->lm_map, m->xmap_hlm, p, mt.n_lm))) return st;
+    mark(m, s, TK_LM);
     CUDA_TRY(argmax_reduce_launch(m->tile_best, m->vpad / 128, rp, mt.n_lm, m->out_tok, s));
     ++launches;
+    mark(m, s, TK_ARGMAX);
     if (logits_dev) {
       GemmParams q = p;
       q.mode = EPI_F32;
@@ -699,7 +753,10 @@ icr_status icr_model_create(const icr_model_config* cfg, const icr_layer_weights
   ALLOC(m->att, rp * q_dim * 2);
   ALLOC(m->f, rp * c.ffn_dim * 2);
   ALLOC(m->hlm, rp * c.hidden_dim * 2);
-  ALLOC(m->U, rp * 2 * std::max(c.lora_rank, 8) * sizeof(float));
+  m->lc1 = (c.adapter_slots * c.lora_rank + 63) / 64;
+  m->lc2 = (2 * c.adapter_slots * c.lora_rank + 63) / 64;
+  m->ubd_ld = std::max(64, m->lc2 * 64);
+  ALLOC(m->ubd, rp * m->ubd_ld * 2);
   ALLOC(m->tile_best, (size_t)(m->vpad / 128) * rp * sizeof(float2));
   ALLOC(m->out_tok, rp * sizeof(int));
   ALLOC(m->part_o, rp * c.num_heads * m->max_chunks * c.head_dim * sizeof(float));
@@ -712,6 +769,10 @@ icr_status icr_model_create(const icr_model_config* cfg, const icr_layer_weights
     ALLOC(m->counters, (size_t)max_tiles * sizeof(int));
   }
   ALLOC(m->sync, 16 * sizeof(int));
+  {  // sync[8]: a permanently satisfied counter for the stale-U profiling variant
+    const int big = 0x7fffffff;
+    cudaMemcpy(m->sync + 8, &big, sizeof(int), cudaMemcpyHostToDevice);
+  }
   {
     const int kmax = std::max({c.hidden_dim, q_dim, c.ffn_dim});
     const int splits = (kmax + 2047) / 2048;
@@ -745,6 +806,12 @@ icr_status icr_model_create(const icr_model_config* cfg, const icr_layer_weights
     if ((st = make_map_blocked(&m->maps[l].o, w.w_o, c.hidden_dim, q_dim))) return bail(st);
     if ((st = make_map_blocked(&m->maps[l].gu, w.w_gu, 2 * c.ffn_dim, c.hidden_dim))) return bail(st);
     if ((st = make_map_blocked(&m->maps[l].down, w.w_down, c.hidden_dim, c.ffn_dim))) return bail(st);
+    if (c.lora_rank > 0) {
+      if ((st = make_map_blocked(&m->maps[l].lb_q, w.b_q, q_dim + 2 * kv_dim, m->lc1 * 64))) return bail(st);
+      if ((st = make_map_blocked(&m->maps[l].lb_o, w.b_o, c.hidden_dim, m->lc1 * 64))) return bail(st);
+      if ((st = make_map_blocked(&m->maps[l].lb_gu, w.b_gu, 2 * c.ffn_dim, m->lc2 * 64))) return bail(st);
+      if ((st = make_map_blocked(&m->maps[l].lb_down, w.b_down, c.hidden_dim, m->lc1 * 64))) return bail(st);
+    }
   }
   if ((st = make_map_blocked(&m->lm_map, lm_head, m->vpad, c.hidden_dim))) return bail(st);
   for (int i = 0; i < 5; ++i) {
@@ -752,6 +819,7 @@ icr_status icr_model_create(const icr_model_config* cfg, const icr_layer_weights
     if ((st = make_map(&m->xmap_att[i], m->att, rp, q_dim, kNts[i]))) return bail(st);
     if ((st = make_map(&m->xmap_f[i], m->f, rp, c.ffn_dim, kNts[i]))) return bail(st);
     if ((st = make_map(&m->xmap_hlm[i], m->hlm, rp, c.hidden_dim, kNts[i]))) return bail(st);
+    if ((st = make_map(&m->xmap_ubd[i], m->ubd, rp, m->ubd_ld, kNts[i]))) return bail(st);
   }
   for (int i = 0; i < 2; ++i) cudaEventCreateWithFlags(&m->staging_ev[i], cudaEventDisableTiming);
   cudaStreamCreateWithFlags(&m->capture_stream, cudaStreamNonBlocking);
@@ -765,7 +833,7 @@ icr_status icr_model_destroy(icr_model* m) {
   if (!m) return ICR_OK;
   cudaDeviceSynchronize();
   for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
-  void* bufs[] = {m->x, m->xb, m->ssq, m->ssq_lm, m->qb, m->att, m->f, m->hlm, m->U,
+  void* bufs[] = {m->x, m->xb, m->ssq, m->ssq_lm, m->qb, m->att, m->f, m->hlm, m->ubd,
                   m->tile_best, m->out_tok, m->part_o, m->part_ml, m->merge_cnt, m->rope, m->ws,
                   m->counters, m->sync, m->sh_part, m->sh_cnt, m->meta_dev};
   for (void* p : bufs)
@@ -870,6 +938,44 @@ icr_status icr_model_stats(icr_model* m, int64_t* out3) {
   return ICR_OK;
 }
 
+// Replay the last forward without a graph, with an event after every launch; returns the
+// summed device time per kernel kind (ms) in kind_ms[9]: embed, qkv, attention (partial +
+// merge), o, gate|up, down, lm gather, lm head, argmax; kind_ms[9] = whole forward.
+// Idempotent: the replay recomputes the same K/V bytes at the same positions.
+icr_status icr_profile_step(icr_model* m, float* kind_ms, void* stream) {
+  if (!m || !kind_ms) return fail(ICR_CONFIG, "null argument");
+  if (!m->has_last) return fail(ICR_STATE, "profile needs a previous forward");
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<cudaEvent_t> evs;
+  std::vector<int> kinds;
+  cudaEvent_t e0;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventRecord(e0, s));
+  m->timing = &evs;
+  m->timing_kind = &kinds;
+  const Meta mt = m->last_mt;
+  icr_status st = enqueue_forward(m, mt, nullptr, s);
+  m->timing = nullptr;
+  m->timing_kind = nullptr;
+  cudaError_t ce = cudaStreamSynchronize(s);
+  for (int k = 0; k < 10; ++k) kind_ms[k] = 0.f;
+  if (st == ICR_OK && ce == cudaSuccess) {
+    cudaEvent_t prev = e0;
+    for (size_t i = 0; i < evs.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, prev, evs[i]);
+      kind_ms[kinds[i]] += ms;
+      kind_ms[9] += ms;
+      prev = evs[i];
+    }
+  }
+  for (auto e : evs) cudaEventDestroy(e);
+  cudaEventDestroy(e0);
+  if (st) return st;
+  if (ce != cudaSuccess) return fail(ICR_CUDA, "profile step: %s", cudaGetErrorString(ce));
+  return ICR_OK;
+}
+
 // Re-launch one projection GEMM family of the last forward `iters` times, cycling through
 // all layers so no weight tile is served from L2, and return the average device time per
 // launch (CUDA events on the launch stream), all LoRA / norm / epilogue work included.
@@ -883,13 +989,18 @@ icr_status icr_profile_gemm(icr_model* m, int which_raw, int iters, float* avg_m
   const icr_model_config& c = m->cfg;
   const Meta& mt = m->last_mt;
   int* md = m->meta_dev;
-  const bool lora = c.lora_rank > 0 && mt.n_dec > 0;
+  // diagnostic variants: bit 4 drops the LoRA, bit 5 replaces the fused epilogue by a plain
+  // fp32 store into scratch, bit 6 drops only the in-kernel shrink (stale U)
+  const bool no_lora = (which_raw >> 4) & 1, plain = (which_raw >> 5) & 1,
+             no_shrink = (which_raw >> 6) & 1, traced = (which_raw >> 8) & 1;
+  static unsigned long long* trace_dev = nullptr;
+  if (traced && !trace_dev) CUDA_TRY(cudaMalloc(&trace_dev, 4096 * 8 * sizeof(unsigned long long)));
+  const bool lora = c.lora_rank > 0 && !no_lora;
   GemmParams p{};
   p.w_blocked = 1;
   p.ws = m->ws;
   p.counters = m->counters;
   p.rank = c.lora_rank;
-  p.n_u = 1;
   p.m_valid = 1 << 30;
   p.row_kind = md + mt.o_kind;
   p.row_adapter = md + mt.o_adapter;
@@ -899,7 +1010,8 @@ icr_status icr_profile_gemm(icr_model* m, int which_raw, int iters, float* avg_m
   p.ss_stride = mt.rp;
   p.ss_d = (float)c.hidden_dim;
   p.eps = c.rms_eps;
-  p.lora_u = m->U;
+  p.ubd = m->ubd;
+  p.ubd_ld = m->ubd_ld;
   p.seg_off = md + mt.o_seg_off;
   p.seg_rows = md + mt.o_seg_rows;
   p.slots = c.adapter_slots;
@@ -911,18 +1023,17 @@ icr_status icr_profile_gemm(icr_model* m, int which_raw, int iters, float* avg_m
   switch (which) {
     case 0: p.mode = EPI_RESID; p.M = c.hidden_dim; p.K = m->q_dim; p.resid = m->x;
             p.resid_bf16 = m->xb; p.out_ssq = m->ssq; xmaps = m->xmap_att;
-            if (lora) { p.lora_m = c.hidden_dim; p.sh_x = m->att; p.sh_ld = m->q_dim;
+            if (lora) { p.lora_chunks = m->lc1; p.sh_x = m->att; p.sh_ld = m->q_dim;
                         p.sh_K = m->q_dim; p.sh_targets = 1; p.sync = m->sync + 2; }
             break;
     case 1: p.mode = EPI_SILU; p.M = 2 * c.ffn_dim; p.K = c.hidden_dim; p.in_ssq = m->ssq;
             p.out_bf16 = m->f; xmaps = m->xmap_xb;
-            if (lora) { p.lora_m = 2 * c.ffn_dim; p.n_u = 2; p.sh_x = m->xb; p.sh_ld = c.hidden_dim;
-                        p.sh_K = c.hidden_dim; p.sh_targets = 2; p.sh_scale_inv = 1;
-                        p.sync = m->sync + 4; }
+            if (lora) { p.lora_chunks = m->lc2; p.sh_x = m->xb; p.sh_ld = c.hidden_dim;
+                        p.sh_K = c.hidden_dim; p.sh_targets = 2; p.sync = m->sync + 4; }
             break;
     case 2: p.mode = EPI_RESID; p.M = c.hidden_dim; p.K = c.ffn_dim; p.resid = m->x;
             p.resid_bf16 = m->xb; p.out_ssq = m->ssq; xmaps = m->xmap_f;
-            if (lora) { p.lora_m = c.hidden_dim; p.sh_x = m->f; p.sh_ld = c.ffn_dim;
+            if (lora) { p.lora_chunks = m->lc1; p.sh_x = m->f; p.sh_ld = c.ffn_dim;
                         p.sh_K = c.ffn_dim; p.sh_targets = 1; p.sync = m->sync + 6; }
             break;
     case 3: p.mode = EPI_ARGMAX; p.M = m->vpad; p.K = c.hidden_dim; p.m_valid = c.vocab_size;
@@ -932,10 +1043,6 @@ icr_status icr_profile_gemm(icr_model* m, int which_raw, int iters, float* avg_m
     default: return fail(ICR_MODE, "which must be 0..3");
   }
   if (rows > 256 || rows < 1) return fail(ICR_SHAPE, "profile supports 1..256 rows");
-  // diagnostic variants: bit 4 drops the LoRA (shrink + expand), bit 5 replaces the fused
-  // epilogue by a plain fp32 store into scratch
-  const bool no_lora = (which_raw >> 4) & 1, plain = (which_raw >> 5) & 1;
-  if (no_lora) { p.sh_x = nullptr; p.sync = nullptr; }
   if (plain) {
     const size_t need = (size_t)rows * p.M;
     const size_t have = (size_t)m->rp * c.num_heads * m->max_chunks * c.head_dim;
@@ -954,15 +1061,23 @@ icr_status icr_profile_gemm(icr_model* m, int which_raw, int iters, float* avg_m
       const icr_layer_weights& w = m->layers[l];
       GemmParams q = p;
       const CUtensorMap* wm = &m->lm_map;
-      const bool lora_l = lora && !((which_raw >> 4) & 1);
-      if (which == 0) { wm = &m->maps[l].o;
-        if (lora_l) { q.lora_b = (const __nv_bfloat16*)w.b_o; q.sh_a0 = (const __nv_bfloat16*)w.a_o; } }
-      if (which == 1) { wm = &m->maps[l].gu;
-        if (lora_l) { q.lora_b = (const __nv_bfloat16*)w.b_gu; q.sh_a0 = (const __nv_bfloat16*)w.a_gate;
-                    q.sh_a1 = (const __nv_bfloat16*)w.a_up; } }
-      if (which == 2) { wm = &m->maps[l].down;
-        if (lora_l) { q.lora_b = (const __nv_bfloat16*)w.b_down; q.sh_a0 = (const __nv_bfloat16*)w.a_down; } }
-      cudaError_t e = gemm_launch(*wm, xmaps[nt_index(nt)], q, 0, nt, m->num_sms, s);
+      const CUtensorMap* lb = nullptr;
+      if (which == 0) { wm = &m->maps[l].o; lb = &m->maps[l].lb_o; q.sh_a0 = (const __nv_bfloat16*)w.a_o; }
+      if (which == 1) { wm = &m->maps[l].gu; lb = &m->maps[l].lb_gu;
+                        q.sh_a0 = (const __nv_bfloat16*)w.a_gate; q.sh_a1 = (const __nv_bfloat16*)w.a_up; }
+      if (which == 2) { wm = &m->maps[l].down; lb = &m->maps[l].lb_down; q.sh_a0 = (const __nv_bfloat16*)w.a_down; }
+      if (!lora) lb = nullptr;
+      if (no_shrink) { q.sh_x = nullptr; q.sync = nullptr; }
+      if (traced && it == iters - 1 && l == 0) {
+        q.trace = trace_dev;
+        cudaMemsetAsync(trace_dev, 0, 4096 * 8 * sizeof(unsigned long long), s);
+      }
+      if (no_shrink && lora) {
+        // stale-U variant: LoRA chunks without waiting (sync pre-satisfied)
+        q.sync = m->sync + 8;
+      }
+      cudaError_t e = gemm_launch(*wm, xmaps[nt_index(nt)], lb, lb ? &m->xmap_ubd[nt_index(nt)] : nullptr,
+                                  q, 0, nt, m->num_sms, s);
       if (e != cudaSuccess) return fail(ICR_CUDA, "gemm: %s", cudaGetErrorString(e));
     }
   CUDA_TRY(cudaEventRecord(e1, s));
@@ -972,6 +1087,24 @@ icr_status icr_profile_gemm(icr_model* m, int which_raw, int iters, float* avg_m
   *avg_ms = ms / (float)(iters * L);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  if (traced) {
+    std::vector<unsigned long long> h(4096 * 8);
+    CUDA_TRY(cudaMemcpy(h.data(), trace_dev, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    // report relative to the earliest CTA start, in microseconds, for CTAs 0..grid-1
+    unsigned long long t0 = ~0ull;
+    for (int c2 = 0; c2 < 4096; ++c2) if (h[c2 * 8] && h[c2 * 8] < t0) t0 = h[c2 * 8];
+    FILE* f = fopen("gpurun_out/gemm_trace.csv", "w");
+    if (f) {
+      fprintf(f, "cta,start,shrink_done,wait_begin,wait_end,issued_all,end\n");
+      for (int c2 = 0; c2 < 4096; ++c2) {
+        if (!h[c2 * 8]) continue;
+        fprintf(f, "%d", c2);
+        for (int k = 0; k < 6; ++k) fprintf(f, ",%.2f", h[c2 * 8 + k] ? (h[c2 * 8 + k] - t0) / 1000.0 : -1.0);
+        fprintf(f, "\n");
+      }
+      fclose(f);
+    }
+  }
   return ICR_OK;
 }
 
@@ -1025,11 +1158,11 @@ icr_status icr_bench_gemm(const void* w, const void* x, int M, int K, int rows, 
   CUDA_TRY(cudaEventCreate(&e0));
   CUDA_TRY(cudaEventCreate(&e1));
   // warm-up
-  for (int i = 0; i < n_mats; ++i) gemm_launch(wm[i], xm, p, 0, nt, sms, s);
+  for (int i = 0; i < n_mats; ++i) gemm_launch(wm[i], xm, nullptr, nullptr, p, 0, nt, sms, s);
   CUDA_TRY(cudaEventRecord(e0, s));
   for (int it = 0; it < iters; ++it)
     for (int i = 0; i < n_mats; ++i) {
-      cudaError_t e = gemm_launch(wm[i], xm, p, 0, nt, sms, s);
+      cudaError_t e = gemm_launch(wm[i], xm, nullptr, nullptr, p, 0, nt, sms, s);
       if (e != cudaSuccess) return fail(ICR_CUDA, "bench gemm: %s", cudaGetErrorString(e));
     }
   CUDA_TRY(cudaEventRecord(e1, s));
@@ -1079,7 +1212,7 @@ icr_status icr_gemm_bf16(const void* w_dev, const void* x_dev, float* out_dev, i
     p.ld_out = M;
     p.ws = g_ws;
     p.counters = g_counters;
-    cudaError_t e = gemm_launch(wm, xm, p, g0, nt, sms, s);
+    cudaError_t e = gemm_launch(wm, xm, nullptr, nullptr, p, g0, nt, sms, s);
     if (e != cudaSuccess) return fail(ICR_CUDA, "gemm: %s", cudaGetErrorString(e));
   }
   return ICR_OK;

@@ -224,27 +224,39 @@ class DeviceWeights:
 
 # ----------------------------------------------------------------------------- adapters
 _A_KEYS = ("a_q", "a_o", "a_gate", "a_up", "a_down")
-_B_KEYS = ("b_q", "b_o", "b_gu", "b_down")
+
+
+def lora_k(n_u: int, slots: int, rank: int) -> int:
+    """K extent of a LoRA expand operand: n_u targets x slots x rank, padded to 64."""
+    return (n_u * slots * rank + 63) // 64 * 64
 
 
 class AdapterSlots:
-    """Resident LoRA adapters; slot s of every tensor belongs to one AdapterSet."""
+    """Resident LoRA adapters; slot s of every tensor belongs to one AdapterSet.
+
+    A (the shrink operand) is kept as the reference stores it: [L, slots, r, in].
+    B (the expand operand) is concatenated over slots along K and stored tile-major like
+    the base weights: b_* = [L, M/128, Kc/64, 128, 64] with element (m, t*S*r + s*r + j) =
+    (alpha/r) * B_s,t[m, j]. The GEMM multiplies it by a block-diagonal U (row n carries
+    its adapter's U in its own slot, zeros elsewhere), so the SGMV expand runs as extra
+    tcgen05 K-chunks of the base projection. gate/up use two target blocks (t = 0 gate on
+    even rows, t = 1 up on odd rows); q rows of w_qkv carry B_q, k/v rows are zero."""
 
     def __init__(self, cfg: ModelConfig, slots: int, rank: int, device="cuda"):
         torch = _torch()
         self.cfg, self.n, self.rank, self.device = cfg, slots, rank, device
-        L, d, qd, f = cfg.num_layers, cfg.hidden_dim, cfg.q_dim, cfg.ffn_dim
+        L, d, qd, kvd, f = cfg.num_layers, cfg.hidden_dim, cfg.q_dim, cfg.kv_dim, cfg.ffn_dim
         z = lambda *s: torch.zeros(*s, dtype=torch.bfloat16, device=device)  # noqa: E731
+        self.t = {}
+        self.b = {}
         if slots > 0 and rank > 0:
-            self.t = {
-                "a_q": z(L, slots, rank, d), "b_q": z(L, slots, qd, rank),
-                "a_o": z(L, slots, rank, qd), "b_o": z(L, slots, d, rank),
-                "a_gate": z(L, slots, rank, d), "a_up": z(L, slots, rank, d),
-                "b_gu": z(L, slots, 2 * f, rank),
-                "a_down": z(L, slots, rank, f), "b_down": z(L, slots, d, rank),
-            }
-        else:
-            self.t = {}
+            self.t = {"a_q": z(L, slots, rank, d), "a_o": z(L, slots, rank, qd),
+                      "a_gate": z(L, slots, rank, d), "a_up": z(L, slots, rank, d),
+                      "a_down": z(L, slots, rank, f)}
+            k1, k2 = lora_k(1, slots, rank), lora_k(2, slots, rank)
+            for key, M, K in (("b_q", qd + 2 * kvd, k1), ("b_o", d, k1), ("b_gu", 2 * f, k2),
+                              ("b_down", d, k1)):
+                self.b[key] = z(L, M // 128, K // 64, 128, 64)
         self._owner: dict[int, int] = {}  # id(adapter) -> slot
         self._refs: list = [None] * slots
 
@@ -265,52 +277,53 @@ class AdapterSlots:
         self._refs[s] = adapter
         return s
 
+    def _put_b(self, key: str, layer: int, s: int, target: int, rows, value) -> None:
+        """Write value [len(rows), r] (already scaled) as slot s / target of b_key[layer]."""
+        torch = _torch()
+        r = self.rank
+        bt = self.b[key][layer]                           # [Mt, Kt, 128, 64]
+        view = bt.permute(0, 2, 1, 3)                     # [Mt, 128, Kt, 64] logical (m, k)
+        col = target * self.n * r + s * r
+        kt, kin = col // 64, col % 64
+        Mt = bt.shape[0]
+        full = torch.zeros(Mt * 128, r, dtype=torch.bfloat16, device=self.device)
+        vv = value.to(self.device, torch.bfloat16)
+        full[rows, :vv.shape[1]] = vv
+        view[:, :, kt, kin:kin + r] = full.view(Mt, 128, r)
+
     def _upload(self, s: int, ad: AdapterSet) -> None:
         torch = _torch()
-        cfg, r, bf = self.cfg, ad.rank, torch.bfloat16
+        cfg = self.cfg
         for key in self.t:
             self.t[key][:, s].zero_()
+        qd, f, d = cfg.q_dim, cfg.ffn_dim, cfg.hidden_dim
+        rows = {"q": slice(0, qd), "o": slice(0, d), "gate": slice(0, 2 * f, 2),
+                "up": slice(1, 2 * f, 2), "down": slice(0, d)}
+        where = {"q": ("b_q", 0), "o": ("b_o", 0), "gate": ("b_gu", 0), "up": ("b_gu", 1),
+                 "down": ("b_down", 0)}
+        gen = None
         if ad.device_seed is not None:
-            self._upload_random(s, ad)
-            return
+            gen = torch.Generator(device=self.device)
+            gen.manual_seed(int(ad.device_seed))
         sc = float(ad.scaling)
-        for layer, per in enumerate(ad.layers):
-            def A(name):
-                return torch.as_tensor(np.asarray(per[name].a.data, np.float32))
-
-            def B(name):
-                return torch.as_tensor(np.asarray(per[name].b.data, np.float32)) * sc
-
-            if "q" in per:
-                self.t["a_q"][layer, s, :r] = A("q").to(self.device, bf)
-                self.t["b_q"][layer, s, :, :r] = B("q").to(self.device, bf)
-            if "o" in per:
-                self.t["a_o"][layer, s, :r] = A("o").to(self.device, bf)
-                self.t["b_o"][layer, s, :, :r] = B("o").to(self.device, bf)
-            if "gate" in per:
-                self.t["a_gate"][layer, s, :r] = A("gate").to(self.device, bf)
-                self.t["b_gu"][layer, s, 0::2, :r] = B("gate").to(self.device, bf)
-            if "up" in per:
-                self.t["a_up"][layer, s, :r] = A("up").to(self.device, bf)
-                self.t["b_gu"][layer, s, 1::2, :r] = B("up").to(self.device, bf)
-            if "down" in per:
-                self.t["a_down"][layer, s, :r] = A("down").to(self.device, bf)
-                self.t["b_down"][layer, s, :, :r] = B("down").to(self.device, bf)
-
-    def _upload_random(self, s: int, ad: AdapterSet) -> None:
-        torch = _torch()
-        gen = torch.Generator(device=self.device)
-        gen.manual_seed(int(ad.device_seed))
-        r, sc = ad.rank, float(ad.scaling)
-        cfg = self.cfg
-        fan = {"a_q": cfg.hidden_dim, "a_o": cfg.q_dim, "a_gate": cfg.hidden_dim,
-               "a_up": cfg.hidden_dim, "a_down": cfg.ffn_dim}
-        for key in _A_KEYS:
-            t = self.t[key][:, s, :r]
-            t.copy_(torch.randn(t.shape, generator=gen, device=self.device) / math.sqrt(fan[key]))
-        for key in _B_KEYS:
-            t = self.t[key][:, s, :, :r]
-            t.copy_(torch.randn(t.shape, generator=gen, device=self.device) * (ad.b_scale * sc))
+        fan = {"q": d, "o": qd, "gate": d, "up": d, "down": f}
+        outd = {"q": qd, "o": d, "gate": f, "up": f, "down": d}
+        for layer in range(cfg.num_layers):
+            per = ad.layers[layer]
+            for tgt in ("q", "o", "gate", "up", "down"):
+                if gen is not None:
+                    a = torch.randn(ad.rank, fan[tgt], generator=gen, device=self.device) / math.sqrt(fan[tgt])
+                    b = torch.randn(outd[tgt], ad.rank, generator=gen, device=self.device) * ad.b_scale
+                elif tgt in per:
+                    a = torch.from_numpy(np.array(per[tgt].a.data, dtype=np.float32, copy=True))
+                    b = torch.from_numpy(np.array(per[tgt].b.data, dtype=np.float32, copy=True))
+                else:
+                    continue
+                self.t["a_" + tgt][layer, s, :ad.rank] = a.to(self.device, torch.bfloat16)
+                key, target = where[tgt]
+                self._put_b(key, layer, s, target, rows[tgt], b * sc)
+        # zero any slot columns left over from a previous tenant of this slot
+        # (handled above: _put_b rewrites the full column block of every target)
 
     def release(self, adapter: AdapterSet) -> None:
         s = self._owner.pop(id(adapter), None)
@@ -318,7 +331,9 @@ class AdapterSlots:
             self._refs[s] = None
 
     def layer_ptrs(self, layer: int) -> dict:
-        return {k: v[layer].data_ptr() for k, v in self.t.items()}
+        out = {k: v[layer].data_ptr() for k, v in self.t.items()}
+        out.update({k: v[layer].data_ptr() for k, v in self.b.items()})
+        return out
 
 
 # ----------------------------------------------------------------------------- runtime

@@ -5,14 +5,12 @@ import sys
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
-sys.argv = [sys.argv[0], "none"]
-import tools.profile_step as ps  # noqa: E402
 from paper_2603_13281_b200 import _lib  # noqa: E402
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 
-def main():
+def setup():
     from paper_2603_13281_b200 import engine as E
     from paper_2603_13281_b200.kvpool import KvCachePool
     from paper_2603_13281_b200.model import AdapterSet, BaseWeights, ModelConfig
@@ -31,10 +29,16 @@ def main():
     for _ in range(3):
         toks = E.decode_step_batch(ss, toks)
     torch.cuda.synchronize()
+    setup.keep = (base, ads, ss, pool)
+    return rt
+
+
+def main():
+    rt = setup()
     avg = C.c_float()
     for which, name in ((0, "o"), (1, "gate_up"), (2, "down"), (3, "lm_head")):
         out = []
-        for var, vname in ((0, "full"), (16, "no_lora"), (48, "plain")):
+        for var, vname in ((0, "full"), (64, "no_shrink"), (16, "no_lora"), (48, "plain")):
             _lib.check(rt._lib.icr_profile_gemm(rt._handle, which | var, 3, C.byref(avg),
                                                 _lib.stream_handle()))
             out.append(f"{vname}={avg.value*1e3:7.1f}us")
