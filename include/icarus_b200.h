@@ -157,6 +157,15 @@ icr_status icr_bench_gemm(const void* w, const void* x, int M, int K, int rows, 
                           int blocked, int stages, int ctas_per_sm, int skip_mma, int iters,
                           float* avg_ms, void* stream);
 
+/* Paged-attention micro-benchmark (C4 sweep): plan once, time `iters` launches of the
+ * partial + merge kernels (memset of flush_dev between launches evicts L2 when non-NULL). */
+icr_status icr_bench_attention(const void* q_dev, const void* k_pages, const void* v_pages,
+                               int num_heads, int num_kv_heads, int head_dim, int chunk_pages,
+                               int n_rows, const int32_t* row_seq_host, const int32_t* row_pos_host,
+                               const int32_t* block_table_host, int n_seqs, int max_pages_per_seq,
+                               void* out_dev, void* flush_dev, long long flush_bytes, int iters,
+                               float* avg_ms, int32_t* n_items_out, void* stream);
+
 /* --- building blocks, exported for parity tests -------------------------------- */
 
 /* out_f32[n, m] = sum_k W[m, k] X[n, k]; W [M, K] bf16 (dev), X [n_rows, K] bf16 (dev).

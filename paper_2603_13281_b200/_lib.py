@@ -24,7 +24,8 @@ _STATUS = {
 # Every symbol the header declares; tests/test_capi.py checks the library exports them.
 EXPORTED = (
     "icr_model_create", "icr_model_destroy", "icr_forward", "icr_decode_loop",
-    "icr_model_stats", "icr_profile_step", "icr_profile_gemm", "icr_bench_gemm", "icr_gemm_bf16", "icr_paged_attention",
+    "icr_model_stats", "icr_profile_step", "icr_profile_gemm", "icr_bench_gemm",
+    "icr_bench_attention", "icr_gemm_bf16", "icr_paged_attention",
     "icr_last_error", "icr_abi_version", "icr_num_sms",
 )
 
@@ -73,6 +74,9 @@ def load():
         "icr_profile_step": [p, C.POINTER(C.c_float), p],
         "icr_bench_gemm": [p, p, i, i, i, i, i, i, i, i, i, C.POINTER(C.c_float), p],
         "icr_gemm_bf16": [p, p, p, i, i, i, p],
+        "icr_bench_attention": [p, p, p, i, i, i, i, i, C.POINTER(C.c_int32),
+                                C.POINTER(C.c_int32), C.POINTER(C.c_int32), i, i, p, p,
+                                C.c_longlong, i, C.POINTER(C.c_float), C.POINTER(C.c_int32), p],
         "icr_paged_attention": [p, p, p, i, i, i, i, i, C.POINTER(C.c_int32),
                                 C.POINTER(C.c_int32), C.POINTER(C.c_int32), i, i, p,
                                 C.POINTER(C.c_int32), p],

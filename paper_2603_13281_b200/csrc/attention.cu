@@ -61,65 +61,89 @@ __device__ __forceinline__ uint32_t swz(int row, int chunk) {
   return (uint32_t)(row * HD * 2 + ((chunk ^ (row & 7)) << 4));
 }
 
-constexpr int PAGE_STAGES = 8;  // K/V pages in flight per CTA (two per pipeline step)
+constexpr int PAGE_STAGES = 16;  // K/V pages in flight per CTA (TMA ring, 8 KB each)
+constexpr int ATTN_THREADS = 288;  // warp 0: TMA producer; warps 1..8: consumers
 
 template <int HD>
-constexpr size_t attn_smem() { return (size_t)64 * HD * 2 + (size_t)PAGE_STAGES * 2 * 16 * HD * 2; }
-
-// 8 warps: warp w owns query rows [16*(w&3), +16) and the chunk's pages of parity (w>>2).
-// The two page-parity halves keep separate online-softmax states and are combined at the
-// end in a fixed order (even pages first), so a row's partial depends only on its own query,
-// the chunk's keys and its position.
+__host__ __device__ constexpr uint32_t page_bytes() { return 16 * HD * 2; }  // one K (or V) page of one head
 template <int HD>
-__global__ void __launch_bounds__(256, 2)
-    attn_partial_kernel(const __nv_bfloat16* __restrict__ q, int q_ld,
-                        const __nv_bfloat16* __restrict__ k_pages,
-                        const __nv_bfloat16* __restrict__ v_pages, int num_kv_heads, int group,
-                        const AttnItem* __restrict__ items, const int* __restrict__ item_pages,
-                        const int2* __restrict__ item_rows, const int* __restrict__ row_pos,
-                        int num_heads, int max_chunks, float scale, float* __restrict__ part_o,
-                        float2* __restrict__ part_ml, const int* __restrict__ n_items_dev,
-                        const uint8_t* __restrict__ pf_base, long long pf_bytes) {
+constexpr size_t attn_smem() {
+  return 1024 + (size_t)PAGE_STAGES * 2 * page_bytes<HD>() + (size_t)64 * HD * 2 + 256;
+}
+
+// Page tile in smem as written by TMA with 128-byte swizzle: HD/64 halves of [16 keys][128 B],
+// 16-byte chunk c of key row r at (c ^ (r & 7)) -- exactly what ldmatrix reads conflict-free.
+template <int HD>
+__device__ __forceinline__ uint32_t page_off(int key, int ch) {
+  return (uint32_t)((ch >> 3) * 2048 + key * 128 + (((ch & 7) ^ (key & 7)) << 4));
+}
+
+// Warp-specialised shared-page attention. The producer warp streams each page of the chunk
+// (K and V for this KV head) into a PAGE_STAGES-deep smem ring with TMA; 8 consumer warps
+// -- 4 query-row groups x 2 page parities -- read every staged page for ALL rows of the
+// item (the encoder and decoder heads of every sequence sharing the pages), with per-stage
+// mbarriers instead of block barriers. The two page-parity states are combined at the end
+// in a fixed order, so a row's partial depends only on its own query, the chunk's keys and
+// its position.
+template <int HD>
+__global__ void __launch_bounds__(ATTN_THREADS, 1)
+    attn_partial_kernel(const __grid_constant__ CUtensorMap tm_k,
+                        const __grid_constant__ CUtensorMap tm_v, const __nv_bfloat16* __restrict__ q,
+                        int q_ld, int num_kv_heads, int group, const AttnItem* __restrict__ items,
+                        const int* __restrict__ item_pages, const int2* __restrict__ item_rows,
+                        const int* __restrict__ row_pos, int num_heads, int max_chunks, float scale,
+                        float* __restrict__ part_o, float2* __restrict__ part_ml,
+                        const int* __restrict__ n_items_dev, const uint8_t* __restrict__ pf_base,
+                        long long pf_bytes) {
   constexpr int CH = HD / 8;  // 16-byte chunks per row
-  extern __shared__ __align__(128) uint8_t attn_smem_raw[];
+  constexpr uint32_t PB = page_bytes<HD>();
+  extern __shared__ uint8_t attn_smem_raw[];
+  uint8_t* base = attn_smem_raw + ((1024 - (smem_u32(attn_smem_raw) & 1023)) & 1023);
+  uint8_t* ring = base;                                   // [stage][K | V] pages
+  __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(ring + PAGE_STAGES * 2 * PB);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sQ + 64 * HD);
+  uint64_t* empty = full + PAGE_STAGES;
+
   // attention moves few bytes: use the idle HBM to pull the o-projection weights into L2
   prefetch_slice_l2(pf_base, pf_bytes, blockIdx.y * gridDim.x + blockIdx.x, gridDim.x * gridDim.y);
-  __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(attn_smem_raw);
-  __nv_bfloat16* sKV = sQ + 64 * HD;  // [stage][K | V][16][HD]
-
   pdl_launch();
   const int item_id = blockIdx.x;
   if (item_id >= *n_items_dev) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int i = 0; i < PAGE_STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 4); }
+    fence_barrier_init();
+  }
+  __syncthreads();
   pdl_wait();
   const AttnItem it = items[item_id];
   const int g = blockIdx.y;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int rg = warp & 3, kg = warp >> 2;
 
-  auto load_page = [&](int pi) {
-    const int buf = pi % PAGE_STAGES;
-    const int page = item_pages[it.page_off + pi];
-    const size_t off = ((size_t)page * num_kv_heads + g) * 16 * HD;
-    const uint8_t* ks = reinterpret_cast<const uint8_t*>(k_pages + off);
-    const uint8_t* vs = reinterpret_cast<const uint8_t*>(v_pages + off);
-    const uint32_t kd = smem_u32(sKV + (size_t)buf * 32 * HD), vd = kd + 16 * HD * 2;
-    for (int idx = tid; idx < 16 * CH; idx += 256) {
-      const int row = idx / CH, ch = idx % CH;
-      cp_async16(kd + swz<HD>(row, ch), ks + idx * 16);
-      cp_async16(vd + swz<HD>(row, ch), vs + idx * 16);
-    }
-  };
-  const int n_steps = (it.n_pages + 1) / 2;
-  // ring prologue: steps 0 .. PAGE_STAGES/2 - 2 (two pages each) in flight before Q
+  if (warp == 0) {
+    // ---------------- producer: TMA page ring ----------------
+    if (elect_one()) {
+      tma_prefetch_desc(&tm_k);
+      tma_prefetch_desc(&tm_v);
+      for (int pi = 0; pi < it.n_pages; ++pi) {
+        const int st = pi % PAGE_STAGES;
+        mbar_wait(&empty[st], ((pi / PAGE_STAGES) & 1) ^ 1);
+        const int plane = item_pages[it.page_off + pi] * num_kv_heads + g;
+        uint8_t* kd = ring + (size_t)st * 2 * PB;
+        mbar_expect_tx(&full[st], 2 * PB);
 #pragma unroll
-  for (int st = 0; st < PAGE_STAGES / 2 - 1; ++st) {
-    if (2 * st < it.n_pages) load_page(2 * st);
-    if (2 * st + 1 < it.n_pages) load_page(2 * st + 1);
-    cp_async_commit();
+        for (int h = 0; h < HD / 64; ++h) {
+          tma_load_3d(kd + h * 2048, &tm_k, &full[st], h * 64, 0, plane);
+          tma_load_3d(kd + PB + h * 2048, &tm_v, &full[st], h * 64, 0, plane);
+        }
+      }
+    }
+    return;
   }
 
-  // ---- stage Q rows (swizzled) ----
-  for (int idx = tid; idx < 64 * CH; idx += 256) {
+  // ---------------- consumers ----------------
+  const int cw = warp - 1, rg = cw & 3, kg = cw >> 2;
+  const int ctid = tid - 32;
+  for (int idx = ctid; idx < 64 * CH; idx += 256) {
     const int row = idx / CH, ch = idx % CH;
     uint4 val = make_uint4(0, 0, 0, 0);
     if (row < it.n_rows) {
@@ -129,7 +153,7 @@ __global__ void __launch_bounds__(256, 2)
     }
     *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(sQ) + swz<HD>(row, ch)) = val;
   }
-  __syncthreads();
+  named_bar_sync(1, 256);
 
   const int r_lo = rg * 16 + (lane >> 2);  // rows r_lo and r_lo + 8 of the item
   const bool active = rg * 16 < it.n_rows;
@@ -153,27 +177,19 @@ __global__ void __launch_bounds__(256, 2)
   for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
   float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;
 
-  for (int st = 0; st < n_steps; ++st) {
-    {
-      const int nxt = st + PAGE_STAGES / 2 - 1;
-      if (2 * nxt < it.n_pages) load_page(2 * nxt);
-      if (2 * nxt + 1 < it.n_pages) load_page(2 * nxt + 1);
-      cp_async_commit();
-    }
-    cp_async_wait<PAGE_STAGES / 2 - 1>();
-    __syncthreads();
-    const int pi = 2 * st + kg;
-    if (active && pi < it.n_pages) {
-      const int buf = pi % PAGE_STAGES;
+  for (int pi = kg; pi < it.n_pages; pi += 2) {
+    const int st = pi % PAGE_STAGES;
+    mbar_wait(&full[st], (pi / PAGE_STAGES) & 1);
+    if (active) {
       // S = Q K^T for 16 keys (two n8 tiles)
       float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-      const uint32_t kbase = smem_u32(sKV + (size_t)buf * 32 * HD);
+      const uint32_t kbase = smem_u32(ring + (size_t)st * 2 * PB);
 #pragma unroll
       for (int kk = 0; kk < HD / 16; ++kk) {
         const int key = (lane & 7) + ((lane >> 4) << 3);
         const int ch = kk * 2 + ((lane >> 3) & 1);
         uint32_t b0, b1, b2, b3;
-        ldsm_x4(kbase + swz<HD>(key, ch), b0, b1, b2, b3);
+        ldsm_x4(kbase + page_off<HD>(key, ch), b0, b1, b2, b3);
         mma_bf16_16816(s[0], qa[kk], b0, b1);
         mma_bf16_16816(s[1], qa[kk], b2, b3);
       }
@@ -233,24 +249,24 @@ __global__ void __launch_bounds__(256, 2)
       pa[1] = pack_bf16(s[0][2], s[0][3]);
       pa[2] = pack_bf16(s[1][0], s[1][1]);
       pa[3] = pack_bf16(s[1][2], s[1][3]);
-      const uint32_t vbase = kbase + 16 * HD * 2;
+      const uint32_t vbase = kbase + PB;
 #pragma unroll
       for (int dt = 0; dt < HD / 16; ++dt) {
         const int key = (lane & 7) + (((lane >> 3) & 1) << 3);
         const int ch = dt * 2 + (lane >> 4);
         uint32_t b0, b1, b2, b3;
-        ldsm_x4_t(vbase + swz<HD>(key, ch), b0, b1, b2, b3);
+        ldsm_x4_t(vbase + page_off<HD>(key, ch), b0, b1, b2, b3);
         mma_bf16_16816(o[dt * 2], pa, b0, b1);
         mma_bf16_16816(o[dt * 2 + 1], pa, b2, b3);
       }
     }
-    __syncthreads();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
   }
-  cp_async_wait<0>();
-  __syncthreads();
 
   // ---- combine the odd-page state into the even-page state (fixed order) ----
-  float* so = reinterpret_cast<float*>(sKV);        // [64 rows][HD] from the odd-page warps
+  named_bar_sync(1, 256);  // every consumer is done with the ring
+  float* so = reinterpret_cast<float*>(ring);  // [64 rows][HD] from the odd-page warps
   float2* sml = reinterpret_cast<float2*>(so + 64 * HD);
   if (kg == 1 && active) {
 #pragma unroll
@@ -265,7 +281,7 @@ __global__ void __launch_bounds__(256, 2)
       if ((lane & 3) == 0) sml[r] = half == 0 ? make_float2(m_lo, l_lo) : make_float2(m_hi, l_hi);
     }
   }
-  __syncthreads();
+  named_bar_sync(1, 256);
   if (kg == 1 || !active) return;
   const int chunk = it.chunk_idx;
 #pragma unroll
@@ -346,8 +362,8 @@ static cudaError_t attn_launch_hd(const AttnLaunch& a, cudaStream_t s) {
     attr = true;
   }
   dim3 grid(a.n_items_cap, a.num_kv_heads);
-  cudaError_t e = launch_pdl(attn_partial_kernel<HD>, grid, dim3(256), attn_smem<HD>(), s, a.q,
-                             a.q_ld, a.k_pages, a.v_pages, a.num_kv_heads, a.group, a.items,
+  cudaError_t e = launch_pdl(attn_partial_kernel<HD>, grid, dim3(ATTN_THREADS), attn_smem<HD>(), s,
+                             a.tm_k, a.tm_v, a.q, a.q_ld, a.num_kv_heads, a.group, a.items,
                              a.item_pages, a.item_rows, a.row_pos, a.num_heads, a.max_chunks,
                              a.scale, a.part_o, a.part_ml, a.n_items_dev, a.pf_base, a.pf_bytes);
   if (e != cudaSuccess) return e;

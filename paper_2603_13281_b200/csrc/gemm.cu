@@ -11,7 +11,10 @@ constexpr uint32_t W_BYTES = BM * BK * 2;
 constexpr int MAX_RANK = 32;
 // barriers, reduction scratch, staged row metadata and the LoRA U rows of the launch
 template <int NT>
-constexpr size_t aux_smem() { return 2048 + (size_t)NT * 5 * 4; }
+constexpr size_t aux_smem() {
+  // + SGMV segment table: slots + 1 offsets and up to 256 row ids
+  return 2048 + (size_t)NT * 5 * 4 + (64 + 1 + 512) * 4;
+}
 
 template <int NT>
 struct Cfg {
@@ -194,7 +197,7 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
 // that delivers a row's last slice folds the partials in slice order (deterministic).
 constexpr int SHRINK_SLICE = 2048;  // 8 x (32 lanes x 8 bf16)
 __device__ __forceinline__ void lora_shrink_tasks(const GemmParams& p, int gwarp, int nwarps,
-                                                  int lane) {
+                                                  int lane, const int* s_off, const int* s_rows) {
   const int per_t = p.slots * p.rank;
   const int splits = (p.sh_K + SHRINK_SLICE - 1) / SHRINK_SLICE;
   const int tasks = p.sh_targets * per_t * splits;
@@ -202,7 +205,7 @@ __device__ __forceinline__ void lora_shrink_tasks(const GemmParams& p, int gwarp
     const int ks = task % splits, combo = task / splits;
     const int t = combo / per_t, rem = combo % per_t;
     const int a = rem / p.rank, j = rem % p.rank;
-    const int r0 = p.seg_off[a], r1 = p.seg_off[a + 1];
+    const int r0 = s_off[a], r1 = s_off[a + 1];
     if (r0 == r1) continue;
     const int k0 = ks * SHRINK_SLICE;
     const __nv_bfloat16* A = (t == 0 ? p.sh_a0 : p.sh_a1) + ((size_t)a * p.rank + j) * p.sh_K;
@@ -213,7 +216,7 @@ __device__ __forceinline__ void lora_shrink_tasks(const GemmParams& p, int gwarp
       araw[i] = k < p.sh_K ? __ldg(reinterpret_cast<const uint4*>(A + k)) : make_uint4(0, 0, 0, 0);
     }
     for (int rr = r0; rr < r1; ++rr) {
-      const int gr = p.seg_rows[rr];
+      const int gr = s_rows[rr];
       if (gr < p.row0 || gr >= p.row0 + p.n_rows) continue;
       uint4 xraw[8];
 #pragma unroll
@@ -248,7 +251,7 @@ __device__ __forceinline__ void lora_shrink_tasks(const GemmParams& p, int gwarp
       if (atomicAdd(cnt, 1) == splits - 1) {
         __threadfence();
         for (int rr = r0; rr < r1; ++rr) {
-          const int gr = p.seg_rows[rr];
+          const int gr = s_rows[rr];
           if (gr < p.row0 || gr >= p.row0 + p.n_rows) continue;
           const size_t slot = ((size_t)gr * 2 + t) * p.rank + j;
           float s = 0.f;
@@ -323,6 +326,15 @@ __global__ void __launch_bounds__(256, 1)
     }
   };
   if (threadIdx.x == 0) stamp(0);
+  // pull the NEXT projection's adapter A matrices into L2 so its shrink loads hit L2
+  if (p.pfa_bytes > 0 && warp == 3) {
+    const long long units = p.pfa_bytes >> 14;
+    const long long b = (long long)blockIdx.x * units / gridDim.x;
+    const long long e = (long long)(blockIdx.x + 1) * units / gridDim.x;
+    for (long long u = b + lane_id(); u < e; u += 32) bulk_prefetch_l2(p.pfa + (u << 14), 16384);
+    if (p.pfa2 != nullptr)
+      for (long long u = b + lane_id(); u < e; u += 32) bulk_prefetch_l2(p.pfa2 + (u << 14), 16384);
+  }
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
@@ -339,11 +351,16 @@ __global__ void __launch_bounds__(256, 1)
       };
       auto tile_ls = [&](int t) {
         if (Lc == 0) return 0;
-        const long long t0 = (long long)t * sp.Ut;
-        const long long nxt = sp.ubegin(sp.owner(t0) + 1);
-        const long long e0 = (t0 + sp.Ut < nxt) ? t0 + sp.Ut : nxt;
-        const int portion = (int)(e0 - t0);
-        return portion >= Lc ? portion - Lc : 0;
+        const long long t0 = (long long)t * sp.Ut, t1 = t0 + sp.Ut;
+        // first CTA portion of the tile long enough to hold the LoRA chunks; a portion
+        // that ends before the tile does ends at that CTA's range end (late in its range)
+        for (int cc = sp.owner(t0); cc < sp.G; ++cc) {
+          const long long b = sp.ubegin(cc) > t0 ? sp.ubegin(cc) : t0;
+          const long long e = sp.ubegin(cc + 1) < t1 ? sp.ubegin(cc + 1) : t1;
+          if (e - b >= Lc) return (int)(e - Lc - t0);
+          if (e >= t1) break;
+        }
+        return sp.Ut - Lc;
       };
       auto chunk_of = [&](const Cursor& cu, int& ch) {
         if (cu.k < cu.ls || Lc == 0) { ch = cu.k; return false; }
@@ -457,7 +474,16 @@ __global__ void __launch_bounds__(256, 1)
     if (p.sh_x != nullptr) {
       pdl_wait();
       const int lane = lane_id();
-      lora_shrink_tasks(p, blockIdx.x * 2 + (warp - 2), gridDim.x * 2, lane);
+      // stage the SGMV segment table (adapter slot -> decoder rows) in smem once
+      int* s_off = rm.kind + 5 * NT;           // after the epilogue's row metadata
+      int* s_rows = s_off + (p.slots + 1);
+      const int t64 = threadIdx.x - 64;        // 0..63 across warps 2-3
+      for (int i = t64; i <= p.slots; i += 64) s_off[i] = p.seg_off[i];
+      named_bar_sync(2, 64);
+      const int nseg = s_off[p.slots];
+      for (int i = t64; i < nseg; i += 64) s_rows[i] = p.seg_rows[i];
+      named_bar_sync(2, 64);
+      lora_shrink_tasks(p, blockIdx.x * 2 + (warp - 2), gridDim.x * 2, lane, s_off, s_rows);
       __syncwarp();
       __threadfence();
       asm volatile("fence.proxy.async.global;\n" ::: "memory");  // U is read by TMA

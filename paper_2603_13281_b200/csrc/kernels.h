@@ -69,6 +69,7 @@ struct AttnLaunch {
   float* part_o;
   float2* part_ml;
   int* merge_cnt;  // unused (kept for ABI of the test entry)
+  CUtensorMap tm_k, tm_v;  // page-arena maps: dims {hd, 16, pages*H_kv}, box {64, 16, 1}, 128B swizzle
   const uint8_t* pf_base;  // L2 prefetch of the next projection's weights (null = none)
   long long pf_bytes;
   __nv_bfloat16* out;

@@ -100,6 +100,25 @@ static icr_status make_map_blocked(CUtensorMap* m, const void* ptr, uint64_t row
   return ICR_OK;
 }
 
+// KV page arena of one layer [planes = pages*H_kv][16][hd] bf16: box {64, 16, 1} = one
+// 128-byte-swizzled half page of one KV head (attention TMA ring).
+static icr_status make_page_map(CUtensorMap* m, const void* ptr, uint64_t planes, uint64_t hd) {
+  icr_status st = get_encode();
+  if (st) return st;
+  cuuint64_t dims[3] = {hd, 16, planes};
+  cuuint64_t strides[2] = {hd * 2, 16 * hd * 2};
+  cuuint32_t box[3] = {64, 16, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(ICR_CUDA, "cuTensorMapEncodeTiled (pages) failed (%d) planes=%llu", (int)r,
+                (unsigned long long)planes);
+  return ICR_OK;
+}
+
 static int nt_index(int nt) {
   switch (nt) {
     case 16: return 0;
@@ -219,6 +238,7 @@ struct Meta {
 struct LayerMaps {
   CUtensorMap qkv, o, gu, down;          // base weights (tile-major)
   CUtensorMap lb_q, lb_o, lb_gu, lb_down;  // LoRA B_cat (tile-major), when lora_rank > 0
+  CUtensorMap kpg, vpg;                    // this layer's K / V page arenas (attention TMA)
 };
 
 struct GraphKey {
@@ -439,6 +459,7 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
   // without an adapter), so stream-K split points -- and with them every encoder row's
   // bits -- never depend on which rows the batch holds.
   const bool lora = c.lora_rank > 0;
+  const bool pf_a_on = !getenv("ICR_NO_PREFETCH");
   const int d = c.hidden_dim, rp = mt.rp;
   long long launches = 0;
 
@@ -507,6 +528,9 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
   al.out_ld = m->q_dim;
 
   icr_status st;
+  auto a_bytes = [&](int K) -> long long {
+    return pf_a_on ? (long long)c.adapter_slots * c.lora_rank * K * 2 : 0;
+  };
   const int qkv_M = m->q_dim + 2 * m->kv_dim;
   const bool pf_on = rp <= 256 && !getenv("ICR_NO_PREFETCH");
   CUDA_TRY(embed_launch(tokens, kind, m->embed, m->x, m->xb, m->ssq, rp, rp, d,
@@ -528,6 +552,8 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
         p.sh_x = m->xb; p.sh_ld = d; p.sh_K = d; p.sh_targets = 1;
         p.sh_a0 = (const __nv_bfloat16*)w.a_q;
         p.sync = m->sync + 0;
+        p.pfa = (const uint8_t*)w.a_o;  // next shrink: o
+        p.pfa_bytes = a_bytes(m->q_dim);
       }
       p.out_bf16 = m->qb;
       p.q_dim = m->q_dim;
@@ -544,6 +570,8 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
     }
     al.k_pages = (const __nv_bfloat16*)w.k_pages;
     al.v_pages = (const __nv_bfloat16*)w.v_pages;
+    al.tm_k = lm.kpg;
+    al.tm_v = lm.vpg;
     al.pf_base = pf_on ? (const uint8_t*)w.w_o : nullptr;
     al.pf_bytes = (long long)d * m->q_dim * 2;
     {  // attention over 2H heads (src/model.py:497-501)
@@ -562,6 +590,9 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
         p.sh_x = m->att; p.sh_ld = m->q_dim; p.sh_K = m->q_dim; p.sh_targets = 1;
         p.sh_a0 = (const __nv_bfloat16*)w.a_o;
         p.sync = m->sync + 2;
+        p.pfa = (const uint8_t*)w.a_gate;  // next shrink: gate | up
+        p.pfa2 = (const uint8_t*)w.a_up;
+        p.pfa_bytes = a_bytes(d);
       }
       p.resid = m->x;
       p.resid_bf16 = m->xb;
@@ -581,6 +612,8 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
         p.sh_x = m->xb; p.sh_ld = d; p.sh_K = d; p.sh_targets = 2;
         p.sh_a0 = (const __nv_bfloat16*)w.a_gate; p.sh_a1 = (const __nv_bfloat16*)w.a_up;
         p.sync = m->sync + 4;
+        p.pfa = (const uint8_t*)w.a_down;  // next shrink: down
+        p.pfa_bytes = a_bytes(c.ffn_dim);
       }
       p.out_bf16 = m->f;
       set_prefetch(m, p, w.w_down, d, c.ffn_dim, rp);
@@ -597,6 +630,10 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
         p.sh_x = m->f; p.sh_ld = c.ffn_dim; p.sh_K = c.ffn_dim; p.sh_targets = 1;
         p.sh_a0 = (const __nv_bfloat16*)w.a_down;
         p.sync = m->sync + 6;
+        if (l + 1 < c.num_layers) {  // next shrink: the next layer's q
+          p.pfa = (const uint8_t*)m->layers[l + 1].a_q;
+          p.pfa_bytes = a_bytes(d);
+        }
       }
       p.resid = m->x;
       p.resid_bf16 = m->xb;
@@ -806,6 +843,8 @@ icr_status icr_model_create(const icr_model_config* cfg, const icr_layer_weights
     if ((st = make_map_blocked(&m->maps[l].o, w.w_o, c.hidden_dim, q_dim))) return bail(st);
     if ((st = make_map_blocked(&m->maps[l].gu, w.w_gu, 2 * c.ffn_dim, c.hidden_dim))) return bail(st);
     if ((st = make_map_blocked(&m->maps[l].down, w.w_down, c.hidden_dim, c.ffn_dim))) return bail(st);
+    if ((st = make_page_map(&m->maps[l].kpg, w.k_pages, (uint64_t)c.num_pages * c.num_kv_heads, c.head_dim))) return bail(st);
+    if ((st = make_page_map(&m->maps[l].vpg, w.v_pages, (uint64_t)c.num_pages * c.num_kv_heads, c.head_dim))) return bail(st);
     if (c.lora_rank > 0) {
       if ((st = make_map_blocked(&m->maps[l].lb_q, w.b_q, q_dim + 2 * kv_dim, m->lc1 * 64))) return bail(st);
       if ((st = make_map_blocked(&m->maps[l].lb_o, w.b_o, c.hidden_dim, m->lc1 * 64))) return bail(st);
@@ -1175,6 +1214,103 @@ icr_status icr_bench_gemm(const void* w, const void* x, int M, int K, int rows, 
   return ICR_OK;
 }
 
+// Attention micro-benchmark (C4 sweep): plans once, then launches partial + merge `iters`
+// times (L2 flushed between launches by the caller-provided flush buffer when non-null);
+// returns the average device ms per launch pair and the number of work items.
+icr_status icr_bench_attention(const void* q_dev, const void* k_pages, const void* v_pages,
+                               int num_heads, int num_kv_heads, int head_dim, int chunk_pages,
+                               int n_rows, const int32_t* row_seq_host, const int32_t* row_pos_host,
+                               const int32_t* block_table_host, int n_seqs, int max_pages_per_seq,
+                               void* out_dev, void* flush_dev, long long flush_bytes, int iters,
+                               float* avg_ms, int32_t* n_items_out, void* stream) {
+  if (head_dim != 64 && head_dim != 128) return fail(ICR_CONFIG, "head_dim must be 64 or 128");
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<int> kind(n_rows, 0);
+  AttnPlan plan;
+  icr_status st = build_attn_plan(n_rows, kind.data(), row_seq_host, row_pos_host, block_table_host,
+                                  n_seqs, max_pages_per_seq, 1 << 30, num_heads / num_kv_heads,
+                                  chunk_pages, plan);
+  if (st) return st;
+  if (n_items_out) *n_items_out = (int)plan.items.size();
+  int maxpos = 0;
+  for (int r = 0; r < n_rows; ++r) maxpos = std::max(maxpos, row_pos_host[r]);
+  const int max_chunks = maxpos / (chunk_pages * 16) + 1;
+  int *d_pos, *d_kind, *d_pages, *d_n;
+  AttnItem* d_items;
+  int2* d_rows;
+  float* d_po;
+  float2* d_pml;
+  CUDA_TRY(cudaMalloc(&d_pos, n_rows * sizeof(int)));
+  CUDA_TRY(cudaMalloc(&d_kind, n_rows * sizeof(int)));
+  CUDA_TRY(cudaMalloc(&d_pages, std::max<size_t>(plan.pages.size(), 1) * sizeof(int)));
+  CUDA_TRY(cudaMalloc(&d_n, sizeof(int)));
+  CUDA_TRY(cudaMalloc(&d_items, std::max<size_t>(plan.items.size(), 1) * sizeof(AttnItem)));
+  CUDA_TRY(cudaMalloc(&d_rows, std::max<size_t>(plan.rows.size(), 1) * sizeof(int2)));
+  CUDA_TRY(cudaMalloc(&d_po, (size_t)n_rows * num_heads * max_chunks * head_dim * sizeof(float)));
+  CUDA_TRY(cudaMalloc(&d_pml, (size_t)n_rows * num_heads * max_chunks * sizeof(float2)));
+  int nitems = (int)plan.items.size();
+  CUDA_TRY(cudaMemcpy(d_pos, row_pos_host, n_rows * sizeof(int), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(d_kind, kind.data(), n_rows * sizeof(int), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(d_pages, plan.pages.data(), plan.pages.size() * sizeof(int), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(d_items, plan.items.data(), plan.items.size() * sizeof(AttnItem), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(d_rows, plan.rows.data(), plan.rows.size() * sizeof(int2), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(d_n, &nitems, sizeof(int), cudaMemcpyHostToDevice));
+  AttnLaunch a{};
+  a.q = (const __nv_bfloat16*)q_dev;
+  a.q_ld = num_heads * head_dim;
+  a.k_pages = (const __nv_bfloat16*)k_pages;
+  a.v_pages = (const __nv_bfloat16*)v_pages;
+  a.num_kv_heads = num_kv_heads;
+  a.num_heads = num_heads;
+  a.group = num_heads / num_kv_heads;
+  a.head_dim = head_dim;
+  a.items = d_items;
+  a.item_pages = d_pages;
+  a.item_rows = d_rows;
+  a.n_items_dev = d_n;
+  a.n_items_cap = nitems;
+  a.row_pos = d_pos;
+  a.row_kind = d_kind;
+  a.n_rows = n_rows;
+  a.max_chunks = max_chunks;
+  a.chunk_tokens = chunk_pages * 16;
+  a.scale = (float)(1.0 / std::sqrt((double)head_dim));
+  a.part_o = d_po;
+  a.part_ml = d_pml;
+  a.out = (__nv_bfloat16*)out_dev;
+  a.out_ld = num_heads * head_dim;
+  {
+    int maxpage = 0;
+    for (size_t i = 0; i < plan.pages.size(); ++i) maxpage = std::max(maxpage, plan.pages[i]);
+    const uint64_t planes = (uint64_t)(maxpage + 1) * num_kv_heads;
+    if ((st = make_page_map(&a.tm_k, k_pages, planes, head_dim))) return st;
+    if ((st = make_page_map(&a.tm_v, v_pages, planes, head_dim))) return st;
+  }
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  float total = 0.f;
+  cudaError_t e = attn_launch(a, s);  // warm-up
+  for (int it = 0; it < iters && e == cudaSuccess; ++it) {
+    if (flush_dev) cudaMemsetAsync(flush_dev, it & 0xff, (size_t)flush_bytes, s);
+    cudaEventRecord(e0, s);
+    e = attn_launch(a, s);
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    total += ms;
+  }
+  *avg_ms = total / iters;
+  cudaStreamSynchronize(s);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  void* bufs[] = {d_pos, d_kind, d_pages, d_n, d_items, d_rows, d_po, d_pml};
+  for (void* p : bufs) cudaFree(p);
+  if (e != cudaSuccess) return fail(ICR_CUDA, "attention bench: %s", cudaGetErrorString(e));
+  return ICR_OK;
+}
+
 // ---- building blocks for parity tests ----
 static float* g_ws = nullptr;
 static int* g_counters = nullptr;
@@ -1284,6 +1420,13 @@ icr_status icr_paged_attention(const void* q_dev, const void* k_pages, const voi
   a.part_o = d_po;
   a.part_ml = d_pml;
   a.merge_cnt = d_cnt;
+  {
+    int maxpage = 0;
+    for (size_t i = 0; i < plan.pages.size(); ++i) maxpage = std::max(maxpage, plan.pages[i]);
+    const uint64_t planes = (uint64_t)(maxpage + 1) * num_kv_heads;
+    if ((st = make_page_map(&a.tm_k, k_pages, planes, head_dim))) return st;
+    if ((st = make_page_map(&a.tm_v, v_pages, planes, head_dim))) return st;
+  }
   a.out = (__nv_bfloat16*)out_dev;
   a.out_ld = num_heads * head_dim;
   cudaError_t e = attn_launch(a, s);
