@@ -158,7 +158,7 @@ icr_status icr_bench_gemm(const void* w, const void* x, int M, int K, int rows, 
                           float* avg_ms, void* stream);
 
 /* Paged-attention micro-benchmark (C4 sweep): plan once, time `iters` launches of the
- * partial + merge kernels (memset of flush_dev between launches evicts L2 when non-NULL). */
+ * partial + merge kernels (a read of flush_dev between launches evicts L2 when non-NULL). */
 icr_status icr_bench_attention(const void* q_dev, const void* k_pages, const void* v_pages,
                                int num_heads, int num_kv_heads, int head_dim, int chunk_pages,
                                int n_rows, const int32_t* row_seq_host, const int32_t* row_pos_host,

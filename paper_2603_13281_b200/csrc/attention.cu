@@ -8,7 +8,8 @@
 //     prefix) are grouped into one work item, so each shared page is staged into shared
 //     memory once and reused by the encoder and every adapter's decoder queries;
 //   * a work item x one KV head = one CTA; up to 64 query rows (4 warps x 16).
-// Per (row, head, chunk) the kernel emits an unnormalised partial (o, m, l); the merge
+// Per (row, head, chunk) the kernel emits an unnormalised partial (o, m, l) -- m in the log2
+// domain (scores scaled by log2 e, exp2 throughout); the merge
 // kernel folds chunks 0..last in fixed order. Partials depend only on the row's own query, the chunk's keys and the row's position, never on which other rows share the
 // CTA -- the batch-invariance the reference gets from its per-head loop (2H == H||H,
 // tests/test_model.py:225-239) and that makes prefill / decode KV bytes identical.
@@ -175,38 +176,50 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
   float o[HD / 8][4];
 #pragma unroll
   for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  // running max in the log2 domain (scores pre-multiplied by scale * log2(e))
   float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;
+  const float sl2 = scale * 1.4426950408889634f;
 
-  for (int pi = kg; pi < it.n_pages; pi += 2) {
-    const int st = pi % PAGE_STAGES;
-    mbar_wait(&full[st], (pi / PAGE_STAGES) & 1);
+  // Key groups of 4 pages (64 keys): group kb belongs to page parity kg = kb & 1.
+  for (int kb = kg; kb * 4 < it.n_pages; kb += 2) {
+    const int p0 = kb * 4;
+    const int np = min(4, it.n_pages - p0);
+    for (int j = 0; j < np; ++j) mbar_wait(&full[(p0 + j) % PAGE_STAGES], ((p0 + j) / PAGE_STAGES) & 1);
     if (active) {
-      // S = Q K^T for 16 keys (two n8 tiles)
-      float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-      const uint32_t kbase = smem_u32(ring + (size_t)st * 2 * PB);
+      // S = Q K^T for up to 64 keys: 8 n8 tiles, independent accumulation chains
+      float s[8][4];
 #pragma unroll
-      for (int kk = 0; kk < HD / 16; ++kk) {
-        const int key = (lane & 7) + ((lane >> 4) << 3);
-        const int ch = kk * 2 + ((lane >> 3) & 1);
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4(kbase + page_off<HD>(key, ch), b0, b1, b2, b3);
-        mma_bf16_16816(s[0], qa[kk], b0, b1);
-        mma_bf16_16816(s[1], qa[kk], b2, b3);
+      for (int t = 0; t < 8; ++t) s[t][0] = s[t][1] = s[t][2] = s[t][3] = 0.f;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (j < np) {
+          const uint32_t kbase = smem_u32(ring + (size_t)((p0 + j) % PAGE_STAGES) * 2 * PB);
+#pragma unroll
+          for (int kk = 0; kk < HD / 16; ++kk) {
+            const int key = (lane & 7) + ((lane >> 4) << 3);
+            const int ch = kk * 2 + ((lane >> 3) & 1);
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4(kbase + page_off<HD>(key, ch), b0, b1, b2, b3);
+            mma_bf16_16816(s[2 * j], qa[kk], b0, b1);
+            mma_bf16_16816(s[2 * j + 1], qa[kk], b2, b3);
+          }
+        }
       }
-      // scale, mask, online softmax (src/model.py:415-423, src/tensor.py:249-267)
-      const int kpos0 = it.chunk_start + pi * 16;
+      // scale into the log2 domain, mask (src/model.py:415-423), block row max
+      const int kpos0 = it.chunk_start + p0 * 16;
       float mx_lo = m_lo, mx_hi = m_hi;
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
+      for (int t = 0; t < 8; ++t) {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int kp = kpos0 + nt * 8 + (lane & 3) * 2 + e;
-          float a = __fmul_rn(s[nt][e], scale);
-          float b = __fmul_rn(s[nt][2 + e], scale);
-          a = (kp <= pos_lo) ? a : -INFINITY;
-          b = (kp <= pos_hi) ? b : -INFINITY;
-          s[nt][e] = a;
-          s[nt][2 + e] = b;
+          const int kp = kpos0 + t * 8 + (lane & 3) * 2 + e;
+          const bool inb = t < 2 * np;
+          float a = __fmul_rn(s[t][e], sl2);
+          float b = __fmul_rn(s[t][2 + e], sl2);
+          a = (inb && kp <= pos_lo) ? a : -INFINITY;
+          b = (inb && kp <= pos_hi) ? b : -INFINITY;
+          s[t][e] = a;
+          s[t][2 + e] = b;
           mx_lo = fmaxf(mx_lo, a);
           mx_hi = fmaxf(mx_hi, b);
         }
@@ -215,20 +228,28 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
       mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, 2));
       mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 1));
       mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 2));
-      const float corr_lo = (mx_lo == -INFINITY) ? 1.f : expf(m_lo - mx_lo);
-      const float corr_hi = (mx_hi == -INFINITY) ? 1.f : expf(m_hi - mx_hi);
+      const float corr_lo = (mx_lo == -INFINITY) ? 1.f : exp2f(m_lo - mx_lo);
+      const float corr_hi = (mx_hi == -INFINITY) ? 1.f : exp2f(m_hi - mx_hi);
       float sum_lo = 0.f, sum_hi = 0.f;
+      uint32_t pa[4][4];  // P as bf16 A-fragments, one per 16-key page
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
+      for (int t = 0; t < 8; ++t) {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const float a = (s[nt][e] == -INFINITY) ? 0.f : expf(s[nt][e] - mx_lo);
-          const float b = (s[nt][2 + e] == -INFINITY) ? 0.f : expf(s[nt][2 + e] - mx_hi);
-          s[nt][e] = a;
-          s[nt][2 + e] = b;
+          const float a = (s[t][e] == -INFINITY) ? 0.f : exp2f(s[t][e] - mx_lo);
+          const float b = (s[t][2 + e] == -INFINITY) ? 0.f : exp2f(s[t][2 + e] - mx_hi);
+          s[t][e] = a;
+          s[t][2 + e] = b;
           sum_lo += a;
           sum_hi += b;
         }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        pa[j][0] = pack_bf16(s[2 * j][0], s[2 * j][1]);
+        pa[j][1] = pack_bf16(s[2 * j][2], s[2 * j][3]);
+        pa[j][2] = pack_bf16(s[2 * j + 1][0], s[2 * j + 1][1]);
+        pa[j][3] = pack_bf16(s[2 * j + 1][2], s[2 * j + 1][3]);
       }
       sum_lo += __shfl_xor_sync(0xffffffffu, sum_lo, 1);
       sum_lo += __shfl_xor_sync(0xffffffffu, sum_lo, 2);
@@ -238,30 +259,34 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
       l_hi = l_hi * corr_hi + sum_hi;
       m_lo = mx_lo;
       m_hi = mx_hi;
+      // rescale O only when some row's running max moved (rare on long contexts)
+      if (__any_sync(0xffffffffu, corr_lo != 1.f || corr_hi != 1.f)) {
 #pragma unroll
-      for (int i = 0; i < HD / 8; ++i) {
-        o[i][0] *= corr_lo; o[i][1] *= corr_lo;
-        o[i][2] *= corr_hi; o[i][3] *= corr_hi;
+        for (int i = 0; i < HD / 8; ++i) {
+          o[i][0] *= corr_lo; o[i][1] *= corr_lo;
+          o[i][2] *= corr_hi; o[i][3] *= corr_hi;
+        }
       }
-      // O += P V
-      uint32_t pa[4];
-      pa[0] = pack_bf16(s[0][0], s[0][1]);
-      pa[1] = pack_bf16(s[0][2], s[0][3]);
-      pa[2] = pack_bf16(s[1][0], s[1][1]);
-      pa[3] = pack_bf16(s[1][2], s[1][3]);
-      const uint32_t vbase = kbase + PB;
+      // O += P V, page by page
 #pragma unroll
-      for (int dt = 0; dt < HD / 16; ++dt) {
-        const int key = (lane & 7) + (((lane >> 3) & 1) << 3);
-        const int ch = dt * 2 + (lane >> 4);
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4_t(vbase + page_off<HD>(key, ch), b0, b1, b2, b3);
-        mma_bf16_16816(o[dt * 2], pa, b0, b1);
-        mma_bf16_16816(o[dt * 2 + 1], pa, b2, b3);
+      for (int j = 0; j < 4; ++j) {
+        if (j < np) {
+          const uint32_t vbase = smem_u32(ring + (size_t)((p0 + j) % PAGE_STAGES) * 2 * PB) + PB;
+#pragma unroll
+          for (int dt = 0; dt < HD / 16; ++dt) {
+            const int key = (lane & 7) + (((lane >> 3) & 1) << 3);
+            const int ch = dt * 2 + (lane >> 4);
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4_t(vbase + page_off<HD>(key, ch), b0, b1, b2, b3);
+            mma_bf16_16816(o[dt * 2], pa[j], b0, b1);
+            mma_bf16_16816(o[dt * 2 + 1], pa[j], b2, b3);
+          }
+        }
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
+    if (lane == 0)
+      for (int j = 0; j < np; ++j) mbar_arrive(&empty[(p0 + j) % PAGE_STAGES]);
   }
 
   // ---- combine the odd-page state into the even-page state (fixed order) ----
@@ -291,8 +316,8 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
     const float m0 = half == 0 ? m_lo : m_hi, l0 = half == 0 ? l_lo : l_hi;
     const float2 ml1 = sml[r];
     const float M = fmaxf(m0, ml1.x);
-    const float w0 = (m0 == -INFINITY) ? 0.f : expf(m0 - M);
-    const float w1 = (ml1.x == -INFINITY) ? 0.f : expf(ml1.x - M);
+    const float w0 = (m0 == -INFINITY) ? 0.f : exp2f(m0 - M);
+    const float w1 = (ml1.x == -INFINITY) ? 0.f : exp2f(ml1.x - M);
     const int2 rr = item_rows[it.row_off + r];
     const int head = g * group + rr.y;
     const size_t slot = ((size_t)rr.x * num_heads + head) * max_chunks + chunk;
@@ -334,7 +359,7 @@ __global__ void __launch_bounds__(512)
     float L = 0.f;
     for (int c = 0; c < nch; ++c) {
       const float2 ml = part_ml[base + c];
-      const float w = expf(ml.x - M);
+      const float w = exp2f(ml.x - M);  // partial maxima are in the log2 domain
       wts[tid * max_chunks + c] = w;
       L = fmaf(ml.y, w, L);
     }

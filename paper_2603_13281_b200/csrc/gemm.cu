@@ -389,8 +389,8 @@ __global__ void __launch_bounds__(256, 1)
         const bool lo = chunk_of(cu, ch);
         uint8_t* dst = smem + (size_t)stage * C::STAGE + W_BYTES;
         if (lo) {
-          if (!lora_ready) {  // U is produced by this grid's shrink warps
-            const int target = gridDim.x * 2;
+          if (!lora_ready) {  // U is produced by this grid's shrink warps (6 per CTA)
+            const int target = gridDim.x * 6;
             stamp(2);
             while (ld_acquire(p.sync) < target) __nanosleep(32);
             stamp(3);
@@ -479,11 +479,11 @@ __global__ void __launch_bounds__(256, 1)
       int* s_rows = s_off + (p.slots + 1);
       const int t64 = threadIdx.x - 64;        // 0..63 across warps 2-3
       for (int i = t64; i <= p.slots; i += 64) s_off[i] = p.seg_off[i];
-      named_bar_sync(2, 64);
+      named_bar_sync(3, 64);
       const int nseg = s_off[p.slots];
       for (int i = t64; i < nseg; i += 64) s_rows[i] = p.seg_rows[i];
-      named_bar_sync(2, 64);
-      lora_shrink_tasks(p, blockIdx.x * 2 + (warp - 2), gridDim.x * 2, lane, s_off, s_rows);
+      named_bar_sync(2, 192);  // publish the table to the epilogue warps as well
+      lora_shrink_tasks(p, blockIdx.x * 2 + (warp - 2), gridDim.x * 6, lane, s_off, s_rows);
       __syncwarp();
       __threadfence();
       asm volatile("fence.proxy.async.global;\n" ::: "memory");  // U is read by TMA
@@ -521,6 +521,20 @@ __global__ void __launch_bounds__(256, 1)
       rm.inv[n] = inv;
     }
     named_bar_sync(1, 128);
+    if (p.sh_x != nullptr) {
+      // the epilogue warps are idle until the first tile drains: help with the shrink so U
+      // is ready long before any LoRA chunk is streamed (latency under full HBM load)
+      const int lane = ep_t & 31;
+      const int* s_off = rm.kind + 5 * NT;
+      const int* s_rows = s_off + (p.slots + 1);
+      named_bar_sync(2, 192);
+      lora_shrink_tasks(p, gridDim.x * 2 + blockIdx.x * 4 + (warp - 4), gridDim.x * 6, lane, s_off,
+                        s_rows);
+      __syncwarp();
+      __threadfence();
+      asm volatile("fence.proxy.async.global;\n" ::: "memory");
+      if (lane == 0) atomicAdd(p.sync, 1);
+    }
     uint32_t tphase = 0;
     for (int t = t_first; t <= t_last; ++t) {
       const long long t0 = (long long)t * sp.Ut;

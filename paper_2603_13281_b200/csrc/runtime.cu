@@ -1214,6 +1214,17 @@ icr_status icr_bench_gemm(const void* w, const void* x, int M, int K, int rows, 
   return ICR_OK;
 }
 
+// Reads a buffer larger than L2 (clean eviction: a memset would leave dirty lines whose
+// write-back the next timed kernel would pay).
+__global__ void l2_flush_read_kernel(const uint4* __restrict__ p, size_t n, unsigned* sink) {
+  unsigned acc = 0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const uint4 v = __ldcs(p + i);
+    acc ^= v.x ^ v.w;
+  }
+  if (acc == 0x12345678u) *sink = acc;
+}
+
 // Attention micro-benchmark (C4 sweep): plans once, then launches partial + merge `iters`
 // times (L2 flushed between launches by the caller-provided flush buffer when non-null);
 // returns the average device ms per launch pair and the number of work items.
@@ -1292,7 +1303,9 @@ icr_status icr_bench_attention(const void* q_dev, const void* k_pages, const voi
   float total = 0.f;
   cudaError_t e = attn_launch(a, s);  // warm-up
   for (int it = 0; it < iters && e == cudaSuccess; ++it) {
-    if (flush_dev) cudaMemsetAsync(flush_dev, it & 0xff, (size_t)flush_bytes, s);
+    if (flush_dev)
+      l2_flush_read_kernel<<<1184, 256, 0, s>>>((const uint4*)flush_dev, (size_t)flush_bytes / 16,
+                                                (unsigned*)flush_dev);
     cudaEventRecord(e0, s);
     e = attn_launch(a, s);
     cudaEventRecord(e1, s);
