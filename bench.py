@@ -227,14 +227,12 @@ def run_b200(args) -> None:
     _lib.check(rt._lib.icr_model_stats(rt._handle, stats.ctypes.data_as(
         __import__("ctypes").POINTER(__import__("ctypes").c_int64))))
     launches_per_step = int(stats[0]) + 1  # + the on-device token feedback kernel
-    t_max = torch.tensor([elapsed_ms], device="cuda")
-    if world > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    elapsed_ms = float(t_max.item())
+    from paper_2603_13281_b200 import dist as D
+    elapsed_ms = D.max_over_ranks(elapsed_ms, device="cuda")
     for s in sessions:
         s.cache.advance(W + K)
     value = world * N_ADAPTERS * K / (elapsed_ms / 1e3)
-    p95 = float(np.sort(step_ms)[max(0, int(np.ceil(0.95 * K)) - 1)])
+    p95 = D.global_p95([float(x) for x in step_ms])
 
     # ---------------- end to end through the public API (e2e) ----------------
     toks = [int(t) for t in last[fb[0::2]]]
@@ -249,10 +247,7 @@ def run_b200(args) -> None:
     _lib.check(rt._lib.icr_model_stats(rt._handle, stats.ctypes.data_as(
         __import__("ctypes").POINTER(__import__("ctypes").c_int64))))
     h2d = int(stats[1])
-    t_e2e = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t_e2e, op=dist.ReduceOp.MAX)
-    e2e_value = world * N_ADAPTERS * E2E / float(t_e2e.item())
+    e2e_value = world * N_ADAPTERS * E2E / D.max_over_ranks(e2e_s, device="cuda")
 
     # ---------------- roofline of the dominant kernel (gate|up GEMM) ----------------
     import ctypes as C
