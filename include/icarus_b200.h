@@ -149,6 +149,11 @@ icr_status icr_profile_step(icr_model* m, float* kind_ms, void* stream);
 /* Average device time of one projection-GEMM launch (which: 0 wo, 1 gate|up, 2 down,
  * 3 lm_head) re-run `iters` times over all layers with the last forward's rows. */
 icr_status icr_profile_gemm(icr_model* m, int which, int iters, float* avg_ms, void* stream);
+/* Diagnostic: average ms of the last forward replayed as a graph with kernel kinds
+ * (bit k = kind k of icr_profile_step) left out. */
+icr_status icr_profile_ablate(icr_model* m, int skip_mask, int iters, float* avg_ms, void* stream);
+/* Diagnostic: per-CTA timestamps of every GEMM launch of the last forward -> CSV. */
+icr_status icr_profile_trace(icr_model* m, const char* path, void* stream);
 
 /* Weight-streaming GEMM micro-benchmark (tuning): cycles n_mats matrices [n_mats][M][K]
  * (tile-major if blocked) against `rows` token rows; stages / ctas_per_sm / skip_mma

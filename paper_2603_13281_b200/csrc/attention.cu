@@ -95,10 +95,18 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
                         const int* __restrict__ row_pos, int num_heads, int max_chunks, float scale,
                         float* __restrict__ part_o, float2* __restrict__ part_ml,
                         const int* __restrict__ n_items_dev, const uint8_t* __restrict__ pf_base,
-                        long long pf_bytes) {
+                        long long pf_bytes, unsigned long long* __restrict__ trace) {
   constexpr int CH = HD / 8;  // 16-byte chunks per row
   constexpr uint32_t PB = page_bytes<HD>();
   extern __shared__ uint8_t attn_smem_raw[];
+  const int cta_id = blockIdx.y * gridDim.x + blockIdx.x;
+  if (trace != nullptr && threadIdx.x == 0 && cta_id < 4096)
+    trace[(size_t)cta_id * 16 + 6] = globaltimer();
+  if (trace != nullptr && threadIdx.x == 0 && cta_id < 4096) {
+    unsigned int smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    trace[(size_t)cta_id * 16 + 8] = smid + 1;
+  }
   uint8_t* base = attn_smem_raw + ((1024 - (smem_u32(attn_smem_raw) & 1023)) & 1023);
   uint8_t* ring = base;                                   // [stage][K | V] pages
   __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(ring + PAGE_STAGES * 2 * PB);
@@ -117,6 +125,8 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
   }
   __syncthreads();
   pdl_wait();
+  if (trace != nullptr && threadIdx.x == 0 && cta_id < 4096)
+    trace[(size_t)cta_id * 16 + 7] = globaltimer();
   const AttnItem it = items[item_id];
   const int g = blockIdx.y;
 
@@ -307,6 +317,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
     }
   }
   named_bar_sync(1, 256);
+  if (trace != nullptr && tid == 32 && cta_id < 4096) trace[(size_t)cta_id * 16 + 5] = globaltimer();
   if (kg == 1 || !active) return;
   const int chunk = it.chunk_idx;
 #pragma unroll
@@ -342,10 +353,14 @@ __global__ void __launch_bounds__(512)
     attn_merge_kernel(const float* __restrict__ part_o, const float2* __restrict__ part_ml,
                       const int* __restrict__ row_pos, const int* __restrict__ row_kind,
                       int num_heads, int group, int max_chunks, int chunk_tokens,
-                      __nv_bfloat16* __restrict__ out, int out_ld) {
+                      __nv_bfloat16* __restrict__ out, int out_ld,
+                      unsigned long long* __restrict__ trace) {
   extern __shared__ float merge_smem[];  // [group][max_chunks] weights + [group] L
+  const int cta_id = blockIdx.y * gridDim.x + blockIdx.x;
+  if (trace != nullptr && threadIdx.x == 0 && cta_id < 4096) trace[(size_t)cta_id * 16 + 6] = globaltimer();
   pdl_launch();
   pdl_wait();
+  if (trace != nullptr && threadIdx.x == 0 && cta_id < 4096) trace[(size_t)cta_id * 16 + 7] = globaltimer();
   const int r = blockIdx.x, g = blockIdx.y;
   if (row_kind[r] < 0) return;
   const int nch = row_pos[r] / chunk_tokens + 1;
@@ -374,6 +389,7 @@ __global__ void __launch_bounds__(512)
     for (int c = 0; c < nch; ++c) O = fmaf(part_o[(base + c) * HD + d], wts[hg * max_chunks + c], O);
     out[(size_t)r * out_ld + head * HD + d] = __float2bfloat16_rn(__fdiv_rn(O, Ls[hg]));
   }
+  if (trace != nullptr && threadIdx.x == 0 && cta_id < 4096) trace[(size_t)cta_id * 16 + 5] = globaltimer();
 }
 
 template <int HD>
@@ -390,13 +406,14 @@ static cudaError_t attn_launch_hd(const AttnLaunch& a, cudaStream_t s) {
   cudaError_t e = launch_pdl(attn_partial_kernel<HD>, grid, dim3(ATTN_THREADS), attn_smem<HD>(), s,
                              a.tm_k, a.tm_v, a.q, a.q_ld, a.num_kv_heads, a.group, a.items,
                              a.item_pages, a.item_rows, a.row_pos, a.num_heads, a.max_chunks,
-                             a.scale, a.part_o, a.part_ml, a.n_items_dev, a.pf_base, a.pf_bytes);
+                             a.scale, a.part_o, a.part_ml, a.n_items_dev, a.pf_base, a.pf_bytes, a.trace);
   if (e != cudaSuccess) return e;
   const int mthreads = std::min(512, ((a.group * HD + 31) / 32) * 32);
   const size_t msmem = (size_t)a.group * (a.max_chunks + 1) * sizeof(float);
   return launch_pdl(attn_merge_kernel<HD>, dim3(a.n_rows, a.num_kv_heads), dim3(mthreads), msmem, s,
                     a.part_o, a.part_ml, a.row_pos, a.row_kind, a.num_heads, a.group,
-                    a.max_chunks, a.chunk_tokens, a.out, a.out_ld);
+                    a.max_chunks, a.chunk_tokens, a.out, a.out_ld,
+                    a.trace ? a.trace + 4096 * 16 : nullptr);
 }
 
 cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t s) {

@@ -27,13 +27,106 @@ struct Cfg {
   static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE + aux_smem<NT>();
 };
 
+// Stream-K partition of U units over G CTAs. 32-bit arithmetic (the host guarantees
+// U * (G + 1) < 2^32): 64-bit division is a ~100-instruction software sequence, and the
+// epilogue's critical path evaluates these per tile and per reduced segment.
 struct Split {
   long long U;
   int Ut, G;
-  __device__ __host__ long long ubegin(int c) const { return (long long)c * U / G; }
+  __device__ __host__ long long ubegin(int c) const {
+    return (long long)(((unsigned)c * (unsigned)U) / (unsigned)G);
+  }
   // largest CTA whose range contains unit x
-  __device__ __host__ int owner(long long x) const { return (int)(((x + 1) * G - 1) / U); }
+  __device__ __host__ int owner(long long x) const {
+    return (int)(((unsigned)(x + 1) * (unsigned)G - 1u) / (unsigned)U);
+  }
 };
+
+// Warp transpose-reduction of 16 per-lane values: 16 shuffles instead of 16 x 5. Returns in
+// every lane the warp total of value index (lane >> 1) & 15. The tree for each index is fixed
+// (independent of the other indices' values), so per-row sums stay batch-invariant.
+__device__ __forceinline__ float warp_reduce16(const float (&v)[16], int lane) {
+  float a8[8], a4[4], a2[2];
+  {
+    const bool hi = lane & 16;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float send = hi ? v[i] : v[8 + i];
+      const float keep = hi ? v[8 + i] : v[i];
+      a8[i] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 16));
+    }
+  }
+  {
+    const bool hi = lane & 8;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float send = hi ? a8[i] : a8[4 + i];
+      const float keep = hi ? a8[4 + i] : a8[i];
+      a4[i] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 8));
+    }
+  }
+  {
+    const bool hi = lane & 4;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const float send = hi ? a4[i] : a4[2 + i];
+      const float keep = hi ? a4[2 + i] : a4[i];
+      a2[i] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 4));
+    }
+  }
+  const bool hi = lane & 2;
+  float a1 = __fadd_rn(hi ? a2[1] : a2[0], __shfl_xor_sync(0xffffffffu, hi ? a2[0] : a2[1], 2));
+  return __fadd_rn(a1, __shfl_xor_sync(0xffffffffu, a1, 1));
+}
+
+// Same transpose pattern for (max value, lowest index) pairs; argmax with lowest-index ties is
+// order independent, so the result equals a sequential scan (src/engine.py:75-76).
+__device__ __forceinline__ void argmax_pick(float& v, int& i, float ov, int oi) {
+  if (ov > v || (ov == v && oi < i)) { v = ov; i = oi; }
+}
+__device__ __forceinline__ void warp_argmax16(const float (&v)[16], int idx, int lane, float& bv,
+                                              int& bi) {
+  float a8[8], a4[4], a2[2];
+  int i8[8], i4[4], i2[2];
+  {
+    const bool hi = lane & 16;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float sv = hi ? v[i] : v[8 + i];
+      a8[i] = hi ? v[8 + i] : v[i];
+      i8[i] = idx;
+      argmax_pick(a8[i], i8[i], __shfl_xor_sync(0xffffffffu, sv, 16), __shfl_xor_sync(0xffffffffu, idx, 16));
+    }
+  }
+  {
+    const bool hi = lane & 8;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float sv = hi ? a8[i] : a8[4 + i];
+      const int si = hi ? i8[i] : i8[4 + i];
+      a4[i] = hi ? a8[4 + i] : a8[i];
+      i4[i] = hi ? i8[4 + i] : i8[i];
+      argmax_pick(a4[i], i4[i], __shfl_xor_sync(0xffffffffu, sv, 8), __shfl_xor_sync(0xffffffffu, si, 8));
+    }
+  }
+  {
+    const bool hi = lane & 4;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const float sv = hi ? a4[i] : a4[2 + i];
+      const int si = hi ? i4[i] : i4[2 + i];
+      a2[i] = hi ? a4[2 + i] : a4[i];
+      i2[i] = hi ? i4[2 + i] : i4[i];
+      argmax_pick(a2[i], i2[i], __shfl_xor_sync(0xffffffffu, sv, 4), __shfl_xor_sync(0xffffffffu, si, 4));
+    }
+  }
+  const bool hi = lane & 2;
+  bv = hi ? a2[1] : a2[0];
+  bi = hi ? i2[1] : i2[0];
+  argmax_pick(bv, bi, __shfl_xor_sync(0xffffffffu, hi ? a2[0] : a2[1], 2),
+              __shfl_xor_sync(0xffffffffu, hi ? i2[0] : i2[1], 2));
+  argmax_pick(bv, bi, __shfl_xor_sync(0xffffffffu, bv, 1), __shfl_xor_sync(0xffffffffu, bi, 1));
+}
 
 // Per-CTA shared state of the epilogue warps.
 struct EpiShared {
@@ -71,7 +164,8 @@ struct RowMeta {
 
 template <int NT>
 __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0, float (&v)[16],
-                                           int ep_t, EpiShared& sh, const RowMeta& rm) {
+                                           int ep_t, EpiShared& sh, const RowMeta& rm,
+                                           const float* pre = nullptr) {
   const int m = tile * BM + ep_t;
   // ---- RMSNorm of the input rows (X was the raw residual stream) ----
   if (p.in_ssq != nullptr) {
@@ -88,21 +182,21 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
     } break;
     case EPI_RESID: {
       const int wq = ep_t >> 5, ln = ep_t & 31;
+      float sq[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int n = n0 + j;
-        float sq = 0.f;
+        sq[j] = 0.f;
         if (n < p.n_rows && rm.kind[n] >= 0) {
           const size_t idx = (size_t)(p.row0 + n) * p.M + m;
-          const float xn = __fadd_rn(p.resid[idx], v[j]);
+          const float xn = __fadd_rn(pre != nullptr ? pre[j] : p.resid[idx], v[j]);
           p.resid[idx] = xn;
           p.resid_bf16[idx] = __float2bfloat16_rn(xn);
-          sq = __fmul_rn(xn, xn);
+          sq[j] = __fmul_rn(xn, xn);
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-        if (ln == 0) sh.red_val[wq * 16 + j] = sq;
       }
+      const float wsum = warp_reduce16(sq, ln);
+      if ((ln & 1) == 0) sh.red_val[wq * 16 + ((ln >> 1) & 15)] = wsum;
       named_bar_sync(1, 128);
       if (ep_t < 16) {
         const int n = n0 + ep_t;
@@ -157,19 +251,13 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
     } break;
     case EPI_ARGMAX: {
       const int wq = ep_t >> 5, ln = ep_t & 31;
+      float vals[16];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int n = n0 + j;
-        float val = (m < p.m_valid && n < p.n_rows) ? v[j] : -INFINITY;
-        int idx = m;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const float ov = __shfl_xor_sync(0xffffffffu, val, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
-          if (ov > val || (ov == val && oi < idx)) { val = ov; idx = oi; }
-        }
-        if (ln == 0) { sh.red_val[wq * 16 + j] = val; sh.red_idx[wq * 16 + j] = idx; }
-      }
+      for (int j = 0; j < 16; ++j) vals[j] = (m < p.m_valid && n0 + j < p.n_rows) ? v[j] : -INFINITY;
+      float bv;
+      int bi;
+      warp_argmax16(vals, m, ln, bv, bi);
+      if ((ln & 1) == 0) { sh.red_val[wq * 16 + ((ln >> 1) & 15)] = bv; sh.red_idx[wq * 16 + ((ln >> 1) & 15)] = bi; }
       named_bar_sync(1, 128);
       if (ep_t < 16) {
         float val = sh.red_val[ep_t];
@@ -246,10 +334,8 @@ __device__ __forceinline__ void lora_shrink_tasks(const GemmParams& p, int gwarp
       }
     }
     if (splits > 1 && lane == 0) {
-      __threadfence();
       int* cnt = p.sh_cnt + combo;
-      if (atomicAdd(cnt, 1) == splits - 1) {
-        __threadfence();
+      if (atom_add_acq_rel(cnt, 1) == splits - 1) {
         for (int rr = r0; rr < r1; ++rr) {
           const int gr = s_rows[rr];
           if (gr < p.row0 || gr >= p.row0 + p.n_rows) continue;
@@ -291,6 +377,21 @@ __global__ void __launch_bounds__(256, 1)
   rm.kvoff = rm.pos + NT;
   rm.inv = reinterpret_cast<float*>(rm.kvoff + NT);
 
+  auto stamp = [&](int slot) {
+    if (p.trace != nullptr) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      p.trace[(size_t)blockIdx.x * 16 + slot] = t;
+    }
+  };
+  if (threadIdx.x == 0) {
+    stamp(6);  // kernel entry (before any setup)
+    if (p.trace != nullptr) {
+      unsigned int smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      p.trace[(size_t)blockIdx.x * 16 + 8] = smid + 1;
+    }
+  }
   const int warp = warp_id();
   const int Kb = p.K / BK;  // base K chunks per tile
   const int Lc = p.lora_chunks;
@@ -300,7 +401,8 @@ __global__ void __launch_bounds__(256, 1)
   sp.G = gridDim.x;
   const int c = blockIdx.x;
   const long long u_begin = sp.ubegin(c), u_end = sp.ubegin(c + 1);
-  const int t_first = (int)(u_begin / sp.Ut), t_last = (int)((u_end - 1) / sp.Ut);
+  const int t_first = (int)((unsigned)u_begin / (unsigned)sp.Ut);
+  const int t_last = (int)((unsigned)(u_end - 1) / (unsigned)sp.Ut);
 
   if (warp == 0 && elect_one()) {
     for (int i = 0; i < NS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
@@ -318,13 +420,6 @@ __global__ void __launch_bounds__(256, 1)
   tc_fence_after();
   pdl_launch();
   const uint32_t tmem_base = *tmem_slot;
-  auto stamp = [&](int slot) {
-    if (p.trace != nullptr) {
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      p.trace[(size_t)blockIdx.x * 8 + slot] = t;
-    }
-  };
   if (threadIdx.x == 0) stamp(0);
   // pull the NEXT projection's adapter A matrices into L2 so its shrink loads hit L2
   if (p.pfa_bytes > 0 && warp == 3) {
@@ -409,11 +504,17 @@ __global__ void __launch_bounds__(256, 1)
       // Weights do not depend on the previous kernel: fill the ring before waiting on it.
       const long long total = u_end - u_begin;
       const int pre = (int)(total < NS ? total : NS);
+      const int pw = p.preissue_cap == 0 ? pre : (p.preissue_cap < 0 ? 0 : min(pre, p.preissue_cap));
       Cursor cu = start;
-      for (int i = 0; i < pre; ++i) { load_w(cu, i); advance(cu); }
+      for (int i = 0; i < pw; ++i) { load_w(cu, i); advance(cu); }
       pdl_wait();
+      stamp(7);  // previous kernel complete
       cu = start;
-      for (int i = 0; i < pre; ++i) { load_x(cu, i); advance(cu); }
+      for (int i = 0; i < pre; ++i) {
+        if (i >= pw) load_w(cu, i);
+        load_x(cu, i);
+        advance(cu);
+      }
       int stage = pre % NS;
       uint32_t phase = (pre == NS) ? 1u : 0u;
       for (long long u = u_begin + pre; u < u_end; ++u) {
@@ -462,7 +563,7 @@ __global__ void __launch_bounds__(256, 1)
                         C::IDESC, (k > kb || kk > 0) ? 1u : 0u);
           }
           tc_commit(&empty[stage]);
-          if (k == ke - 1) tc_commit(tmem_full);
+          if (k == ke - 1) { tc_commit(tmem_full); stamp(12); }
         }
         __syncwarp();
         if (++stage == NS) { stage = 0; phase ^= 1; }
@@ -484,10 +585,9 @@ __global__ void __launch_bounds__(256, 1)
       for (int i = t64; i < nseg; i += 64) s_rows[i] = p.seg_rows[i];
       named_bar_sync(2, 192);  // publish the table to the epilogue warps as well
       lora_shrink_tasks(p, blockIdx.x * 2 + (warp - 2), gridDim.x * 6, lane, s_off, s_rows);
-      __syncwarp();
-      __threadfence();
       asm volatile("fence.proxy.async.global;\n" ::: "memory");  // U is read by TMA
-      if (lane == 0) atomicAdd(p.sync, 1);
+      __syncwarp();
+      if (lane == 0) red_add_release(p.sync, 1);
       if (lane == 0 && warp == 2) stamp(1);
     }
   } else if (warp >= 4) {
@@ -495,6 +595,9 @@ __global__ void __launch_bounds__(256, 1)
     const int ep_t = threadIdx.x - 128;
     const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
     pdl_wait();
+    // the launch that used reset_sync has completed (PDL): re-arm its shrink counter for
+    // its next use (two launches later at the earliest)
+    if (p.reset_sync != nullptr && blockIdx.x == 0 && ep_t == 0) *p.reset_sync = 0;
     // stage this launch's row metadata (+ RMSNorm inverse) in smem
     for (int n = ep_t; n < NT; n += 128) {
       int kind = -1, ad = -1, pos = 0, kvoff = 0;
@@ -530,63 +633,96 @@ __global__ void __launch_bounds__(256, 1)
       named_bar_sync(2, 192);
       lora_shrink_tasks(p, gridDim.x * 2 + blockIdx.x * 4 + (warp - 4), gridDim.x * 6, lane, s_off,
                         s_rows);
-      __syncwarp();
-      __threadfence();
       asm volatile("fence.proxy.async.global;\n" ::: "memory");
-      if (lane == 0) atomicAdd(p.sync, 1);
+      __syncwarp();
+      if (lane == 0) red_add_release(p.sync, 1);
     }
     uint32_t tphase = 0;
     for (int t = t_first; t <= t_last; ++t) {
       const long long t0 = (long long)t * sp.Ut;
       const int c_first = sp.owner(t0), c_last = sp.owner(t0 + sp.Ut - 1);
       const int nseg = c_last - c_first + 1;
+      // residual rows of this tile's first 16 columns: loaded before the accumulator is
+      // ready so the epilogue's critical path has no dependent global load
+      float pre[16];
+      const bool have_pre = p.mode == EPI_RESID;
+      if (have_pre) {
+        const int m = t * BM + ep_t;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          pre[j] = (j < p.n_rows && rm.kind[j] >= 0) ? __ldcg(p.resid + (size_t)(p.row0 + j) * p.M + m) : 0.f;
+      }
       mbar_wait(tmem_full, tphase);
       tc_fence_after();
+      if (ep_t == 0) stamp(13);
       if (nseg == 1) {
         for (int cc = 0; cc < NT / 16; ++cc) {
           float v[16];
           tmem_ld16(tmem_base + lane_base + cc * 16, v);
-          finalize16<NT>(p, t, cc * 16, v, ep_t, sh, rm);
+          finalize16<NT>(p, t, cc * 16, v, ep_t, sh, rm, (have_pre && cc == 0) ? pre : nullptr);
         }
         tc_fence_before();
         mbar_arrive(tmem_empty);
       } else {
+        // partial layout [cta][slot][128 features][NT]: each thread's 16 values of a chunk are
+        // one contiguous 64-byte run (4 x 16-byte stores / loads)
         const int slot = (t == t_first) ? 0 : 1;
-        float* wsp = p.ws + (((size_t)c * 2 + slot) * NT) * BM;
+        float* wsp = p.ws + (((size_t)c * 2 + slot) * BM + ep_t) * NT;
         for (int cc = 0; cc < NT / 16; ++cc) {
           float v[16];
           tmem_ld16(tmem_base + lane_base + cc * 16, v);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) __stcg(wsp + (size_t)(cc * 16 + j) * BM + ep_t, v[j]);
+          for (int q = 0; q < 4; ++q)
+            __stcg(reinterpret_cast<float4*>(wsp + cc * 16) + q,
+                   make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
         }
         tc_fence_before();
         mbar_arrive(tmem_empty);
-        __threadfence();
         named_bar_sync(1, 128);
-        if (ep_t == 0) sh.flag = atomicAdd(&p.counters[t], 1);
+        if (ep_t == 0) { sh.flag = atom_add_acq_rel(&p.counters[t], 1); stamp(15); }
         named_bar_sync(1, 128);
         const bool last = (sh.flag == nseg - 1);
         named_bar_sync(1, 128);
         if (last) {
-          __threadfence();
+          // the last segment to arrive folds all partials in segment order; the loads of up to
+          // SEG_BATCH segments are issued before the first add (one L2 round trip, not nseg)
+          constexpr int SEG_BATCH = 8;
           for (int cc = 0; cc < NT / 16; ++cc) {
             float v[16];
-            for (int s = 0; s < nseg; ++s) {
-              const int cs = c_first + s;
-              const int ts = (int)(sp.ubegin(cs) / sp.Ut);
-              const int sl = (t == ts) ? 0 : 1;
-              const float* src = p.ws + (((size_t)cs * 2 + sl) * NT) * BM;
+            for (int s0 = 0; s0 < nseg; s0 += SEG_BATCH) {
+              float4 buf[SEG_BATCH][4];
 #pragma unroll
-              for (int j = 0; j < 16; ++j) {
-                const float x = __ldcg(src + (size_t)(cc * 16 + j) * BM + ep_t);
-                v[j] = (s == 0) ? x : __fadd_rn(v[j], x);
+              for (int s = 0; s < SEG_BATCH; ++s) {
+                if (s0 + s < nseg) {
+                  const int cs = c_first + s0 + s;
+                  const int sl = (sp.ubegin(cs) >= t0) ? 0 : 1;  // tile t is cs's first tile
+                  const float4* src = reinterpret_cast<const float4*>(
+                      p.ws + (((size_t)cs * 2 + sl) * BM + ep_t) * NT + cc * 16);
+#pragma unroll
+                  for (int q = 0; q < 4; ++q) buf[s][q] = __ldcg(src + q);
+                }
+              }
+#pragma unroll
+              for (int s = 0; s < SEG_BATCH; ++s) {
+                if (s0 + s < nseg) {
+#pragma unroll
+                  for (int q = 0; q < 4; ++q) {
+                    const float x[4] = {buf[s][q].x, buf[s][q].y, buf[s][q].z, buf[s][q].w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                      v[4 * q + e] = (s0 + s == 0) ? x[e] : __fadd_rn(v[4 * q + e], x[e]);
+                  }
+                }
               }
             }
-            finalize16<NT>(p, t, cc * 16, v, ep_t, sh, rm);
+            if (ep_t == 0 && cc == 0) stamp(10);
+            finalize16<NT>(p, t, cc * 16, v, ep_t, sh, rm, (have_pre && cc == 0) ? pre : nullptr);
+            if (ep_t == 0 && cc == 0) stamp(11);
           }
           if (ep_t == 0) p.counters[t] = 0;
         }
       }
+      if (ep_t == 0) stamp(14);
       tphase ^= 1;
     }
   }
@@ -595,15 +731,7 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   if (threadIdx.x == 0) stamp(5);
   if (warp == 2) tmem_dealloc<C::TMEM_COLS>(tmem_base);
-  if (p.sh_x != nullptr && threadIdx.x == 0) {
-    // every CTA has passed its shrink wait: the last one out resets the counters
-    __threadfence();
-    if (atomicAdd(p.sync + 1, 1) == (int)gridDim.x - 1) {
-      p.sync[0] = 0;
-      p.sync[1] = 0;
-      __threadfence();
-    }
-  }
+  if (threadIdx.x == 0) stamp(9);  // exit
 }
 
 // ------------------------------------------------------------------ host side
@@ -621,6 +749,7 @@ static cudaError_t launch_nt(const CUtensorMap& tw, const CUtensorMap& tx, const
   }
   const long long U = (long long)(p.M / BM) * (p.K / BK + p.lora_chunks);
   const int G = (int)(U < num_sms ? U : num_sms);
+  if ((unsigned long long)U * (unsigned long long)(G + 1) >= (1ull << 32)) return cudaErrorInvalidValue;
   const int NS = (p.stages > 0 && p.stages < C::STAGES) ? p.stages : C::STAGES;
   const size_t smem = 1024 + (size_t)NS * C::STAGE + aux_smem<NT>();
   return launch_pdl(gemm_streamk_kernel<NT>, dim3(G), dim3(256), smem, s, tw, tx, tlb, tlu, p,

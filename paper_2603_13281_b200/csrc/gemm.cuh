@@ -73,7 +73,8 @@ struct GemmParams {
   int slots;
   __nv_bfloat16* ubd;           // block-diagonal U [rows_total][ubd_ld] (bf16, TMA operand)
   int ubd_ld;
-  int* sync;                    // [2] shrink-done / exit counters (self-resetting)
+  int* sync;                    // shrink-done counter (target: 6 warps x grid)
+  int* reset_sync;              // counter of an EARLIER launch to zero after griddepcontrol.wait
   float* sh_part;               // [SHRINK_SPLITS][rows_total][2][rank] K-split partials
   int* sh_cnt;                  // [2][slots][rank] split arrivals per adapter row (self-resetting)
   // outputs (GLOBAL row indexing)
@@ -109,6 +110,7 @@ struct GemmParams {
   // tuning / diagnostics (0 = defaults)
   unsigned long long* trace;  // per-CTA %globaltimer stamps [grid][8] (null = off)
   int stages;     // smem ring depth actually used (<= compiled maximum)
+  int preissue_cap;  // weight stages issued before griddepcontrol.wait: 0 all, <0 none, k>0 min(k, ring)
   int skip_mma;   // 1: consume stages without tcgen05.mma (pure TMA streaming rate)
 };
 

@@ -74,6 +74,7 @@ struct AttnLaunch {
   long long pf_bytes;
   __nv_bfloat16* out;
   int out_ld;
+  unsigned long long* trace;  // diagnostic per-CTA stamps [2 launches][4096][8] (null = off)
 };
 cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t s);
 

@@ -301,6 +301,8 @@ struct icr_model {
   // per-launch timing (icr_profile_step): events recorded after every launch when set
   std::vector<cudaEvent_t>* timing = nullptr;
   std::vector<int>* timing_kind = nullptr;
+  unsigned long long* trace = nullptr;  // icr_profile_trace: [launch][grid][8] stamps
+  int skip_mask = 0;  // icr_profile_ablate: kernel kinds (1 << TK_*) left out of the forward
 };
 
 // kinds for icr_profile_step
@@ -464,13 +466,15 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
   long long launches = 0;
 
   auto gemm = [&](const CUtensorMap& wmap, CUtensorMap* xmaps, const GemmParams& p, int rows,
-                  const CUtensorMap* lbmap = nullptr) -> icr_status {
+                  const CUtensorMap* lbmap = nullptr, int kind = -1) -> icr_status {
+    if (kind >= 0 && (m->skip_mask >> kind) & 1) return ICR_OK;
     for (int g0 = 0; g0 < rows; g0 += 256) {
       const int gr = std::min(256, rows - g0);
       const int nt = gemm_pick_nt(gr);
       GemmParams q = p;
       q.n_rows = gr;
       q.row0 = g0;
+      if (m->trace) q.trace = m->trace + (size_t)launches * 4096 * 16;
       cudaError_t e = gemm_launch(wmap, xmaps[nt_index(nt)], lbmap,
                                   lbmap ? &m->xmap_ubd[nt_index(nt)] : nullptr, q, g0, nt,
                                   m->num_sms, s);
@@ -482,6 +486,7 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
 
   GemmParams base{};
   base.w_blocked = 1;
+  if (const char* e = getenv("ICR_PREISSUE")) base.preissue_cap = atoi(e);
   base.ws = m->ws;
   base.counters = m->counters;
   base.rank = c.lora_rank;
@@ -552,6 +557,7 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
         p.sh_x = m->xb; p.sh_ld = d; p.sh_K = d; p.sh_targets = 1;
         p.sh_a0 = (const __nv_bfloat16*)w.a_q;
         p.sync = m->sync + 0;
+        p.reset_sync = m->sync + 6;  // the previous down's
         p.pfa = (const uint8_t*)w.a_o;  // next shrink: o
         p.pfa_bytes = a_bytes(m->q_dim);
       }
@@ -565,7 +571,7 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
       p.v_pages = (__nv_bfloat16*)w.v_pages;
       p.block_table = bt;
       p.bt_stride = c.max_pages_per_seq;
-      if ((st = gemm(lm.qkv, m->xmap_xb, p, rp, lora ? &lm.lb_q : nullptr))) return st;
+      if ((st = gemm(lm.qkv, m->xmap_xb, p, rp, lora ? &lm.lb_q : nullptr, TK_QKV))) return st;
       mark(m, s, TK_QKV);
     }
     al.k_pages = (const __nv_bfloat16*)w.k_pages;
@@ -575,7 +581,8 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
     al.pf_base = pf_on ? (const uint8_t*)w.w_o : nullptr;
     al.pf_bytes = (long long)d * m->q_dim * 2;
     {  // attention over 2H heads (src/model.py:497-501)
-      cudaError_t e = attn_launch(al, s);
+      al.trace = m->trace ? m->trace + (size_t)launches * 4096 * 16 : nullptr;
+      cudaError_t e = (m->skip_mask >> TK_ATTN) & 1 ? cudaSuccess : attn_launch(al, s);
       if (e != cudaSuccess) return fail(ICR_CUDA, "attention launch: %s", cudaGetErrorString(e));
       launches += 2;
       mark(m, s, TK_ATTN);
@@ -590,6 +597,7 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
         p.sh_x = m->att; p.sh_ld = m->q_dim; p.sh_K = m->q_dim; p.sh_targets = 1;
         p.sh_a0 = (const __nv_bfloat16*)w.a_o;
         p.sync = m->sync + 2;
+        p.reset_sync = m->sync + 0;
         p.pfa = (const uint8_t*)w.a_gate;  // next shrink: gate | up
         p.pfa2 = (const uint8_t*)w.a_up;
         p.pfa_bytes = a_bytes(d);
@@ -598,7 +606,7 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
       p.resid_bf16 = m->xb;
       p.out_ssq = m->ssq;
       set_prefetch(m, p, w.w_gu, 2 * c.ffn_dim, d, rp);
-      if ((st = gemm(lm.o, m->xmap_att, p, rp, lora ? &lm.lb_o : nullptr))) return st;
+      if ((st = gemm(lm.o, m->xmap_att, p, rp, lora ? &lm.lb_o : nullptr, TK_O))) return st;
       mark(m, s, TK_O);
     }
     {  // gate | up + SiLU (src/model.py:503-505)
@@ -612,12 +620,13 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
         p.sh_x = m->xb; p.sh_ld = d; p.sh_K = d; p.sh_targets = 2;
         p.sh_a0 = (const __nv_bfloat16*)w.a_gate; p.sh_a1 = (const __nv_bfloat16*)w.a_up;
         p.sync = m->sync + 4;
+        p.reset_sync = m->sync + 2;
         p.pfa = (const uint8_t*)w.a_down;  // next shrink: down
         p.pfa_bytes = a_bytes(c.ffn_dim);
       }
       p.out_bf16 = m->f;
       set_prefetch(m, p, w.w_down, d, c.ffn_dim, rp);
-      if ((st = gemm(lm.gu, m->xmap_xb, p, rp, lora ? &lm.lb_gu : nullptr))) return st;
+      if ((st = gemm(lm.gu, m->xmap_xb, p, rp, lora ? &lm.lb_gu : nullptr, TK_GU))) return st;
       mark(m, s, TK_GU);
     }
     {  // down + residual (src/model.py:506)
@@ -630,6 +639,7 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
         p.sh_x = m->f; p.sh_ld = c.ffn_dim; p.sh_K = c.ffn_dim; p.sh_targets = 1;
         p.sh_a0 = (const __nv_bfloat16*)w.a_down;
         p.sync = m->sync + 6;
+        p.reset_sync = m->sync + 4;
         if (l + 1 < c.num_layers) {  // next shrink: the next layer's q
           p.pfa = (const uint8_t*)m->layers[l + 1].a_q;
           p.pfa_bytes = a_bytes(d);
@@ -642,7 +652,7 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
         set_prefetch(m, p, m->layers[l + 1].w_qkv, qkv_M, d, rp);
       else
         set_prefetch(m, p, m->lm_head, m->vpad, d, rp);
-      if ((st = gemm(lm.down, m->xmap_f, p, rp, lora ? &lm.lb_down : nullptr))) return st;
+      if ((st = gemm(lm.down, m->xmap_f, p, rp, lora ? &lm.lb_down : nullptr, TK_DOWN))) return st;
       mark(m, s, TK_DOWN);
     }
   }
@@ -664,7 +674,7 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
     p.in_ssq = m->ssq_lm;
     p.tile_best = m->tile_best;
     p.best_stride = rp;
-    if ((st = gemm(m->lm_map, m->xmap_hlm, p, mt.n_lm))) return st;
+    if ((st = gemm(m->lm_map, m->xmap_hlm, p, mt.n_lm, nullptr, TK_LM))) return st;
     mark(m, s, TK_LM);
     CUDA_TRY(argmax_reduce_launch(m->tile_best, m->vpad / 128, rp, mt.n_lm, m->out_tok, s));
     ++launches;
@@ -968,6 +978,99 @@ icr_status icr_decode_loop(icr_model* m, const icr_batch* first, const int32_t* 
   return st;
 }
 
+// Replay the last forward as a CUDA graph with the kernel kinds in skip_mask (bits 1 << TK_*)
+// left out, `iters` times; returns the average device ms per forward. The marginal cost of a
+// kernel kind inside the real PDL-chained graph is the difference to skip_mask = 0.
+// Diagnostic only: skipping kernels leaves garbage in scratch (and K/V of the last positions).
+icr_status icr_profile_ablate(icr_model* m, int skip_mask, int iters, float* avg_ms, void* stream) {
+  if (!m || !avg_ms || iters < 1) return fail(ICR_CONFIG, "bad arguments");
+  if (!m->has_last) return fail(ICR_STATE, "profile needs a previous forward");
+  cudaStream_t s = (cudaStream_t)stream;
+  const Meta mt = m->last_mt;
+  cudaGraph_t g;
+  CUDA_TRY(cudaStreamBeginCapture(m->capture_stream, cudaStreamCaptureModeThreadLocal));
+  m->skip_mask = skip_mask;
+  icr_status st = enqueue_forward(m, mt, nullptr, m->capture_stream);
+  m->skip_mask = 0;
+  cudaError_t ce = cudaStreamEndCapture(m->capture_stream, &g);
+  if (st) return st;
+  if (ce != cudaSuccess) return fail(ICR_CUDA, "ablate capture: %s", cudaGetErrorString(ce));
+  cudaGraphExec_t ex;
+  ce = cudaGraphInstantiate(&ex, g, 0);
+  cudaGraphDestroy(g);
+  if (ce != cudaSuccess) return fail(ICR_CUDA, "ablate instantiate: %s", cudaGetErrorString(ce));
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  CUDA_TRY(cudaGraphLaunch(ex, s));
+  CUDA_TRY(cudaEventRecord(e0, s));
+  for (int i = 0; i < iters; ++i) CUDA_TRY(cudaGraphLaunch(ex, s));
+  CUDA_TRY(cudaEventRecord(e1, s));
+  CUDA_TRY(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  *avg_ms = ms / (float)iters;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaGraphExecDestroy(ex);
+  return ICR_OK;
+}
+
+// Replay the last forward as a CUDA graph with per-CTA %globaltimer stamps in every GEMM
+// launch (entry, setup done, shrink done, LoRA wait begin/end, all loads issued, end,
+// previous kernel complete) and write them to `path` as CSV (launch, cta, 8 stamps in us
+// relative to the first stamp). Diagnostic only.
+icr_status icr_profile_trace(icr_model* m, const char* path, void* stream) {
+  if (!m || !path) return fail(ICR_CONFIG, "bad arguments");
+  if (!m->has_last) return fail(ICR_STATE, "profile needs a previous forward");
+  cudaStream_t s = (cudaStream_t)stream;
+  const Meta mt = m->last_mt;
+  const size_t max_launch = 256, n = max_launch * 4096 * 16;
+  unsigned long long* tr = nullptr;
+  CUDA_TRY(cudaMalloc(&tr, n * sizeof(unsigned long long)));
+  CUDA_TRY(cudaMemsetAsync(tr, 0, n * sizeof(unsigned long long), s));
+  cudaGraph_t g;
+  CUDA_TRY(cudaStreamBeginCapture(m->capture_stream, cudaStreamCaptureModeThreadLocal));
+  m->trace = tr;
+  m->skip_mask = getenv("ICR_SKIP") ? atoi(getenv("ICR_SKIP")) : 0;
+  icr_status st = enqueue_forward(m, mt, nullptr, m->capture_stream);
+  m->skip_mask = 0;
+  m->trace = nullptr;
+  const long long nl = m->last_launches;
+  cudaError_t ce = cudaStreamEndCapture(m->capture_stream, &g);
+  if (st) { cudaFree(tr); return st; }
+  if (ce != cudaSuccess) { cudaFree(tr); return fail(ICR_CUDA, "trace capture: %s", cudaGetErrorString(ce)); }
+  cudaGraphExec_t ex;
+  ce = cudaGraphInstantiate(&ex, g, 0);
+  cudaGraphDestroy(g);
+  if (ce != cudaSuccess) { cudaFree(tr); return fail(ICR_CUDA, "trace instantiate: %s", cudaGetErrorString(ce)); }
+  for (int i = 0; i < 3; ++i) CUDA_TRY(cudaGraphLaunch(ex, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  cudaGraphExecDestroy(ex);
+  std::vector<unsigned long long> h(n);
+  CUDA_TRY(cudaMemcpy(h.data(), tr, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  cudaFree(tr);
+  unsigned long long t0 = ~0ull;
+  for (size_t i = 0; i < n; ++i)
+    if (i % 16 < 8 && h[i] && h[i] < t0) t0 = h[i];
+  FILE* f = fopen(path, "w");
+  if (!f) return fail(ICR_CONFIG, "cannot write %s", path);
+  fprintf(f, "launch,cta,start,shrink_done,wait_begin,wait_end,issued_all,end,entry,prev_done,smid,exit,sum_done,fin0_done,mma_last_commit,epi_tmem_full,epi_done,epi_atomic\n");
+  for (size_t l = 0; l < max_launch && (long long)l < nl + 8; ++l)
+    for (int c2 = 0; c2 < 4096; ++c2) {
+      const unsigned long long* r = &h[(l * 4096 + c2) * 16];
+      if (!r[6]) continue;
+      fprintf(f, "%zu,%d", l, c2);
+      for (int k = 0; k < 8; ++k) fprintf(f, ",%.3f", r[k] ? (r[k] - t0) / 1000.0 : -1.0);
+      fprintf(f, ",%d", (int)r[8] - 1);
+      for (int k = 9; k < 12; ++k) fprintf(f, ",%.3f", r[k] ? (r[k] - t0) / 1000.0 : -1.0);
+      for (int k = 12; k < 16; ++k) fprintf(f, ",%.3f", r[k] ? (r[k] - t0) / 1000.0 : -1.0);
+      fprintf(f, "\n");
+    }
+  fclose(f);
+  return ICR_OK;
+}
+
 // Instrumentation: [launches, metadata bytes, attention items] of the last forward.
 icr_status icr_model_stats(icr_model* m, int64_t* out3) {
   if (!m || !out3) return fail(ICR_CONFIG, "null argument");
@@ -1033,7 +1136,7 @@ icr_status icr_profile_gemm(icr_model* m, int which_raw, int iters, float* avg_m
   const bool no_lora = (which_raw >> 4) & 1, plain = (which_raw >> 5) & 1,
              no_shrink = (which_raw >> 6) & 1, traced = (which_raw >> 8) & 1;
   static unsigned long long* trace_dev = nullptr;
-  if (traced && !trace_dev) CUDA_TRY(cudaMalloc(&trace_dev, 4096 * 8 * sizeof(unsigned long long)));
+  if (traced && !trace_dev) CUDA_TRY(cudaMalloc(&trace_dev, 4096 * 16 * sizeof(unsigned long long)));
   const bool lora = c.lora_rank > 0 && !no_lora;
   GemmParams p{};
   p.w_blocked = 1;
@@ -1094,6 +1197,8 @@ icr_status icr_profile_gemm(icr_model* m, int which_raw, int iters, float* avg_m
   CUDA_TRY(cudaEventCreate(&e0));
   CUDA_TRY(cudaEventCreate(&e1));
   const int L = which == 3 ? 1 : c.num_layers;
+  // back-to-back launches alternate between two shrink counters; each re-arms the other
+  CUDA_TRY(cudaMemsetAsync(m->sync + 10, 0, 4 * sizeof(int), s));
   CUDA_TRY(cudaEventRecord(e0, s));
   for (int it = 0; it < iters; ++it)
     for (int l = 0; l < L; ++l) {
@@ -1106,10 +1211,15 @@ icr_status icr_profile_gemm(icr_model* m, int which_raw, int iters, float* avg_m
                         q.sh_a0 = (const __nv_bfloat16*)w.a_gate; q.sh_a1 = (const __nv_bfloat16*)w.a_up; }
       if (which == 2) { wm = &m->maps[l].down; lb = &m->maps[l].lb_down; q.sh_a0 = (const __nv_bfloat16*)w.a_down; }
       if (!lora) lb = nullptr;
-      if (no_shrink) { q.sh_x = nullptr; q.sync = nullptr; }
+      if (q.sync != nullptr) {
+        const int k = it * L + l;
+        q.sync = m->sync + ((k & 1) ? 12 : 10);
+        q.reset_sync = m->sync + ((k & 1) ? 10 : 12);
+      }
+      if (no_shrink) { q.sh_x = nullptr; q.sync = nullptr; q.reset_sync = nullptr; }
       if (traced && it == iters - 1 && l == 0) {
         q.trace = trace_dev;
-        cudaMemsetAsync(trace_dev, 0, 4096 * 8 * sizeof(unsigned long long), s);
+        cudaMemsetAsync(trace_dev, 0, 4096 * 16 * sizeof(unsigned long long), s);
       }
       if (no_shrink && lora) {
         // stale-U variant: LoRA chunks without waiting (sync pre-satisfied)
@@ -1127,18 +1237,18 @@ icr_status icr_profile_gemm(icr_model* m, int which_raw, int iters, float* avg_m
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   if (traced) {
-    std::vector<unsigned long long> h(4096 * 8);
+    std::vector<unsigned long long> h(4096 * 16);
     CUDA_TRY(cudaMemcpy(h.data(), trace_dev, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     // report relative to the earliest CTA start, in microseconds, for CTAs 0..grid-1
     unsigned long long t0 = ~0ull;
-    for (int c2 = 0; c2 < 4096; ++c2) if (h[c2 * 8] && h[c2 * 8] < t0) t0 = h[c2 * 8];
+    for (int c2 = 0; c2 < 4096; ++c2) if (h[c2 * 16] && h[c2 * 16] < t0) t0 = h[c2 * 16];
     FILE* f = fopen("gpurun_out/gemm_trace.csv", "w");
     if (f) {
       fprintf(f, "cta,start,shrink_done,wait_begin,wait_end,issued_all,end\n");
       for (int c2 = 0; c2 < 4096; ++c2) {
-        if (!h[c2 * 8]) continue;
+        if (!h[c2 * 16]) continue;
         fprintf(f, "%d", c2);
-        for (int k = 0; k < 6; ++k) fprintf(f, ",%.2f", h[c2 * 8 + k] ? (h[c2 * 8 + k] - t0) / 1000.0 : -1.0);
+        for (int k = 0; k < 6; ++k) fprintf(f, ",%.2f", h[c2 * 16 + k] ? (h[c2 * 16 + k] - t0) / 1000.0 : -1.0);
         fprintf(f, "\n");
       }
       fclose(f);
