@@ -182,14 +182,23 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
     } break;
     case EPI_RESID: {
       const int wq = ep_t >> 5, ln = ep_t & 31;
-      float sq[16];
+      float sq[16], old[16];
+      // all residual loads before any store (the stores may alias them for the compiler, which
+      // would otherwise expose one L2 round trip per row)
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int n = n0 + j;
+        old[j] = pre != nullptr ? pre[j]
+                 : (n < p.n_rows && rm.kind[n] >= 0) ? __ldcg(p.resid + (size_t)(p.row0 + n) * p.M + m)
+                                                     : 0.f;
+      }
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int n = n0 + j;
         sq[j] = 0.f;
         if (n < p.n_rows && rm.kind[n] >= 0) {
           const size_t idx = (size_t)(p.row0 + n) * p.M + m;
-          const float xn = __fadd_rn(pre != nullptr ? pre[j] : p.resid[idx], v[j]);
+          const float xn = __fadd_rn(old[j], v[j]);
           p.resid[idx] = xn;
           p.resid_bf16[idx] = __float2bfloat16_rn(xn);
           sq[j] = __fmul_rn(xn, xn);
@@ -226,6 +235,15 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
       const int i = (m - base) % hd;
       const int head = (m - base) / hd;
       __nv_bfloat16* pages = region == 1 ? p.k_pages : p.v_pages;
+      // RoPE factors of all 16 rows loaded up front (one round trip, not one per row)
+      float2 csv[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int n = n0 + j;
+        csv[j] = (region < 2 && n < p.n_rows && rm.kind[n] >= 0)
+                     ? __ldg(p.rope + (size_t)rm.pos[n] * (hd >> 1) + (i >> 1))
+                     : make_float2(1.f, 0.f);
+      }
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const float partner = __shfl_xor_sync(0xffffffffu, v[j], 1);
@@ -235,7 +253,7 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
         float out = v[j];
         if (region < 2) {
           // Interleaved-pair RoPE, src/tensor.py:309-315.
-          const float2 cs = p.rope[(size_t)rm.pos[n] * (hd >> 1) + (i >> 1)];
+          const float2 cs = csv[j];
           if ((i & 1) == 0)
             out = __fsub_rn(__fmul_rn(v[j], cs.x), __fmul_rn(partner, cs.y));
           else

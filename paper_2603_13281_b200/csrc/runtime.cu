@@ -433,7 +433,9 @@ static icr_status validate_batch(icr_model* m, const icr_batch* b, const int* po
 static const int kPfMaxUnits = 24;  // per CTA: 24 x 16 KB x 148 CTAs ~= 57 MB of L2
 static void set_prefetch(const icr_model* m, GemmParams& p, const void* next_w, int next_M,
                          int next_K, int rows) {
-  if (next_w == nullptr || rows > 256 || getenv("ICR_NO_PREFETCH")) return;
+  // Off by default: the tail prefetch (up to 57 MB) saturates HBM exactly while the last
+  // tiles' epilogues need low-latency L2 round trips (measured: +0.35 ms per decode step).
+  if (next_w == nullptr || rows > 256 || !getenv("ICR_L2_PREFETCH")) return;
   const long long U = (long long)(next_M / 128) * (next_K / 64);
   const int G = (int)std::min<long long>(U, m->num_sms);
   const int skip = gemm_stages(gemm_pick_nt(rows));
@@ -461,7 +463,7 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
   // without an adapter), so stream-K split points -- and with them every encoder row's
   // bits -- never depend on which rows the batch holds.
   const bool lora = c.lora_rank > 0;
-  const bool pf_a_on = !getenv("ICR_NO_PREFETCH");
+  const bool pf_a_on = getenv("ICR_L2_PREFETCH") != nullptr;
   const int d = c.hidden_dim, rp = mt.rp;
   long long launches = 0;
 
@@ -537,7 +539,7 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
     return pf_a_on ? (long long)c.adapter_slots * c.lora_rank * K * 2 : 0;
   };
   const int qkv_M = m->q_dim + 2 * m->kv_dim;
-  const bool pf_on = rp <= 256 && !getenv("ICR_NO_PREFETCH");
+  const bool pf_on = rp <= 256 && getenv("ICR_L2_PREFETCH") != nullptr;
   CUDA_TRY(embed_launch(tokens, kind, m->embed, m->x, m->xb, m->ssq, rp, rp, d,
                         pf_on ? (const uint8_t*)m->layers[0].w_qkv : nullptr,
                         (long long)qkv_M * d * 2, m->ubd, m->ubd_ld, s));

@@ -24,6 +24,10 @@ __global__ void __launch_bounds__(128, 1)
     int p = 0;
     for (int i = 0; i < 64; ++i) p = chain[p];
     __syncwarp(1);
+    if (streaming) {  // let the streaming CTAs run for a while (TLB / queue pressure)
+      const long long w = clock64();
+      while (clock64() - w < 40000) {}
+    }
     long long t0 = clock64();
     for (int i = 0; i < 64; ++i) p = use_cg ? __ldcg(chain + p) : *(volatile const int*)(chain + p);
     long long t1 = clock64();
@@ -80,13 +84,25 @@ int main() {
   uint8_t* buf;
   cudaMalloc(&buf, total);
   cudaMemset(buf, 1, total);
-  // pointer chain with a 4 KB stride over 1 MB (L2 resident, no L1 reuse)
-  const int N = 1 << 18;
+  // pointer chains: (a) 4 KB stride within 1 MB; (b) one hop per 2 MB page over 256 MB
+  const int N = 1 << 26;  // 256 MB of ints
   int* h = new int[N];
-  for (int i = 0; i < N; ++i) h[i] = (i + 1031) % N;
+  for (int i = 0; i < N; ++i) h[i] = 0;
+  const int small_n = 1 << 18;
+  for (int i = 0; i < small_n; ++i) h[i] = (i + 1031) % small_n;
   int *chain, *atom;
-  cudaMalloc(&chain, N * sizeof(int));
-  cudaMemcpy(chain, h, N * sizeof(int), cudaMemcpyHostToDevice);
+  cudaMalloc(&chain, (size_t)N * sizeof(int));
+  int* chain_far;
+  {
+    // far chain lives in the same allocation at offset 16 MB: hop = 2 MB + 4 KB, 64 hops
+    const int base = 1 << 22, hop = (1 << 19) + 1024;
+    for (int k = 0; k < 100; ++k) {
+      const long long a = base + (long long)k * hop, b = base + (long long)(k + 1) * hop;
+      if (b < N) h[a] = (int)(b - base);
+    }
+    chain_far = chain + base;
+  }
+  cudaMemcpy(chain, h, (size_t)N * sizeof(int), cudaMemcpyHostToDevice);
   cudaMalloc(&atom, 4096 * sizeof(int));
   cudaMemset(atom, 0, 4096 * sizeof(int));
   long long* out;
@@ -94,9 +110,11 @@ int main() {
   const int smem = STAGES * STAGE_BYTES + 1024;
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   long long ho[4096];
+  for (int far = 0; far < 2; ++far)
   for (int streaming = 0; streaming < 2; ++streaming)
-    for (int cg = 0; cg < 2; ++cg) {
-      probe<<<148, 128, smem>>>(buf, 1ll << 30, 8, chain, atom, out, streaming, cg);
+    for (int cg = 1; cg < 2; ++cg) {
+      printf("%s chain: ", far ? "2MB-page-hopping" : "1MB-local");
+      probe<<<148, 128, smem>>>(buf, 1ll << 30, 8, far ? chain_far : chain, atom, out, streaming, cg);
       cudaDeviceSynchronize();
       cudaMemcpy(ho, out, sizeof(ho), cudaMemcpyDeviceToHost);
       long long ld = 0, at = 0;
