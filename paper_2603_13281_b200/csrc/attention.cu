@@ -124,9 +124,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
     fence_barrier_init();
   }
   __syncthreads();
-  pdl_wait();
-  if (trace != nullptr && threadIdx.x == 0 && cta_id < 4096)
-    trace[(size_t)cta_id * 16 + 7] = globaltimer();
+  // the plan (items, pages) was uploaded before the forward: readable before the wait
   const AttnItem it = items[item_id];
   const int g = blockIdx.y;
 
@@ -135,7 +133,13 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
     if (elect_one()) {
       tma_prefetch_desc(&tm_k);
       tma_prefetch_desc(&tm_v);
+      // pages written by earlier steps stream in while the q/k/v GEMM is still finishing
+      const int pre = min(it.n_pre, PAGE_STAGES);
       for (int pi = 0; pi < it.n_pages; ++pi) {
+        if (pi == pre) {
+          pdl_wait();
+          if (trace != nullptr && cta_id < 4096) trace[(size_t)cta_id * 16 + 7] = globaltimer();
+        }
         const int st = pi % PAGE_STAGES;
         mbar_wait(&empty[st], ((pi / PAGE_STAGES) & 1) ^ 1);
         const int plane = item_pages[it.page_off + pi] * num_kv_heads + g;
@@ -147,11 +151,13 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
           tma_load_3d(kd + PB + h * 2048, &tm_v, &full[st], h * 64, 0, plane);
         }
       }
+      if (it.n_pages <= pre) pdl_wait();
     }
     return;
   }
 
   // ---------------- consumers ----------------
+  pdl_wait();  // q comes from the q/k/v GEMM
   const int cw = warp - 1, rg = cw & 3, kg = cw >> 2;
   const int ctid = tid - 32;
   for (int idx = ctid; idx < 64 * CH; idx += 256) {

@@ -48,6 +48,8 @@ struct AttnItem {
   int row_off;      // into item_rows
   int n_rows;       // query rows (<= 64)
   int chunk_idx;    // chunk index c (partial slot)
+  int n_pre;        // leading pages entirely below every row's position: written by earlier
+                    // steps, so the producer may load them before griddepcontrol.wait
 };
 
 struct AttnLaunch {

@@ -154,12 +154,15 @@ static icr_status build_attn_plan(int n_rows, const int* kind, const int* seq, c
   plan.rows.clear();
   std::vector<std::vector<int>> seq_rows(n_seqs);
   std::vector<int> maxpos(n_seqs, -1);
+  // lowest position whose K/V this forward writes, per sequence (encoder rows write K/V)
+  std::vector<int> minnew(n_seqs, INT32_MAX);
   for (int r = 0; r < n_rows; ++r) {
     if (kind[r] < 0) continue;
     const int s = seq[r];
     if (s < 0 || s >= n_seqs) return fail(ICR_SHAPE, "row %d: sequence slot %d outside [0,%d)", r, s, n_seqs);
     seq_rows[s].push_back(r);
     maxpos[s] = std::max(maxpos[s], pos[r]);
+    if (kind[r] == 0) minnew[s] = std::min(minnew[s], pos[r]);
   }
   struct Group {
     int c;
@@ -195,6 +198,8 @@ static icr_status build_attn_plan(int n_rows, const int* kind, const int* seq, c
     const int c0 = gr.c * CT, c1 = (gr.c + 1) * CT - 1;
     std::vector<int2> entries;
     std::vector<int> entry_pos;
+    int fresh = INT32_MAX;  // first key position of these pages written by this forward
+    for (int s : gr.seqs) fresh = std::min(fresh, minnew[s]);
     for (int s : gr.seqs)
       for (int r : seq_rows[s])
         if (pos[r] >= c0)
@@ -214,6 +219,9 @@ static icr_status build_attn_plan(int n_rows, const int* kind, const int* seq, c
       it.row_off = (int)plan.rows.size();
       it.n_rows = (int)(e1 - e0);
       it.chunk_idx = gr.c;
+      // pages [0, n_pre) hold only keys < fresh: none is written by this forward
+      it.n_pre = fresh == INT32_MAX ? npages
+                                    : std::min(npages, std::max(0, (fresh - c0) >> 4));
       plan.items.push_back(it);
       plan.pages.insert(plan.pages.end(), gr.pages.begin(), gr.pages.begin() + npages);
       plan.rows.insert(plan.rows.end(), entries.begin() + e0, entries.begin() + e1);
@@ -489,6 +497,7 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
   GemmParams base{};
   base.w_blocked = 1;
   if (const char* e = getenv("ICR_PREISSUE")) base.preissue_cap = atoi(e);
+  if (const char* e = getenv("ICR_STAGES")) base.stages = atoi(e);
   base.ws = m->ws;
   base.counters = m->counters;
   base.rank = c.lora_rank;
