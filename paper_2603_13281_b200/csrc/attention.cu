@@ -14,6 +14,7 @@
 // CTA -- the batch-invariance the reference gets from its per-head loop (2H == H||H,
 // tests/test_model.py:225-239) and that makes prefill / decode KV bytes identical.
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "ptx.cuh"
@@ -373,16 +374,32 @@ __global__ void __launch_bounds__(512)
   float* wts = merge_smem;
   float* Ls = merge_smem + group * max_chunks;
   const int tid = threadIdx.x;
+  // Chunk partials are loaded MB at a time before they are folded (in chunk order): one L2
+  // round trip per MB chunks instead of one per chunk.
+  constexpr int MB = 16;
   if (tid < group) {
     const size_t base = ((size_t)r * num_heads + g * group + tid) * max_chunks;
     float M = -INFINITY;
-    for (int c = 0; c < nch; ++c) M = fmaxf(M, part_ml[base + c].x);
+    for (int c0 = 0; c0 < nch; c0 += MB) {
+      float2 ml[MB];
+#pragma unroll
+      for (int k = 0; k < MB; ++k) ml[k] = (c0 + k < nch) ? part_ml[base + c0 + k] : make_float2(-INFINITY, 0.f);
+#pragma unroll
+      for (int k = 0; k < MB; ++k) M = fmaxf(M, ml[k].x);
+    }
     float L = 0.f;
-    for (int c = 0; c < nch; ++c) {
-      const float2 ml = part_ml[base + c];
-      const float w = exp2f(ml.x - M);  // partial maxima are in the log2 domain
-      wts[tid * max_chunks + c] = w;
-      L = fmaf(ml.y, w, L);
+    for (int c0 = 0; c0 < nch; c0 += MB) {
+      float2 ml[MB];
+#pragma unroll
+      for (int k = 0; k < MB; ++k) ml[k] = (c0 + k < nch) ? part_ml[base + c0 + k] : make_float2(-INFINITY, 0.f);
+#pragma unroll
+      for (int k = 0; k < MB; ++k) {
+        if (c0 + k < nch) {
+          const float w = exp2f(ml[k].x - M);  // partial maxima are in the log2 domain
+          wts[tid * max_chunks + c0 + k] = w;
+          L = fmaf(ml[k].y, w, L);
+        }
+      }
     }
     Ls[tid] = L;
   }
@@ -392,14 +409,38 @@ __global__ void __launch_bounds__(512)
     const int head = g * group + hg;
     const size_t base = ((size_t)r * num_heads + head) * max_chunks;
     float O = 0.f;
-    for (int c = 0; c < nch; ++c) O = fmaf(part_o[(base + c) * HD + d], wts[hg * max_chunks + c], O);
+    for (int c0 = 0; c0 < nch; c0 += MB) {
+      float po[MB];
+#pragma unroll
+      for (int k = 0; k < MB; ++k) po[k] = (c0 + k < nch) ? part_o[(base + c0 + k) * HD + d] : 0.f;
+#pragma unroll
+      for (int k = 0; k < MB; ++k)
+        if (c0 + k < nch) O = fmaf(po[k], wts[hg * max_chunks + c0 + k], O);
+    }
     out[(size_t)r * out_ld + head * HD + d] = __float2bfloat16_rn(__fdiv_rn(O, Ls[hg]));
   }
   if (trace != nullptr && threadIdx.x == 0 && cta_id < 4096) trace[(size_t)cta_id * 16 + 5] = globaltimer();
 }
 
+static bool use_tc(int head_dim) {
+  static const bool mma_only = getenv("ICR_ATTN_MMA") != nullptr;
+  return head_dim == 128 && !mma_only;
+}
+
+int attn_entries_per_item(int head_dim) { return use_tc(head_dim) ? 128 : 64; }
+
 template <int HD>
 static cudaError_t attn_launch_hd(const AttnLaunch& a, cudaStream_t s) {
+  if (use_tc(HD)) {
+    cudaError_t e = attn_tc_partial_launch(a, a.chunk_tokens / 16, s);
+    if (e != cudaSuccess) return e;
+    const int mthreads = std::min(512, ((a.group * HD + 31) / 32) * 32);
+    const size_t msmem = (size_t)a.group * (a.max_chunks + 1) * sizeof(float);
+    return launch_pdl(attn_merge_kernel<HD>, dim3(a.n_rows, a.num_kv_heads), dim3(mthreads), msmem, s,
+                      a.part_o, a.part_ml, a.row_pos, a.row_kind, a.num_heads, a.group,
+                      a.max_chunks, a.chunk_tokens, a.out, a.out_ld,
+                      a.trace ? a.trace + 4096 * 16 : nullptr);
+  }
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(attn_partial_kernel<HD>,

@@ -79,6 +79,11 @@ struct AttnLaunch {
   unsigned long long* trace;  // diagnostic per-CTA stamps [2 launches][4096][8] (null = off)
 };
 cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t s);
+// tcgen05 partial kernel (attention_tc.cu), head_dim 128, chunks of <= 16 pages.
+cudaError_t attn_tc_partial_launch(const AttnLaunch& a, int chunk_pages, cudaStream_t s);
+// Query entries (row, head-in-group) per work item: 128 = the tcgen05 M (head_dim 128
+// unless ICR_ATTN_MMA=1), 64 for the mma.sync kernel.
+int attn_entries_per_item(int head_dim);
 
 // --------------------------------------------------------------- row ops (rowops.cu)
 // Layer-0 input: x[r] = embed[tok[r]] (fp32 residual stream), xb = bf16(x), and the

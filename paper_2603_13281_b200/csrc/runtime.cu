@@ -147,8 +147,9 @@ struct AttnPlan {
 // is read once per KV head for every query row attached to it.
 static icr_status build_attn_plan(int n_rows, const int* kind, const int* seq, const int* pos,
                                   const int* bt, int n_seqs, int bt_stride, int num_pages,
-                                  int group, int chunk_pages, AttnPlan& plan) {
+                                  int group, int chunk_pages, AttnPlan& plan, int head_dim) {
   const int CT = chunk_pages * 16;
+  const size_t EPI = (size_t)attn_entries_per_item(head_dim);
   plan.items.clear();
   plan.pages.clear();
   plan.rows.clear();
@@ -207,8 +208,8 @@ static icr_status build_attn_plan(int n_rows, const int* kind, const int* seq, c
             entries.push_back(make_int2(r, hg));
             entry_pos.push_back(pos[r]);
           }
-    for (size_t e0 = 0; e0 < entries.size(); e0 += 64) {
-      const size_t e1 = std::min(entries.size(), e0 + 64);
+    for (size_t e0 = 0; e0 < entries.size(); e0 += EPI) {
+      const size_t e1 = std::min(entries.size(), e0 + EPI);
       int npages = 0;
       for (size_t e = e0; e < e1; ++e)
         npages = std::max(npages, ((std::min(entry_pos[e], c1) - c0) >> 4) + 1);
@@ -918,7 +919,7 @@ icr_status icr_forward(icr_model* m, const icr_batch* b, int32_t* out_tokens_hos
   AttnPlan plan;
   st = build_attn_plan(b->n_rows, b->row_kind, b->row_seq, b->row_pos, b->block_table, b->n_seqs,
                        m->cfg.max_pages_per_seq, m->cfg.num_pages, plan_group(m),
-                       m->cfg.chunk_pages, plan);
+                       m->cfg.chunk_pages, plan, m->cfg.head_dim);
   if (st) return st;
   Meta mt = layout_meta(m, b->n_rows);
   if ((st = ensure_meta(m, mt.total))) return st;
@@ -958,7 +959,7 @@ icr_status icr_decode_loop(icr_model* m, const icr_batch* first, const int32_t* 
     AttnPlan plan;
     if ((st = build_attn_plan(n, first->row_kind, first->row_seq, pos.data(), first->block_table,
                               first->n_seqs, m->cfg.max_pages_per_seq, m->cfg.num_pages,
-                              plan_group(m), m->cfg.chunk_pages, plan)))
+                              plan_group(m), m->cfg.chunk_pages, plan, m->cfg.head_dim)))
       break;
     const int slot = i & 1;
     cudaEventSynchronize(m->staging_ev[slot]);
@@ -1361,7 +1362,7 @@ icr_status icr_bench_attention(const void* q_dev, const void* k_pages, const voi
   AttnPlan plan;
   icr_status st = build_attn_plan(n_rows, kind.data(), row_seq_host, row_pos_host, block_table_host,
                                   n_seqs, max_pages_per_seq, 1 << 30, num_heads / num_kv_heads,
-                                  chunk_pages, plan);
+                                  chunk_pages, plan, head_dim);
   if (st) return st;
   if (n_items_out) *n_items_out = (int)plan.items.size();
   int maxpos = 0;
@@ -1500,7 +1501,7 @@ icr_status icr_paged_attention(const void* q_dev, const void* k_pages, const voi
   AttnPlan plan;
   icr_status st = build_attn_plan(n_rows, kind.data(), row_seq_host, row_pos_host, block_table_host,
                                   n_seqs, max_pages_per_seq, 1 << 30, num_heads / num_kv_heads,
-                                  chunk_pages, plan);
+                                  chunk_pages, plan, head_dim);
   if (st) return st;
   if (n_items_out) *n_items_out = (int)plan.items.size();
   int maxpos = 0;
