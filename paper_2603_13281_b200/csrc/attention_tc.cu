@@ -3,48 +3,67 @@
 // heads of `block_forward` decode (src/model.py:495-501): scores = (q . k) * 1/sqrt(hd) with
 // the causal mask, softmax, weights @ V -- per (row, head), batch-invariant.
 //
-// One CTA = one work item (a chunk of <= MAXP pages at fixed absolute positions, shared by
-// every sequence whose block table maps the same physical pages) x one KV head. The up to 128
-// query entries (row, head-in-group) attached to those pages -- the encoder and decoder heads
-// of every model sharing the prefix -- are the M = 128 rows of two tcgen05 MMAs:
-//   S[128 x 16P]  = Q[128 x 128] . K[16P x 128]^T      (K-major Q and K, fp32 in TMEM)
-//   softmax       : one epilogue thread per entry reads its S row from TMEM (exp2 domain,
-//                   causal mask), writes P as bf16 into the SW128 K-major layout over the
-//                   now-dead K buffer
-//   O[128 x 128]  = P[128 x 16P] . V[16P x 128]         (V consumed MN-major, straight from
-//                                                        the TMA-written pages)
-// and the unnormalised partial (O, m, l) per (row, head, chunk) goes to the same fixed-order
-// merge kernel as the mma.sync path. Each K/V page is staged in shared memory once per KV
-// head for all entries: HBM bytes scale with context, not with the number of models.
+// One CTA = one work item x one KV head. A work item is a chunk of pages at fixed absolute
+// positions shared by every sequence whose block table maps the same physical pages; its up to
+// 128 query entries (row, head-in-group) -- the encoder and decoder heads of every model
+// sharing the prefix -- are the M = 128 rows of the tcgen05 MMAs. The chunk is streamed in
+// sub-chunks of SUBP = 8 pages (128 keys) through a 2-stage TMA ring:
+//   S_j[128 x 128] = Q . K_j^T            (K-major Q and K; fp32, double-buffered in TMEM)
+//   softmax        : 8 warps, two per TMEM lane quarter (each half of the key columns), exp2
+//                    domain with the causal mask; running max m, sum l per entry; P_j bf16 into
+//                    the SW128 K-major layout; O rescaled in TMEM when the max moves
+//   O[128 x 128]  += P_j . V_j              (V consumed MN-major straight from the pages)
+// so S_{j+1}, the loads of sub-chunk j+2 and the softmax of j overlap. The unnormalised
+// partial (O, m, l) per (row, head, chunk) goes to the fixed-order merge kernel. Each K/V page
+// is staged in shared memory once per KV head for all entries: HBM bytes scale with context,
+// not with the number of models. Sub-chunk boundaries sit at fixed offsets from the chunk's
+// absolute start, so a row's partial never depends on which other rows share the item.
 #include "kernels.h"
 #include "ptx.cuh"
 
 namespace icr {
 
-constexpr int TC_THREADS = 256;  // w0 TMA, w1 MMA + TMEM, w2-3 Q loaders, w4-7 softmax/epilogue
+constexpr int TC_THREADS = 384;  // w0 K TMA, w1 MMA + TMEM, w2 V TMA, w3-11 Q, w4-11 softmax
 constexpr int TC_ROWS = 128;     // MMA M: query entries per item
+constexpr int SUBP = 8;          // pages per sub-chunk (N = 128 keys per S MMA)
 
-template <int MAXP>
 struct TcLayout {
-  static constexpr uint32_t Q_BYTES = TC_ROWS * 256;            // 2 K-blocks x [128 x 128 B]
-  static constexpr uint32_t HALF = MAXP * 16 * 128;             // one 64-dim half of K or V
-  static constexpr uint32_t KV_BYTES = 2 * HALF;
-  static constexpr uint32_t Q_OFF = 0, K_OFF = Q_BYTES, V_OFF = K_OFF + KV_BYTES;
-  static constexpr uint32_t BAR_OFF = V_OFF + KV_BYTES;
-  static constexpr size_t SMEM = 1024 + BAR_OFF + 64 + 2 * 128 * 4;
-  static constexpr uint32_t S_COLS = MAXP * 16;
-  static constexpr uint32_t TMEM_COLS = (S_COLS + 128) <= 256 ? 256 : 512;
+  static constexpr uint32_t Q_OFF = 0;                     // 2 K-blocks x [128 rows x 128 B]
+  static constexpr uint32_t P_OFF = 32768;                 // [2 buffers][2 K-blocks][128 x 128 B]
+  static constexpr uint32_t P_BYTES = 32768;
+  static constexpr uint32_t HALF = SUBP * 16 * 128;        // 16 KB: one 64-dim half, 128 keys
+  static constexpr uint32_t STAGE0 = P_OFF + 2 * P_BYTES;  // stage s: K halves, then V halves
+  static constexpr uint32_t STAGE_BYTES = 4 * HALF;        // 64 KB
+  static constexpr uint32_t BAR_OFF = STAGE0 + 2 * STAGE_BYTES;
+  static constexpr uint32_t RED_OFF = BAR_OFF + 128;       // float [2 halves][128]
+  // 230,528 B: within the opt-in maximum of 232,448 less the 1 KB the driver reserves
+  static constexpr size_t SMEM = RED_OFF + 256 * 4;
+  static constexpr uint32_t TMEM_COLS = 512;               // S0 [0,128) S1 [128,256) O [256,384)
 };
 
-// MN-major, 128-byte-swizzle shared-memory descriptor (B operand of P.V): 64 consecutive
-// N elements (one 128-byte row) per K index, 8 K rows per 1024-byte atom; SBO = bytes
-// between 8-row K groups, LBO = bytes between 64-element N blocks.
+// 2^x on the FMA / integer pipes (FA4-style split of the exponentials between the SFU and
+// the FMA units): round-to-nearest split x = i + f with the 1.5 * 2^23 magic constant (no
+// F2I / FRND, which would go through the SFU pipe), cubic minimax for 2^f on [-1/2, 1/2]
+// (max rel. error 1.0e-4, below the bf16 rounding P gets next), exponent added as an
+// integer. Valid for -126 <= x <= 8 (x is clamped below; P <= 256 above).
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = x + 12582912.f;           // 1.5 * 2^23: round(x) lands in the low mantissa bits
+  const float fi = t - 12582912.f;
+  const float f = x - fi;                   // [-1/2, 1/2]
+  const float p = fmaf(f, fmaf(f, fmaf(f, 0.05500831f, 0.24220971f), 0.69328286f), 1.0f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 
+// MN-major, 128-byte-swizzle shared-memory descriptor (B operand of P.V): 64 consecutive
+// N elements (one 128-byte row) per K index, 8 K rows per 1024-byte atom; SBO = bytes
+// between 8-row K groups, LBO = bytes between 64-element N blocks.
 __device__ __forceinline__ uint64_t sdesc_mnmajor_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);
@@ -55,8 +74,18 @@ __device__ __forceinline__ uint64_t sdesc_mnmajor_sw128(uint32_t saddr, uint32_t
   return d;
 }
 
-template <int MAXP>
-__global__ void __launch_bounds__(TC_THREADS, MAXP <= 8 ? 2 : 1)
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16};\n" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+
+static_assert(TcLayout::SMEM <= 232448 - 1024, "exceeds the per-block shared memory limit");
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                    const __nv_bfloat16* __restrict__ q, int q_ld, int num_kv_heads, int group,
                    const AttnItem* __restrict__ items, const int* __restrict__ item_pages,
@@ -64,95 +93,149 @@ __global__ void __launch_bounds__(TC_THREADS, MAXP <= 8 ? 2 : 1)
                    int num_heads, int max_chunks, float scale, float* __restrict__ part_o,
                    float2* __restrict__ part_ml, const int* __restrict__ n_items_dev,
                    unsigned long long* __restrict__ trace) {
-  using L = TcLayout<MAXP>;
-  extern __shared__ uint8_t tc_smem_raw[];
-  uint8_t* smem = tc_smem_raw + ((1024 - (smem_u32(tc_smem_raw) & 1023)) & 1023);
+  using L = TcLayout;
+  extern __shared__ __align__(1024) uint8_t tc_smem[];
+  uint8_t* smem = tc_smem;  // no static shared memory: the dynamic window starts 1024-aligned
   uint8_t* sQ = smem + L::Q_OFF;
-  uint8_t* sK = smem + L::K_OFF;  // becomes P after the S MMA has read it
-  uint8_t* sV = smem + L::V_OFF;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
   uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;
-  uint64_t* v_full = bars + 2;
-  uint64_t* s_full = bars + 3;
-  uint64_t* o_full = bars + 5;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6);
+  uint64_t* kv_full = bars + 1;   // [2] K landed
+  uint64_t* kv_empty = bars + 3;  // [2] K consumed by S
+  uint64_t* v_full = bars + 12;   // [2] V landed
+  uint64_t* v_empty = bars + 14;  // [2] V consumed by P.V
+  uint64_t* s_full = bars + 5;    // [2]
+  uint64_t* p_full = bars + 7;
+  uint64_t* o_done = bars + 8;
+  uint64_t* p_free = bars + 9;    // [2]: P buffer b consumed by its P.V
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
+  float* red = reinterpret_cast<float*>(smem + L::RED_OFF);
 
   const int cta_id = blockIdx.y * gridDim.x + blockIdx.x;
   auto stamp = [&](int k) {
     if (trace != nullptr && cta_id < 4096) trace[(size_t)cta_id * 16 + k] = globaltimer();
   };
+  // per-sub-chunk timeline of CTA 0 (diagnostic): [j][0 K issued, 1 S done, 2 P written, 3 PV issued]
+  auto sstamp = [&](int j, int k) {
+    if (trace != nullptr && cta_id == 0 && j < 256) trace[(size_t)2 * 4096 * 16 + j * 8 + k] = globaltimer();
+  };
   if (threadIdx.x == 0) stamp(6);
+  if ((smem_u32(tc_smem) & 1023) != 0) __trap();  // SW128 tiles need a 1024-byte base
   pdl_launch();
   const int item_id = blockIdx.x;
   if (item_id >= *n_items_dev) return;
   const int warp = warp_id(), lane = lane_id();
   if (threadIdx.x == 0) {
-    mbar_init(q_full, 192);
-    mbar_init(k_full, 1);
-    mbar_init(v_full, 1);
-    mbar_init(s_full, 1);
-    mbar_init(o_full, 1);
+    mbar_init(q_full, 288);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&kv_full[b], 1);
+      mbar_init(&kv_empty[b], 1);
+      mbar_init(&v_full[b], 1);
+      mbar_init(&v_empty[b], 1);
+      mbar_init(&s_full[b], 1);
+    }
+    mbar_init(p_full, 256);
+    mbar_init(o_done, 1);
+    mbar_init(&p_free[0], 1);
+    mbar_init(&p_free[1], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<L::TMEM_COLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_s = *tmem_slot;
-  const uint32_t tmem_o = tmem_s + L::S_COLS;
+  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_o = tmem_base + 256;
   const AttnItem it = items[item_id];  // uploaded before the forward
   const int g = blockIdx.y;
   const int np = it.n_pages;
+  const int nsub = (np + SUBP - 1) / SUBP;
 
-  if (warp == 0) {
-    // ---------------- producer: K and V pages of this KV head ----------------
+  if (warp == 0 || warp == 2) {
+    // ---------------- producers: K (warp 0) and V (warp 2) rings, decoupled: a K stage is
+    // free once S has read it, a V stage only after P.V -- K runs ahead of the softmax ------
+    const bool is_k = warp == 0;
     if (elect_one()) {
-      tma_prefetch_desc(&tm_k);
-      tma_prefetch_desc(&tm_v);
-      mbar_expect_tx(k_full, (uint32_t)np * 2 * 2048);
-      mbar_expect_tx(v_full, (uint32_t)np * 2 * 2048);
+      const CUtensorMap* tm = is_k ? &tm_k : &tm_v;
+      uint64_t* full = is_k ? kv_full : v_full;
+      uint64_t* empty = is_k ? kv_empty : v_empty;
+      tma_prefetch_desc(tm);
       const int pre = it.n_pre;  // pages no kernel of this forward writes
-      for (int pi = 0; pi < np; ++pi) {
-        if (pi == pre) {
-          pdl_wait();
-          stamp(7);
-        }
-        const int plane = item_pages[it.page_off + pi] * num_kv_heads + g;
+      bool waited = false;
+      for (int j = 0; j < nsub; ++j) {
+        const int b = j & 1;
+        if (j >= 2) mbar_wait(&empty[b], ((j >> 1) - 1) & 1);
+        const int p0 = j * SUBP, pn = min(SUBP, np - p0);
+        uint8_t* st = smem + L::STAGE0 + b * L::STAGE_BYTES + (is_k ? 0 : 2 * L::HALF);
+        mbar_expect_tx(&full[b], (uint32_t)pn * 2 * 2048);
+        for (int pi = 0; pi < pn; ++pi) {
+          if (!waited && p0 + pi >= pre) {
+            pdl_wait();
+            if (is_k) stamp(7);
+            waited = true;
+          }
+          const int plane = item_pages[it.page_off + p0 + pi] * num_kv_heads + g;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          tma_load_3d(sK + h * L::HALF + pi * 2048, &tm_k, k_full, h * 64, 0, plane);
-          tma_load_3d(sV + h * L::HALF + pi * 2048, &tm_v, v_full, h * 64, 0, plane);
+          for (int h = 0; h < 2; ++h) tma_load_3d(st + h * L::HALF + pi * 2048, tm, &full[b], h * 64, 0, plane);
         }
+        if (is_k) sstamp(j, 0);
       }
-      if (np <= pre) pdl_wait();
+      if (!waited) pdl_wait();
     }
     __syncwarp();
   } else if (warp == 1) {
-    // ---------------- S = Q K^T ----------------
+    // ---------------- MMA issuer ----------------
     mbar_wait(q_full, 0);
-    if (lane == 0) stamp(1);
-    mbar_wait(k_full, 0);
-    if (lane == 0) stamp(2);
     tc_fence_after();
-    if (elect_one()) {
-      const uint32_t idesc_s = idesc_bf16_f32(TC_ROWS, (uint32_t)np * 16);
+    auto issue_s = [&](int j) {
+      const int b = j & 1;
+      mbar_wait(&kv_full[b], (j >> 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const int keys = min(SUBP, np - j * SUBP) * 16;
+        const uint32_t idesc_s = idesc_bf16_f32(TC_ROWS, (uint32_t)keys);
+        const uint32_t kb = smem_u32(smem + L::STAGE0 + b * L::STAGE_BYTES);
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        const uint32_t a = smem_u32(sQ) + (kk >> 2) * (TC_ROWS * 128) + (kk & 3) * 32;
-        const uint32_t b = smem_u32(sK) + (kk >> 2) * L::HALF + (kk & 3) * 32;
-        tc_mma_bf16(tmem_s, sdesc_kmajor_sw128(a), sdesc_kmajor_sw128(b), idesc_s, kk > 0 ? 1u : 0u);
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t a = smem_u32(sQ) + (kk >> 2) * (TC_ROWS * 128) + (kk & 3) * 32;
+          const uint32_t bb = kb + (kk >> 2) * L::HALF + (kk & 3) * 32;
+          tc_mma_bf16(tmem_base + b * 128, sdesc_kmajor_sw128(a), sdesc_kmajor_sw128(bb), idesc_s,
+                      kk > 0 ? 1u : 0u);
+        }
+        tc_commit(&s_full[b]);
+        tc_commit(&kv_empty[b]);
       }
-      tc_commit(s_full);
+      __syncwarp();
+    };
+    issue_s(0);
+    for (int j = 0; j < nsub; ++j) {
+      if (j + 1 < nsub) issue_s(j + 1);
+      mbar_wait(p_full, j & 1);  // softmax j wrote P and rescaled O
+      mbar_wait(&v_full[j & 1], (j >> 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const int pn = min(SUBP, np - j * SUBP);
+        const uint32_t idesc_o = idesc_bf16_f32(TC_ROWS, 128) | (1u << 16);  // B (V) MN-major
+        const uint32_t vb = smem_u32(smem + L::STAGE0 + (j & 1) * L::STAGE_BYTES) + 2 * L::HALF;
+        const uint32_t pb = smem_u32(smem + L::P_OFF + (j & 1) * L::P_BYTES);
+        for (int kk = 0; kk < pn; ++kk) {  // 16 keys (one page) per instruction
+          const uint32_t a = pb + (kk >> 2) * (TC_ROWS * 128) + (kk & 3) * 32;
+          tc_mma_bf16(tmem_o, sdesc_kmajor_sw128(a), sdesc_mnmajor_sw128(vb + kk * 2048, L::HALF, 1024),
+                      idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        sstamp(j, 3);
+        tc_commit(o_done);
+        tc_commit(&p_free[j & 1]);
+        tc_commit(&v_empty[j & 1]);
+      }
+      __syncwarp();
     }
-    __syncwarp();
   } else {
-    // ---------------- Q gather (warps 2-7) ----------------
+    // ---------------- Q gather (warps 3-11) ----------------
     pdl_wait();  // q comes from the q/k/v GEMM
-    const int t = threadIdx.x - 64;  // 0..191
-    // entry e sits in M row / TMEM lane r(e) = (e % 4) * 32 + e / 4, so the entries of a
-    // partly filled item spread over all four lane quarters
-    for (int idx = t; idx < TC_ROWS * 16; idx += 192) {
+    const int t = threadIdx.x - 96;  // 0..287
+    // entry e sits in M row / TMEM lane r(e) = (e % 4) * 32 + e / 4: the entries of a partly
+    // filled item spread over all four lane quarters
+    for (int idx = t; idx < TC_ROWS * 16; idx += 288) {
       const int e = idx >> 4, c = idx & 15;
       const int r = (e & 3) * 32 + (e >> 2);
       uint4 val = make_uint4(0, 0, 0, 0);
@@ -162,159 +245,194 @@ __global__ void __launch_bounds__(TC_THREADS, MAXP <= 8 ? 2 : 1)
       }
       *reinterpret_cast<uint4*>(sQ + (c >> 3) * (TC_ROWS * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4)) = val;
     }
+    // P rows of padding entries stay zero for the whole item (the softmax skips them)
+    for (int idx = t; idx < TC_ROWS * 2 * 2 * 8; idx += 288) {
+      const int r = idx & 127, chunk = idx >> 7;  // chunk: buffer (2) x K-block (2) x 16 B (8)
+      const int e = (r & 31) * 4 + (r >> 5);
+      if (e >= it.n_rows)
+        *reinterpret_cast<uint4*>(smem + L::P_OFF + (chunk >> 3) * (TC_ROWS * 128) + r * 128 + (chunk & 7) * 16) =
+            make_uint4(0, 0, 0, 0);
+    }
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     mbar_arrive(q_full);
-  }
+    if (lane == 0 && warp == 3) stamp(1);
 
-  // ---------------- softmax on all 8 warps ----------------
-  // TMEM lane quarter w % 4 is readable by warps w and w + 4: each row's key columns are split
-  // between the two (16-column groups [0, h) and [h, np)); row max and sum are combined through
-  // shared memory in a fixed order.
-  float* red = reinterpret_cast<float*>(bars + 8);  // [2][128] partial max, then partial sum
-  const int r = (warp & 3) * 32 + lane;             // TMEM lane = M row
-  const int e = (r & 31) * 4 + (r >> 5);            // the query entry held in that row
-  const int half = warp >> 2;
-  const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
-  const bool valid = e < it.n_rows;
-  int2 rr = make_int2(0, 0);
-  int pos = -1;
-  if (valid) {
-    rr = item_rows[it.row_off + e];
-    pos = row_pos[rr.x];
-  }
-  const float sl2 = scale * 1.4426950408889634f;
-  const int hsplit = (np + 1) >> 1;
-  const int c_lo = half == 0 ? 0 : hsplit * 16, c_hi = half == 0 ? hsplit * 16 : np * 16;
-  mbar_wait(s_full, 0);
-  tc_fence_after();
-  if (r == 0 && half == 1) stamp(3);
-  float m = -INFINITY;
-  for (int c0 = c_lo; c0 < c_hi; c0 += 64) {
-    uint32_t v[4][16];
-#pragma unroll
-    for (int q4 = 0; q4 < 4; ++q4)
-      if (c0 + q4 * 16 < c_hi) tmem_ld16_nowait(tmem_s + lane_base + c0 + q4 * 16, v[q4]);
-    tmem_wait_ld();
-#pragma unroll
-    for (int q4 = 0; q4 < 4; ++q4) {
-      tmem_reg_fence(v[q4]);
-      if (c0 + q4 * 16 < c_hi) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j)
-          if (it.chunk_start + c0 + q4 * 16 + j <= pos) m = fmaxf(m, __fmul_rn(__uint_as_float(v[q4][j]), sl2));
+    if (warp >= 4) {
+      // ---------------- softmax: warps w and w + 4 (same SM sub-partition, same TMEM lane
+      // quarter w % 4) split each row's 128 key columns; the row max and sum are exchanged
+      // through shared memory under a 64-thread barrier per quarter ------------------------
+      const int sw = warp - 4;                       // 0..7
+      const int quarter = sw & 3, half = sw >> 2;    // key columns [64 half, 64 half + 64)
+      const int r = quarter * 32 + lane;             // TMEM lane = M row
+      const int e = (r & 31) * 4 + (r >> 5);         // the query entry held in that row
+      const uint32_t lane_base = (uint32_t)(32 * quarter) << 16;
+      const bool valid = e < it.n_rows;
+      int2 rr = make_int2(0, 0);
+      int pos = -1;
+      if (valid) {
+        rr = item_rows[it.row_off + e];
+        pos = row_pos[rr.x];
       }
-    }
-  }
-  red[half * 128 + r] = m;
-  named_bar_sync(1, TC_THREADS);
-  m = fmaxf(red[r], red[128 + r]);
-  named_bar_sync(1, TC_THREADS);  // red is reused for the sums
-  // P = exp2(s - m) as bf16 into the K-major SW128 layout (over the dead K buffer)
-  float l = 0.f;
-  for (int c0 = c_lo; c0 < c_hi; c0 += 64) {
-    uint32_t v[4][16];
+      const float sl2 = scale * 1.4426950408889634f;
+      float m_run = -INFINITY, l_part = 0.f;
+      for (int j = 0; j < nsub; ++j) {
+        const int b = j & 1;
+        const int keys = min(SUBP, np - j * SUBP) * 16;
+        const int kbase = it.chunk_start + j * SUBP * 16 + half * 64;
+        const int hkeys = min(64, keys - half * 64);  // this half's columns (may be <= 0)
+        mbar_wait(&s_full[b], (j >> 1) & 1);
+        tc_fence_after();
+        if (r == 0 && half == 0) sstamp(j, 1);
+        if (r == 0 && half == 0 && j == 0) stamp(2);
+        uint32_t v[4][16];  // raw q.k of this half's (<= 64) keys
 #pragma unroll
-    for (int q4 = 0; q4 < 4; ++q4)
-      if (c0 + q4 * 16 < c_hi) tmem_ld16_nowait(tmem_s + lane_base + c0 + q4 * 16, v[q4]);
-    tmem_wait_ld();
+        for (int q4 = 0; q4 < 4; ++q4)
+          if (q4 * 16 < hkeys) tmem_ld16_nowait(tmem_base + b * 128 + lane_base + half * 64 + q4 * 16, v[q4]);
+        tmem_wait_ld();
 #pragma unroll
-    for (int q4 = 0; q4 < 4; ++q4) {
-      tmem_reg_fence(v[q4]);
-      const int c = c0 + q4 * 16;
-      if (c < c_hi) {
-        uint32_t pk[8];
+        for (int q4 = 0; q4 < 4; ++q4) tmem_reg_fence(v[q4]);
+        if (r == 0 && half == 0) sstamp(j, 4);
+        // visible keys of this half: [kbase, kbase + nvis); max of raw scores x sl2 (> 0)
+        // equals the max of the scaled scores (rounding is monotonic)
+        const int nvis = valid ? max(0, min(hkeys, pos + 1 - kbase)) : 0;
+        const bool full = nvis == 64;
+        float mx = -INFINITY;
+        if (full) {
 #pragma unroll
-        for (int j = 0; j < 16; j += 2) {
-          float p0 = 0.f, p1 = 0.f;
-          if (it.chunk_start + c + j <= pos) p0 = ex2_approx(__fmul_rn(__uint_as_float(v[q4][j]), sl2) - m);
-          if (it.chunk_start + c + j + 1 <= pos) p1 = ex2_approx(__fmul_rn(__uint_as_float(v[q4][j + 1]), sl2) - m);
-          l += p0;
-          l += p1;
-          __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
-          pk[j >> 1] = *reinterpret_cast<uint32_t*>(&h2);
+          for (int q4 = 0; q4 < 4; ++q4)
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) mx = fmaxf(mx, __uint_as_float(v[q4][jj]));
+        } else if (nvis > 0) {
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4)
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj)
+              if (q4 * 16 + jj < nvis) mx = fmaxf(mx, __uint_as_float(v[q4][jj]));
         }
-        const int blk = c >> 6, ch = (c & 63) >> 3;  // 64-key block, 8-key chunk
-        uint8_t* rowp = sK + blk * (TC_ROWS * 128) + r * 128;
-        *reinterpret_cast<uint4*>(rowp + (((ch) ^ (r & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        *reinterpret_cast<uint4*>(rowp + (((ch + 1) ^ (r & 7)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-      }
-    }
-  }
-  red[half * 128 + r] = l;
-  tc_fence_before();
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-  named_bar_sync(1, TC_THREADS);
-  if (r == 0 && half == 1) stamp(4);
-
-  if (warp == 1) {
-    // ---------------- O = P V ----------------
-    mbar_wait(v_full, 0);
-    tc_fence_after();
-    if (elect_one()) {
-      const uint32_t idesc_o = idesc_bf16_f32(TC_ROWS, 128) | (1u << 16);  // B (V) MN-major
-      for (int kk = 0; kk < np; ++kk) {  // 16 keys (one page) per instruction
-        const uint32_t a = smem_u32(sK) + (kk >> 2) * (TC_ROWS * 128) + (kk & 3) * 32;
-        const uint32_t b = smem_u32(sV) + kk * 2048;
-        tc_mma_bf16(tmem_o, sdesc_kmajor_sw128(a), sdesc_mnmajor_sw128(b, L::HALF, 1024), idesc_o,
-                    kk > 0 ? 1u : 0u);
-      }
-      tc_commit(o_full);
-    }
-    __syncwarp();
-  } else if (warp >= 4) {
-    // ---------------- epilogue: unnormalised partial O and (m, l) per (row, head, chunk) ------
-    l = red[r] + red[128 + r];
-    mbar_wait(o_full, 0);
-    tc_fence_after();
-    if (r == 0) stamp(0);
-    const size_t slot = valid ? ((size_t)rr.x * num_heads + g * group + rr.y) * max_chunks + it.chunk_idx : 0;
-    float* dst = part_o + slot * 128;
-#pragma unroll 1
-    for (int c0 = 0; c0 < 128; c0 += 64) {
-      uint32_t v[4][16];
+        // exchange with the partner thread (same row, other half); the second barrier lets
+        // the buffer be rewritten next iteration
+        red[half * 128 + r] = mx;
+        named_bar_sync(1 + quarter, 64);
+        const float m_cand = fmaxf(m_run, __fmul_rn(fmaxf(red[r], red[128 + r]), sl2));
+        named_bar_sync(1 + quarter, 64);
+        // lazy max: keep the reference while the new scores stay within 2^8 of it (P <= 256
+        // is exact enough in bf16 / fp32), so O is rescaled only when the max jumps
+        const float m_new = (m_cand > m_run + 8.f) ? m_cand : m_run;
+        const float corr = (m_run == -INFINITY) ? 1.f : ex2_approx(m_run - m_new);
+        if (r == 0 && half == 0) sstamp(j, 5);
+        // P buffer b was last read by P.V(j - 2)
+        if (j >= 2) mbar_wait(&p_free[b], ((j >> 1) - 1) & 1);
+        if (j > 0 && __any_sync(0xffffffffu, valid && corr != 1.f)) {
+          // the max moved: rescale this half's 64 O columns once P.V(j - 1) has landed
+          mbar_wait(o_done, (j - 1) & 1);
+          tc_fence_after();
+          uint32_t o[4][16];
 #pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4) tmem_ld16_nowait(tmem_o + lane_base + c0 + q4 * 16, v[q4]);
+          for (int q4 = 0; q4 < 4; ++q4) tmem_ld16_nowait(tmem_o + lane_base + half * 64 + q4 * 16, o[q4]);
+          tmem_wait_ld();
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            tmem_reg_fence(o[q4]);
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) o[q4][jj] = __float_as_uint(__uint_as_float(o[q4][jj]) * corr);
+            tmem_st16(tmem_o + lane_base + half * 64 + q4 * 16, o[q4]);
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        }
+        if (r == 0 && half == 0) sstamp(j, 6);
+        const long long clk0 = clock64();
+        uint8_t* rowp0 = smem + L::P_OFF + b * L::P_BYTES + half * (TC_ROWS * 128) + r * 128;
+        float ls0 = 0.f, ls1 = 0.f;
+        if (nvis > 0) {  // padding rows, rows past their position: P stays zero
+          const float nm = -m_new;
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            if (q4 * 16 < hkeys) {
+              uint32_t pk[8];
+#pragma unroll
+              for (int jj = 0; jj < 16; jj += 2) {
+                const int c = q4 * 16 + jj;
+                // 3 of 4 keys on the SFU, 1 of 4 by polynomial on the FMA pipe: balances the
+                // two pipes (SFU: 8 cycles per warp op, polynomial: ~9 FMA-pipe ops)
+                float p0 = ex2_approx(fmaf(__uint_as_float(v[q4][jj]), sl2, nm));
+                const float x1 = fmaf(__uint_as_float(v[q4][jj + 1]), sl2, nm);
+                float p1 = (jj & 2) ? ex2_poly(x1) : ex2_approx(x1);
+                if (!full) {
+                  p0 = c < nvis ? p0 : 0.f;
+                  p1 = c + 1 < nvis ? p1 : 0.f;
+                }
+                ls0 += p0;
+                ls1 += p1;
+                __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+                pk[jj >> 1] = *reinterpret_cast<uint32_t*>(&h2);
+              }
+              const int ch = q4 * 2;  // 8-key chunk index within this half's 64-key block
+              *reinterpret_cast<uint4*>(rowp0 + ((ch ^ (r & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+              *reinterpret_cast<uint4*>(rowp0 + (((ch + 1) ^ (r & 7)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+            }
+          }
+        } else if (valid && hkeys > 0) {
+          // a valid row with no visible key in this half of the sub-chunk: zero its P
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            *reinterpret_cast<uint4*>(rowp0 + ((c ^ (r & 7)) << 4)) = make_uint4(0, 0, 0, 0);
+        }
+        l_part = l_part * corr + (ls0 + ls1);
+        m_run = m_new;
+        if (trace != nullptr && cta_id == 0 && r == 0 && half == 0 && j < 256)
+          trace[(size_t)2 * 4096 * 16 + j * 8 + 7] = (unsigned long long)(clock64() - clk0);
+        tc_fence_before();
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        mbar_arrive(p_full);
+        if (r == 0 && half == 0) sstamp(j, 2);
+      }
+      if (r == 0 && half == 0) stamp(4);
+      // ---------------- epilogue: unnormalised partial O and (m, l) ----------------
+      float* rl = red;  // free: both partners passed the last iteration's second barrier
+      rl[half * 128 + r] = l_part;
+      mbar_wait(o_done, (nsub - 1) & 1);
+      tc_fence_after();
+      if (r == 0 && half == 0) stamp(0);
+      named_bar_sync(1 + quarter, 64);
+      const float l = rl[r] + rl[128 + r];
+      const size_t slot = valid ? ((size_t)rr.x * num_heads + g * group + rr.y) * max_chunks + it.chunk_idx : 0;
+      float* dst = part_o + slot * 128 + half * 64;
+      uint32_t o[4][16];
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) tmem_ld16_nowait(tmem_o + lane_base + half * 64 + q4 * 16, o[q4]);
       tmem_wait_ld();
 #pragma unroll
       for (int q4 = 0; q4 < 4; ++q4) {
-        tmem_reg_fence(v[q4]);
+        tmem_reg_fence(o[q4]);
         if (valid) {
 #pragma unroll
-          for (int j = 0; j < 16; j += 4)
-            *reinterpret_cast<float4*>(dst + c0 + q4 * 16 + j) =
-                make_float4(__uint_as_float(v[q4][j]), __uint_as_float(v[q4][j + 1]),
-                            __uint_as_float(v[q4][j + 2]), __uint_as_float(v[q4][j + 3]));
+          for (int jj = 0; jj < 16; jj += 4)
+            *reinterpret_cast<float4*>(dst + q4 * 16 + jj) =
+                make_float4(__uint_as_float(o[q4][jj]), __uint_as_float(o[q4][jj + 1]),
+                            __uint_as_float(o[q4][jj + 2]), __uint_as_float(o[q4][jj + 3]));
         }
       }
+      if (valid && half == 0) part_ml[slot] = make_float2(m_run, l);
+      if (r == 0 && half == 0) stamp(5);
     }
-    if (valid) part_ml[slot] = make_float2(m, l);
-    if (r == 0) stamp(5);
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc<L::TMEM_COLS>(tmem_s);
+  if (warp == 1) tmem_dealloc<L::TMEM_COLS>(tmem_base);
 }
 
-template <int MAXP>
-static cudaError_t launch_tc(const AttnLaunch& a, cudaStream_t s) {
-  using L = TcLayout<MAXP>;
+cudaError_t attn_tc_partial_launch(const AttnLaunch& a, int /*chunk_pages*/, cudaStream_t s) {
+  using L = TcLayout;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<MAXP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)L::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  return launch_pdl(attn_tc_kernel<MAXP>, dim3(a.n_items_cap, a.num_kv_heads), dim3(TC_THREADS), L::SMEM, s,
+  return launch_pdl(attn_tc_kernel, dim3(a.n_items_cap, a.num_kv_heads), dim3(TC_THREADS), L::SMEM, s,
                     a.tm_k, a.tm_v, a.q, a.q_ld, a.num_kv_heads, a.group, a.items, a.item_pages,
                     a.item_rows, a.row_pos, a.num_heads, a.max_chunks, a.scale, a.part_o, a.part_ml,
                     a.n_items_dev, a.trace);
-}
-
-cudaError_t attn_tc_partial_launch(const AttnLaunch& a, int chunk_pages, cudaStream_t s) {
-  if (chunk_pages <= 8) return launch_tc<8>(a, s);
-  if (chunk_pages <= 16) return launch_tc<16>(a, s);
-  return cudaErrorInvalidValue;
 }
 
 }  // namespace icr

@@ -1423,13 +1423,21 @@ icr_status icr_bench_attention(const void* q_dev, const void* k_pages, const voi
   CUDA_TRY(cudaEventCreate(&e0));
   CUDA_TRY(cudaEventCreate(&e1));
   float total = 0.f;
+  unsigned long long* tr = nullptr;  // ICR_ATTN_TRACE=path: per-CTA + CTA-0 sub-chunk stamps
+  const char* trace_path = getenv("ICR_ATTN_TRACE");
+  if (trace_path) {
+    CUDA_TRY(cudaMalloc(&tr, (size_t)3 * 4096 * 16 * sizeof(unsigned long long)));
+    CUDA_TRY(cudaMemset(tr, 0, (size_t)3 * 4096 * 16 * sizeof(unsigned long long)));
+  }
   cudaError_t e = attn_launch(a, s);  // warm-up
   for (int it = 0; it < iters && e == cudaSuccess; ++it) {
     if (flush_dev)
       l2_flush_read_kernel<<<1184, 256, 0, s>>>((const uint4*)flush_dev, (size_t)flush_bytes / 16,
                                                 (unsigned*)flush_dev);
     cudaEventRecord(e0, s);
+    if (tr && it == iters - 1) a.trace = tr;
     e = attn_launch(a, s);
+    a.trace = nullptr;
     cudaEventRecord(e1, s);
     cudaEventSynchronize(e1);
     float ms = 0.f;
@@ -1438,6 +1446,33 @@ icr_status icr_bench_attention(const void* q_dev, const void* k_pages, const voi
   }
   *avg_ms = total / iters;
   cudaStreamSynchronize(s);
+  if (tr) {
+    std::vector<unsigned long long> h((size_t)3 * 4096 * 16);
+    cudaMemcpy(h.data(), tr, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    cudaFree(tr);
+    unsigned long long t0 = ~0ull;
+    for (size_t i = 0; i < (size_t)2 * 4096 * 16; ++i)
+      if (i % 16 < 8 && h[i] && h[i] < t0) t0 = h[i];
+    if (FILE* f = fopen(trace_path, "w")) {
+      fprintf(f, "kind,idx,s0,s1,s2,s3,s4,s5,s6,s7\n");
+      for (int k = 0; k < 2; ++k)
+        for (int c2 = 0; c2 < 4096; ++c2) {
+          const unsigned long long* r = &h[((size_t)k * 4096 + c2) * 16];
+          if (!r[6]) continue;
+          fprintf(f, "%s,%d", k ? "merge" : "partial", c2);
+          for (int q = 0; q < 8; ++q) fprintf(f, ",%.3f", r[q] ? (r[q] - t0) / 1000.0 : -1.0);
+          fprintf(f, "\n");
+        }
+      for (int j = 0; j < 256; ++j) {
+        const unsigned long long* r = &h[(size_t)2 * 4096 * 16 + j * 8];
+        if (!r[0] && !r[1]) continue;
+        fprintf(f, "sub,%d", j);
+        for (int q = 0; q < 7; ++q) fprintf(f, ",%.3f", r[q] ? (r[q] - t0) / 1000.0 : -1.0);
+        fprintf(f, ",%llu\n", (unsigned long long)r[7]);
+      }
+      fclose(f);
+    }
+  }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   void* bufs[] = {d_pos, d_kind, d_pages, d_n, d_items, d_rows, d_po, d_pml};
