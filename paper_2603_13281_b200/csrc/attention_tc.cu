@@ -235,15 +235,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int t = threadIdx.x - 96;  // 0..287
     // entry e sits in M row / TMEM lane r(e) = (e % 4) * 32 + e / 4: the entries of a partly
     // filled item spread over all four lane quarters
-    for (int idx = t; idx < TC_ROWS * 16; idx += 288) {
+    // all of a thread's loads are issued before its first store: one round trip, not eight
+    constexpr int QPT = (TC_ROWS * 16 + 287) / 288;  // 16-byte chunks per thread
+    uint4 qv[QPT];
+#pragma unroll
+    for (int k = 0; k < QPT; ++k) {
+      const int idx = t + k * 288;
       const int e = idx >> 4, c = idx & 15;
-      const int r = (e & 3) * 32 + (e >> 2);
-      uint4 val = make_uint4(0, 0, 0, 0);
-      if (e < it.n_rows) {
+      qv[k] = make_uint4(0, 0, 0, 0);
+      if (idx < TC_ROWS * 16 && e < it.n_rows) {
         const int2 rr = item_rows[it.row_off + e];
-        val = *reinterpret_cast<const uint4*>(q + (size_t)rr.x * q_ld + (g * group + rr.y) * 128 + c * 8);
+        qv[k] = __ldg(reinterpret_cast<const uint4*>(q + (size_t)rr.x * q_ld + (g * group + rr.y) * 128 + c * 8));
       }
-      *reinterpret_cast<uint4*>(sQ + (c >> 3) * (TC_ROWS * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4)) = val;
+    }
+#pragma unroll
+    for (int k = 0; k < QPT; ++k) {
+      const int idx = t + k * 288;
+      if (idx < TC_ROWS * 16) {
+        const int e = idx >> 4, c = idx & 15;
+        const int r = (e & 3) * 32 + (e >> 2);
+        *reinterpret_cast<uint4*>(sQ + (c >> 3) * (TC_ROWS * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4)) = qv[k];
+      }
     }
     // P rows of padding entries stay zero for the whole item (the softmax skips them)
     for (int idx = t; idx < TC_ROWS * 2 * 2 * 8; idx += 288) {

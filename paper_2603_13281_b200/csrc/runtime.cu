@@ -195,7 +195,17 @@ static icr_status build_attn_plan(int n_rows, const int* kind, const int* seq, c
       }
     }
   }
-  for (const Group& gr : groups) {
+  // longest work first: with more CTAs than SMs the short private tails fill in behind the
+  // long shared chunks instead of pushing one of them into a second wave (item order does not
+  // affect any result: partials are indexed by (row, head, chunk))
+  std::vector<int> order(groups.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    const size_t wa = groups[a].pages.size() * groups[a].seqs.size(), wb = groups[b].pages.size() * groups[b].seqs.size();
+    return groups[a].pages.size() != groups[b].pages.size() ? groups[a].pages.size() > groups[b].pages.size() : wa > wb;
+  });
+  for (int gi : order) {
+    const Group& gr = groups[gi];
     const int c0 = gr.c * CT, c1 = (gr.c + 1) * CT - 1;
     std::vector<int2> entries;
     std::vector<int> entry_pos;
