@@ -277,6 +277,19 @@ def run_b200(args) -> None:
         traffic = prof.get("dram_bytes_per_launch")
     except Exception:
         pass
+    # ---------------- C4: long-context shared-KV attention (BASELINE.json configs[3]) ----------
+    attn_c4 = None
+    if not args.no_attention:
+        try:
+            from tools.attn_sweep import run as attn_run
+            r4 = attn_run(32768, N_ADAPTERS, 128)
+            attn_c4 = {"kernel": "attn_tc_kernel (tcgen05) + attn_merge_kernel",
+                       "context": 32768, "adapters": N_ADAPTERS, "chunk_pages": 128,
+                       "us": r4["ms"] * 1e3, "unique_kv_bytes": r4["unique_kv_bytes"],
+                       "achieved_gbs": r4["gbs"], "frac": r4["gbs"] / float(peaks.get("hbm_gbs", 6650.0)),
+                       "l2": "flushed between launches (256 MB read)"}
+        except Exception as exc:  # the C4 line is informative; never fail the bench on it
+            attn_c4 = {"error": str(exc)[:200]}
     step_bytes = (rt.dw.nbytes_streamed() + N_ADAPTERS * 73_400_320
                   + (PROMPT + N_ADAPTERS * (W + K // 2)) * cfg.num_layers * 2 * cfg.kv_dim * 2)
 
@@ -305,6 +318,7 @@ def run_b200(args) -> None:
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",
                      "gemm_launch_us": per_kind},
         "step_breakdown_ms": step_breakdown,
+        "attention_c4": attn_c4,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         res = cpu_baseline_sample(1, 2, 0)
@@ -329,6 +343,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-attention", action="store_true", help="skip the C4 attention line")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
