@@ -152,6 +152,8 @@ icr_status icr_profile_gemm(icr_model* m, int which, int iters, float* avg_ms, v
 /* Diagnostic: average ms of the last forward replayed as a graph with kernel kinds
  * (bit k = kind k of icr_profile_step) left out. */
 icr_status icr_profile_ablate(icr_model* m, int skip_mask, int iters, float* avg_ms, void* stream);
+/* Instrumentation: host time split of icr_forward calls [calls, prep us, launch us, wait us]. */
+icr_status icr_host_timing(double* out4, int reset);
 /* Diagnostic: per-CTA timestamps of every GEMM launch of the last forward -> CSV. */
 icr_status icr_profile_trace(icr_model* m, const char* path, void* stream);
 

@@ -24,7 +24,7 @@ _STATUS = {
 # Every symbol the header declares; tests/test_capi.py checks the library exports them.
 EXPORTED = (
     "icr_model_create", "icr_model_destroy", "icr_forward", "icr_decode_loop",
-    "icr_model_stats", "icr_profile_step", "icr_profile_gemm", "icr_profile_ablate", "icr_profile_trace", "icr_bench_gemm",
+    "icr_model_stats", "icr_profile_step", "icr_profile_gemm", "icr_profile_ablate", "icr_profile_trace", "icr_host_timing", "icr_bench_gemm",
     "icr_bench_attention", "icr_gemm_bf16", "icr_paged_attention",
     "icr_last_error", "icr_abi_version", "icr_num_sms",
 )
@@ -73,6 +73,7 @@ def load():
         "icr_profile_gemm": [p, i, i, C.POINTER(C.c_float), p],
         "icr_profile_ablate": [p, i, i, C.POINTER(C.c_float), p],
         "icr_profile_trace": [p, C.c_char_p, p],
+        "icr_host_timing": [C.POINTER(C.c_double), i],
         "icr_profile_step": [p, C.POINTER(C.c_float), p],
         "icr_bench_gemm": [p, p, i, i, i, i, i, i, i, i, i, C.POINTER(C.c_float), p],
         "icr_gemm_bf16": [p, p, p, i, i, i, p],

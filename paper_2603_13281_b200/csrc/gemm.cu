@@ -651,6 +651,25 @@ __global__ void __launch_bounds__(256, 1)
       rm.inv[n] = inv;
     }
     named_bar_sync(1, 128);
+    if (p.touch) {
+      // warm the translations of everything the tail touches (stream-K partials of the
+      // segments sharing this CTA's tiles, residual rows, sums-of-squares, tile counters)
+      // while the weights stream: diagnostic switch ICR_TOUCH=1
+      int acc = 0;
+      if (ep_t < 32) {
+        const int tt = ep_t < 16 ? t_first : t_last;
+        const long long tb = (long long)tt * sp.Ut;
+        const int cf = sp.owner(tb), cl = sp.owner(tb + sp.Ut - 1);
+        const int cs = cf + (ep_t & 15);
+        if (cs <= cl) acc += __float_as_int(__ldcg(p.ws + (((size_t)cs * 2) * BM) * NT));
+        if (ep_t == 0) acc += __ldcg(p.counters + tt);
+        if (p.resid && ep_t == 1) acc += __float_as_int(__ldcg(p.resid + (size_t)p.row0 * p.M + tt * BM));
+        if (p.resid_bf16 && ep_t == 2) acc += (int)__ldcg(reinterpret_cast<const unsigned short*>(p.resid_bf16) + (size_t)p.row0 * p.M + tt * BM);
+        if (p.out_ssq && ep_t == 3) acc += __float_as_int(__ldcg(p.out_ssq + (size_t)tt * p.ss_stride));
+        if (p.out_bf16 && ep_t == 4) acc += (int)__ldcg(reinterpret_cast<const unsigned short*>(p.out_bf16) + (size_t)p.row0 * p.q_dim);
+      }
+      if (acc == 0x7fffffff) p.counters[0] = acc;  // keeps the loads alive
+    }
     if (p.sh_x != nullptr) {
       // the epilogue warps are idle until the first tile drains: help with the shrink so U
       // is ready long before any LoRA chunk is streamed (latency under full HBM load)

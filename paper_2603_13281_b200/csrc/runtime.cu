@@ -18,6 +18,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <chrono>
 #include <map>
 #include <string>
 #include <vector>
@@ -509,6 +510,7 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
   base.w_blocked = 1;
   if (const char* e = getenv("ICR_PREISSUE")) base.preissue_cap = atoi(e);
   if (const char* e = getenv("ICR_STAGES")) base.stages = atoi(e);
+  if (const char* e = getenv("ICR_TOUCH")) base.touch = atoi(e);
   base.ws = m->ws;
   base.counters = m->counters;
   base.rank = c.lora_rank;
@@ -920,9 +922,25 @@ icr_status icr_model_destroy(icr_model* m) {
 
 static int plan_group(icr_model* m) { return m->group; }
 
+// Host-side time split of icr_forward (instrumentation): [calls, validate+plan+pack us,
+// upload+graph launch us, wait-for-device us].
+static double g_fwd_time[4] = {0, 0, 0, 0};
+static double now_us() {
+  return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+icr_status icr_host_timing(double* out4, int reset) {
+  if (out4)
+    for (int i = 0; i < 4; ++i) out4[i] = g_fwd_time[i];
+  if (reset)
+    for (int i = 0; i < 4; ++i) g_fwd_time[i] = 0;
+  return ICR_OK;
+}
+
 icr_status icr_forward(icr_model* m, const icr_batch* b, int32_t* out_tokens_host,
                        float* logits_dev, void* stream) {
   if (!m || !b) return fail(ICR_CONFIG, "null argument");
+  const double t0 = now_us();
   cudaStream_t s = (cudaStream_t)stream;
   icr_status st = validate_batch(m, b, b->row_pos);
   if (st) return st;
@@ -935,10 +953,12 @@ icr_status icr_forward(icr_model* m, const icr_batch* b, int32_t* out_tokens_hos
   if ((st = ensure_meta(m, mt.total))) return st;
   CUDA_TRY(cudaEventSynchronize(m->staging_ev[0]));
   if ((st = pack_meta(m, b, b->row_pos, nullptr, plan, m->staging[0], mt))) return st;
+  const double t1 = now_us();
   CUDA_TRY(cudaMemcpyAsync(m->meta_dev, m->staging[0], mt.used * sizeof(int), cudaMemcpyHostToDevice, s));
   CUDA_TRY(cudaEventRecord(m->staging_ev[0], s));
   m->last_meta_bytes = (long long)mt.used * sizeof(int);
   if ((st = run_forward(m, mt, logits_dev, s))) return st;
+  const double t2 = now_us();
   if (mt.n_lm > 0 && out_tokens_host) {
     int* pin = m->staging[1];
     CUDA_TRY(cudaEventSynchronize(m->staging_ev[1]));
@@ -948,6 +968,11 @@ icr_status icr_forward(icr_model* m, const icr_batch* b, int32_t* out_tokens_hos
   } else {
     CUDA_TRY(cudaStreamSynchronize(s));
   }
+  const double t3 = now_us();
+  g_fwd_time[0] += 1;
+  g_fwd_time[1] += t1 - t0;
+  g_fwd_time[2] += t2 - t1;
+  g_fwd_time[3] += t3 - t2;
   return ICR_OK;
 }
 
