@@ -120,3 +120,56 @@ def test_paged_attention_matches_torch_and_sharing_is_bitwise(cuda, hd, H, Hkv):
                                Hkv, hd, chunk_pages=4)
     assert n_items2 > n_items  # sharing really merged work items
     assert torch.equal(got, got2)
+
+
+@pytest.mark.parametrize("chunk_pages", [4, 8, 16, 32, 128])
+def test_tc_attention_chunkings_match_torch(cuda, chunk_pages):
+    """tcgen05 attention (head_dim 128) over 1..16 pipelined 8-page sub-chunks per item,
+    partial last sub-chunks, private tails and a shared prefix, at every chunking the
+    runtime exposes (chunk_pages is a deployment knob: 16 for decode, 128 for long context)."""
+    import torch
+    g = torch.Generator(device="cpu").manual_seed(7 + chunk_pages)
+    H, Hkv, hd = 32, 8, 128
+    shared = 45  # 720-token shared prefix: not a multiple of any sub-chunk
+    n_pages = shared + 16
+    kp = torch.randn(n_pages, Hkv, 16, hd, generator=g).to(torch.bfloat16)
+    vp = torch.randn(n_pages, Hkv, 16, hd, generator=g).to(torch.bfloat16)
+    n_seq = 4
+    bt = np.full((n_seq, 50), -1, np.int32)
+    for s in range(n_seq):
+        bt[s, :shared] = np.arange(shared)
+        bt[s, shared:shared + 2] = [shared + 2 * s, shared + 2 * s + 1]
+    row_seq = [s for s in range(n_seq) for _ in range(2)]
+    row_pos = [shared * 16 + 3 + s for s in range(n_seq) for _ in range(2)]
+    # a few large-magnitude queries: the running max jumps between sub-chunks (O rescale path)
+    q = torch.randn(len(row_seq), H * hd, generator=g)
+    q[1::2] *= 3.0
+    q = q.to(torch.bfloat16)
+    ref = _attention_ref(q, kp, vp, bt, row_seq, row_pos, H, Hkv, hd)
+    got, _ = _run_attn(q.to(cuda), kp.to(cuda), vp.to(cuda), bt, row_seq, row_pos, H, Hkv, hd,
+                       chunk_pages=chunk_pages)
+    err = (got.float().cpu() - ref).abs().max().item()
+    assert err < 3e-2, err
+
+
+def test_tc_attention_prefill_rows_causal_and_many_entries(cuda):
+    """Prefill-shaped work: 48 rows of one sequence at consecutive positions (causal mask
+    inside the chunk, rows sharing pages at different positions), 48 x 4 heads = 192 query
+    entries per KV head -> more than one 128-entry item per chunk."""
+    import torch
+    g = torch.Generator(device="cpu").manual_seed(11)
+    H, Hkv, hd = 32, 8, 128
+    n_pages = 12
+    kp = torch.randn(n_pages, Hkv, 16, hd, generator=g).to(torch.bfloat16)
+    vp = torch.randn(n_pages, Hkv, 16, hd, generator=g).to(torch.bfloat16)
+    bt = np.full((1, 16), -1, np.int32)
+    bt[0, :n_pages] = np.arange(n_pages)
+    row_pos = list(range(130, 178))
+    row_seq = [0] * len(row_pos)
+    q = torch.randn(len(row_seq), H * hd, generator=g).to(torch.bfloat16)
+    ref = _attention_ref(q, kp, vp, bt, row_seq, row_pos, H, Hkv, hd)
+    for chunk_pages in (8, 16):
+        got, n_items = _run_attn(q.to(cuda), kp.to(cuda), vp.to(cuda), bt, row_seq, row_pos, H, Hkv,
+                                 hd, chunk_pages=chunk_pages)
+        err = (got.float().cpu() - ref).abs().max().item()
+        assert err < 2e-2, (chunk_pages, err)
