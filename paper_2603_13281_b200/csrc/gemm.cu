@@ -310,41 +310,66 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
 // (target t, slot a, rank index j) over one K slice of <= SHRINK_SLICE elements; all of
 // a lane's loads for the slice are issued before use (one memory round trip). The warp
 // that delivers a row's last slice folds the partials in slice order (deterministic).
-constexpr int SHRINK_SLICE = 2048;  // 8 x (32 lanes x 8 bf16)
-__device__ __forceinline__ void lora_shrink_tasks(const GemmParams& p, int gwarp, int nwarps,
-                                                  int lane, const int* s_off, const int* s_rows) {
+// A task = one adapter row (target t, slot a, rank index j) over one K slice of SL elements
+// (SL = 4096 when K fits: no cross-warp combine at all). The A slice of a warp's first task is
+// loaded before griddepcontrol.wait (adapters do not depend on the previous kernel), so only
+// the activation round trip remains on the critical path.
+template <int SL>
+struct ShrinkTask {
+  static constexpr int NI = SL / 256;  // uint4 per lane
+  uint4 a[NI];
+};
+
+template <int SL>
+__device__ __forceinline__ int shrink_tasks_total(const GemmParams& p) {
+  return p.sh_targets * p.slots * p.rank * ((p.sh_K + SL - 1) / SL);
+}
+
+template <int SL>
+__device__ __forceinline__ void shrink_load_a(const GemmParams& p, int task, int lane, ShrinkTask<SL>& st) {
+  const int splits = (p.sh_K + SL - 1) / SL;
   const int per_t = p.slots * p.rank;
-  const int splits = (p.sh_K + SHRINK_SLICE - 1) / SHRINK_SLICE;
+  const int ks = task % splits, combo = task / splits;
+  const int t = combo / per_t, rem = combo % per_t;
+  const int a = rem / p.rank, j = rem % p.rank;
+  const __nv_bfloat16* A = (t == 0 ? p.sh_a0 : p.sh_a1) + ((size_t)a * p.rank + j) * p.sh_K;
+#pragma unroll
+  for (int i = 0; i < ShrinkTask<SL>::NI; ++i) {
+    const int k = ks * SL + i * 256 + lane * 8;
+    st.a[i] = k < p.sh_K ? __ldg(reinterpret_cast<const uint4*>(A + k)) : make_uint4(0, 0, 0, 0);
+  }
+}
+
+template <int SL>
+__device__ __forceinline__ void lora_shrink_tasks(const GemmParams& p, int gwarp, int nwarps, int lane,
+                                                  const int* s_off, const int* s_rows, ShrinkTask<SL>& st) {
+  constexpr int NI = ShrinkTask<SL>::NI;
+  const int per_t = p.slots * p.rank;
+  const int splits = (p.sh_K + SL - 1) / SL;
   const int tasks = p.sh_targets * per_t * splits;
   for (int task = gwarp; task < tasks; task += nwarps) {
     const int ks = task % splits, combo = task / splits;
     const int t = combo / per_t, rem = combo % per_t;
     const int a = rem / p.rank, j = rem % p.rank;
     const int r0 = s_off[a], r1 = s_off[a + 1];
+    if (task != gwarp) shrink_load_a<SL>(p, task, lane, st);  // the first was preloaded
     if (r0 == r1) continue;
-    const int k0 = ks * SHRINK_SLICE;
-    const __nv_bfloat16* A = (t == 0 ? p.sh_a0 : p.sh_a1) + ((size_t)a * p.rank + j) * p.sh_K;
-    uint4 araw[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int k = k0 + i * 256 + lane * 8;
-      araw[i] = k < p.sh_K ? __ldg(reinterpret_cast<const uint4*>(A + k)) : make_uint4(0, 0, 0, 0);
-    }
+    const int k0 = ks * SL;
     for (int rr = r0; rr < r1; ++rr) {
       const int gr = s_rows[rr];
       if (gr < p.row0 || gr >= p.row0 + p.n_rows) continue;
-      uint4 xraw[8];
+      uint4 xraw[NI];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < NI; ++i) {
         const int k = k0 + i * 256 + lane * 8;
         xraw[i] = k < p.sh_K ? *reinterpret_cast<const uint4*>(p.sh_x + (size_t)gr * p.sh_ld + k)
                              : make_uint4(0, 0, 0, 0);
       }
       float acc = 0.f;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < NI; ++i) {
         float af[8], xf[8];
-        unpack8(araw[i], af);
+        unpack8(st.a[i], af);
         unpack8(xraw[i], xf);
 #pragma unroll
         for (int e = 0; e < 8; ++e) acc = fmaf(xf[e], af[e], acc);
@@ -378,6 +403,17 @@ __device__ __forceinline__ void lora_shrink_tasks(const GemmParams& p, int gwarp
       }
     }
   }
+}
+
+// The shrink of one warp: A of its first task preloaded before the PDL wait, then the tasks.
+// SL = 4096 for K <= 4096 (q, o, gate|up: one slice, no combine), 2048 otherwise (down).
+template <int SL>
+__device__ __forceinline__ void shrink_warp(const GemmParams& p, int gwarp, int nwarps, int lane,
+                                            const int* s_off, const int* s_rows, bool wait_first) {
+  ShrinkTask<SL> st;
+  if (gwarp < shrink_tasks_total<SL>(p)) shrink_load_a<SL>(p, gwarp, lane, st);
+  if (wait_first) pdl_wait();
+  lora_shrink_tasks<SL>(p, gwarp, nwarps, lane, s_off, s_rows, st);
 }
 
 template <int NT>
@@ -600,9 +636,9 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp == 2 || warp == 3) {
     // ---------------- LoRA shrink (SGMV) on the two otherwise idle warps ----------------
     if (p.sh_x != nullptr) {
-      pdl_wait();
       const int lane = lane_id();
-      // stage the SGMV segment table (adapter slot -> decoder rows) in smem once
+      // stage the SGMV segment table (adapter slot -> decoder rows) in smem once; it is part
+      // of the metadata uploaded before the forward, so it is read before the PDL wait
       int* s_off = rm.kind + 5 * NT;           // after the epilogue's row metadata
       int* s_rows = s_off + (p.slots + 1);
       const int t64 = threadIdx.x - 64;        // 0..63 across warps 2-3
@@ -611,7 +647,11 @@ __global__ void __launch_bounds__(256, 1)
       const int nseg = s_off[p.slots];
       for (int i = t64; i < nseg; i += 64) s_rows[i] = p.seg_rows[i];
       named_bar_sync(2, 192);  // publish the table to the epilogue warps as well
-      lora_shrink_tasks(p, blockIdx.x * 2 + (warp - 2), gridDim.x * 6, lane, s_off, s_rows);
+      const int gw = blockIdx.x * 2 + (warp - 2);
+      if (p.sh_K <= 4096)
+        shrink_warp<4096>(p, gw, gridDim.x * 6, lane, s_off, s_rows, true);
+      else
+        shrink_warp<2048>(p, gw, gridDim.x * 6, lane, s_off, s_rows, true);
       asm volatile("fence.proxy.async.global;\n" ::: "memory");  // U is read by TMA
       __syncwarp();
       if (lane == 0) red_add_release(p.sync, 1);
@@ -651,25 +691,6 @@ __global__ void __launch_bounds__(256, 1)
       rm.inv[n] = inv;
     }
     named_bar_sync(1, 128);
-    if (p.touch) {
-      // warm the translations of everything the tail touches (stream-K partials of the
-      // segments sharing this CTA's tiles, residual rows, sums-of-squares, tile counters)
-      // while the weights stream: diagnostic switch ICR_TOUCH=1
-      int acc = 0;
-      if (ep_t < 32) {
-        const int tt = ep_t < 16 ? t_first : t_last;
-        const long long tb = (long long)tt * sp.Ut;
-        const int cf = sp.owner(tb), cl = sp.owner(tb + sp.Ut - 1);
-        const int cs = cf + (ep_t & 15);
-        if (cs <= cl) acc += __float_as_int(__ldcg(p.ws + (((size_t)cs * 2) * BM) * NT));
-        if (ep_t == 0) acc += __ldcg(p.counters + tt);
-        if (p.resid && ep_t == 1) acc += __float_as_int(__ldcg(p.resid + (size_t)p.row0 * p.M + tt * BM));
-        if (p.resid_bf16 && ep_t == 2) acc += (int)__ldcg(reinterpret_cast<const unsigned short*>(p.resid_bf16) + (size_t)p.row0 * p.M + tt * BM);
-        if (p.out_ssq && ep_t == 3) acc += __float_as_int(__ldcg(p.out_ssq + (size_t)tt * p.ss_stride));
-        if (p.out_bf16 && ep_t == 4) acc += (int)__ldcg(reinterpret_cast<const unsigned short*>(p.out_bf16) + (size_t)p.row0 * p.q_dim);
-      }
-      if (acc == 0x7fffffff) p.counters[0] = acc;  // keeps the loads alive
-    }
     if (p.sh_x != nullptr) {
       // the epilogue warps are idle until the first tile drains: help with the shrink so U
       // is ready long before any LoRA chunk is streamed (latency under full HBM load)
@@ -677,8 +698,11 @@ __global__ void __launch_bounds__(256, 1)
       const int* s_off = rm.kind + 5 * NT;
       const int* s_rows = s_off + (p.slots + 1);
       named_bar_sync(2, 192);
-      lora_shrink_tasks(p, gridDim.x * 2 + blockIdx.x * 4 + (warp - 4), gridDim.x * 6, lane, s_off,
-                        s_rows);
+      const int gw = gridDim.x * 2 + blockIdx.x * 4 + (warp - 4);
+      if (p.sh_K <= 4096)
+        shrink_warp<4096>(p, gw, gridDim.x * 6, lane, s_off, s_rows, false);
+      else
+        shrink_warp<2048>(p, gw, gridDim.x * 6, lane, s_off, s_rows, false);
       asm volatile("fence.proxy.async.global;\n" ::: "memory");
       __syncwarp();
       if (lane == 0) red_add_release(p.sync, 1);
@@ -725,7 +749,10 @@ __global__ void __launch_bounds__(256, 1)
         tc_fence_before();
         mbar_arrive(tmem_empty);
         named_bar_sync(1, 128);
-        if (ep_t == 0) { sh.flag = atom_add_acq_rel(&p.counters[t], 1); stamp(15); }
+        if (ep_t == 0) {
+          sh.flag = atom_add_acq_rel(&p.counters[t], 1);
+          stamp(15);
+        }
         named_bar_sync(1, 128);
         const bool last = (sh.flag == nseg - 1);
         named_bar_sync(1, 128);

@@ -510,7 +510,6 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
   base.w_blocked = 1;
   if (const char* e = getenv("ICR_PREISSUE")) base.preissue_cap = atoi(e);
   if (const char* e = getenv("ICR_STAGES")) base.stages = atoi(e);
-  if (const char* e = getenv("ICR_TOUCH")) base.touch = atoi(e);
   base.ws = m->ws;
   base.counters = m->counters;
   base.rank = c.lora_rank;
