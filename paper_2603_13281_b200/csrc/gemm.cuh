@@ -108,10 +108,9 @@ struct GemmParams {
   long long pf_units;   // U' of the next GEMM
   int pf_G, pf_skip, pf_max;
   // tuning / diagnostics (0 = defaults)
-  unsigned long long* trace;  // per-CTA %globaltimer stamps [grid][8] (null = off)
+  unsigned long long* trace;  // per-CTA %globaltimer stamps [grid][16] (null = off)
   int stages;     // smem ring depth actually used (<= compiled maximum)
-  int preissue_cap;
-  int touch;      // diagnostic: pre-touch the tail's buffers at kernel start  // weight stages issued before griddepcontrol.wait: 0 all, <0 none, k>0 min(k, ring)
+  int preissue_cap;  // weight stages issued before griddepcontrol.wait: 0 all, <0 none, k>0 min(k, ring)
   int skip_mma;   // 1: consume stages without tcgen05.mma (pure TMA streaming rate)
 };
 
