@@ -482,7 +482,10 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
   // LoRA chunks are part of every launch of an adapter-carrying model (zero U for rows
   // without an adapter), so stream-K split points -- and with them every encoder row's
   // bits -- never depend on which rows the batch holds.
-  const bool lora = c.lora_rank > 0;
+  // ICR_DIAG_NO_LORA=1 (timing diagnostics only, adapters ignored): drops the LoRA chunks and
+  // the in-kernel shrink to measure their share of the step
+  static const bool diag_no_lora = getenv("ICR_DIAG_NO_LORA") != nullptr;
+  const bool lora = c.lora_rank > 0 && !diag_no_lora;
   const bool pf_a_on = getenv("ICR_L2_PREFETCH") != nullptr;
   const int d = c.hidden_dim, rp = mt.rp;
   long long launches = 0;
