@@ -171,7 +171,7 @@ struct RowMeta {
   float* inv;
 };
 
-template <int NT>
+template <int NT, int MODE>
 __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0, float (&v)[16],
                                            int ep_t, EpiShared& sh, const RowMeta& rm,
                                            const float* pre = nullptr) {
@@ -181,15 +181,13 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] = __fmul_rn(v[j], rm.inv[n0 + j]);
   }
-  switch (p.mode) {
-    case EPI_F32: {
+  if constexpr (MODE == EPI_F32) {
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int n = n0 + j;
         if (n < p.n_rows) p.out_f32[(size_t)(p.row0 + n) * p.ld_out + m] = v[j];
       }
-    } break;
-    case EPI_RESID: {
+  } else if constexpr (MODE == EPI_RESID) {
       const int wq = ep_t >> 5, ln = ep_t & 31;
       float sq[16], old[16];
       // all residual loads before any store (the stores may alias them for the compiler, which
@@ -225,8 +223,7 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
         }
       }
       named_bar_sync(1, 128);
-    } break;
-    case EPI_SILU: {
+  } else if constexpr (MODE == EPI_SILU) {
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const float partner = __shfl_xor_sync(0xffffffffu, v[j], 1);
@@ -236,8 +233,7 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
           p.out_bf16[(size_t)(p.row0 + n) * (p.M >> 1) + (m >> 1)] = __float2bfloat16_rn(f);
         }
       }
-    } break;
-    case EPI_QKV: {
+  } else if constexpr (MODE == EPI_QKV) {
       const int hd = p.head_dim;
       const int region = m < p.q_dim ? 0 : (m < p.q_dim + p.kv_dim ? 1 : 2);
       const int base = region == 0 ? 0 : (region == 1 ? p.q_dim : p.q_dim + p.kv_dim);
@@ -275,8 +271,7 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
           pages[(size_t)rm.kvoff[n] + (size_t)head * 16 * hd + i] = __float2bfloat16_rn(out);
         }
       }
-    } break;
-    case EPI_ARGMAX: {
+  } else if constexpr (MODE == EPI_ARGMAX) {
       const int wq = ep_t >> 5, ln = ep_t & 31;
       float vals[16];
 #pragma unroll
@@ -300,9 +295,6 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
               make_float2(val, __int_as_float(idx));
       }
       named_bar_sync(1, 128);
-    } break;
-    default:
-      break;
   }
 }
 
@@ -355,6 +347,7 @@ __device__ __forceinline__ void lora_shrink_tasks(const GemmParams& p, int gwarp
     if (task != gwarp) shrink_load_a<SL>(p, task, lane, st);  // the first was preloaded
     if (r0 == r1) continue;
     const int k0 = ks * SL;
+#pragma unroll 1
     for (int rr = r0; rr < r1; ++rr) {
       const int gr = s_rows[rr];
       if (gr < p.row0 || gr >= p.row0 + p.n_rows) continue;
@@ -388,11 +381,13 @@ __device__ __forceinline__ void lora_shrink_tasks(const GemmParams& p, int gwarp
     if (splits > 1 && lane == 0) {
       int* cnt = p.sh_cnt + combo;
       if (atom_add_acq_rel(cnt, 1) == splits - 1) {
+#pragma unroll 1
         for (int rr = r0; rr < r1; ++rr) {
           const int gr = s_rows[rr];
           if (gr < p.row0 || gr >= p.row0 + p.n_rows) continue;
           const size_t slot = ((size_t)gr * 2 + t) * p.rank + j;
           float s = 0.f;
+#pragma unroll 1
           for (int q = 0; q < splits; ++q)
             s = (q == 0) ? __ldcg(p.sh_part + slot)
                          : __fadd_rn(s, __ldcg(p.sh_part + (size_t)q * p.rows_total * 2 * p.rank + slot));
@@ -406,7 +401,8 @@ __device__ __forceinline__ void lora_shrink_tasks(const GemmParams& p, int gwarp
 }
 
 // The shrink of one warp: A of its first task preloaded before the PDL wait, then the tasks.
-// SL = 4096 for K <= 4096 (q, o, gate|up: one slice, no combine), 2048 otherwise (down).
+// One 4096-element slice per task: q, o, gate|up need no combine; down (K = 14336) combines 4.
+constexpr int SHRINK_SL = 4096;
 template <int SL>
 __device__ __forceinline__ void shrink_warp(const GemmParams& p, int gwarp, int nwarps, int lane,
                                             const int* s_off, const int* s_rows, bool wait_first) {
@@ -416,7 +412,7 @@ __device__ __forceinline__ void shrink_warp(const GemmParams& p, int gwarp, int 
   lora_shrink_tasks<SL>(p, gwarp, nwarps, lane, s_off, s_rows, st);
 }
 
-template <int NT>
+template <int NT, int MODE>
 __global__ void __launch_bounds__(256, 1)
     gemm_streamk_kernel(const __grid_constant__ CUtensorMap tm_w,
                         const __grid_constant__ CUtensorMap tm_x,
@@ -485,14 +481,6 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) stamp(0);
   // pull the NEXT projection's adapter A matrices into L2 so its shrink loads hit L2
-  if (p.pfa_bytes > 0 && warp == 3) {
-    const long long units = p.pfa_bytes >> 14;
-    const long long b = (long long)blockIdx.x * units / gridDim.x;
-    const long long e = (long long)(blockIdx.x + 1) * units / gridDim.x;
-    for (long long u = b + lane_id(); u < e; u += 32) bulk_prefetch_l2(p.pfa + (u << 14), 16384);
-    if (p.pfa2 != nullptr)
-      for (long long u = b + lane_id(); u < e; u += 32) bulk_prefetch_l2(p.pfa2 + (u << 14), 16384);
-  }
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
@@ -547,8 +535,8 @@ __global__ void __launch_bounds__(256, 1)
         const bool lo = chunk_of(cu, ch);
         uint8_t* dst = smem + (size_t)stage * C::STAGE + W_BYTES;
         if (lo) {
-          if (!lora_ready) {  // U is produced by this grid's shrink warps (6 per CTA)
-            const int target = gridDim.x * 6;
+          if (!lora_ready) {  // U is produced by this grid's shrink warps (2 per CTA)
+            const int target = gridDim.x * 2;  // every shrink warp (2 per CTA) published
             stamp(2);
             while (ld_acquire(p.sync) < target) __nanosleep(32);
             stamp(3);
@@ -588,16 +576,6 @@ __global__ void __launch_bounds__(256, 1)
         if (++stage == NS) { stage = 0; phase ^= 1; }
       }
       stamp(4);
-      // all of this CTA's weight bytes are requested: keep HBM busy with the next weights
-      if (p.pf_w != nullptr) {
-        for (int c2 = c; c2 < p.pf_G; c2 += gridDim.x) {
-          const long long b = (long long)c2 * p.pf_units / p.pf_G;
-          const long long e = (long long)(c2 + 1) * p.pf_units / p.pf_G;
-          const long long s0 = b + p.pf_skip;
-          const long long s1 = (e < s0 + p.pf_max) ? e : s0 + p.pf_max;
-          for (long long u = s0; u < s1; ++u) bulk_prefetch_l2(p.pf_w + u * W_BYTES, W_BYTES);
-        }
-      }
     }
   } else if (warp == 1) {
     // ---------------- tcgen05.mma issuer ----------------
@@ -646,12 +624,8 @@ __global__ void __launch_bounds__(256, 1)
       named_bar_sync(3, 64);
       const int nseg = s_off[p.slots];
       for (int i = t64; i < nseg; i += 64) s_rows[i] = p.seg_rows[i];
-      named_bar_sync(2, 192);  // publish the table to the epilogue warps as well
-      const int gw = blockIdx.x * 2 + (warp - 2);
-      if (p.sh_K <= 4096)
-        shrink_warp<4096>(p, gw, gridDim.x * 6, lane, s_off, s_rows, true);
-      else
-        shrink_warp<2048>(p, gw, gridDim.x * 6, lane, s_off, s_rows, true);
+      named_bar_sync(3, 64);
+      shrink_warp<SHRINK_SL>(p, blockIdx.x * 2 + (warp - 2), gridDim.x * 2, lane, s_off, s_rows, true);
       asm volatile("fence.proxy.async.global;\n" ::: "memory");  // U is read by TMA
       __syncwarp();
       if (lane == 0) red_add_release(p.sync, 1);
@@ -674,12 +648,13 @@ __global__ void __launch_bounds__(256, 1)
         kind = p.row_kind ? p.row_kind[gn] : 0;
         ad = p.row_adapter ? p.row_adapter[gn] : -1;
         pos = p.row_pos ? p.row_pos[gn] : 0;
-        if (p.mode == EPI_QKV && kind == 0) {
+        if (MODE == EPI_QKV && kind == 0) {
           const int page = p.block_table[(size_t)p.row_seq[gn] * p.bt_stride + (pos >> 4)];
           kvoff = (page * p.num_kv_heads * 16 + (pos & 15)) * p.head_dim;
         }
         if (p.in_ssq != nullptr) {
           float ss = 0.f;
+#pragma unroll 4
           for (int t = 0; t < p.ss_tiles; ++t) ss = __fadd_rn(ss, p.in_ssq[(size_t)t * p.ss_stride + gn]);
           inv = __fdiv_rn(1.f, sqrtf(__fadd_rn(__fdiv_rn(ss, p.ss_d), p.eps)));
         }
@@ -691,22 +666,6 @@ __global__ void __launch_bounds__(256, 1)
       rm.inv[n] = inv;
     }
     named_bar_sync(1, 128);
-    if (p.sh_x != nullptr) {
-      // the epilogue warps are idle until the first tile drains: help with the shrink so U
-      // is ready long before any LoRA chunk is streamed (latency under full HBM load)
-      const int lane = ep_t & 31;
-      const int* s_off = rm.kind + 5 * NT;
-      const int* s_rows = s_off + (p.slots + 1);
-      named_bar_sync(2, 192);
-      const int gw = gridDim.x * 2 + blockIdx.x * 4 + (warp - 4);
-      if (p.sh_K <= 4096)
-        shrink_warp<4096>(p, gw, gridDim.x * 6, lane, s_off, s_rows, false);
-      else
-        shrink_warp<2048>(p, gw, gridDim.x * 6, lane, s_off, s_rows, false);
-      asm volatile("fence.proxy.async.global;\n" ::: "memory");
-      __syncwarp();
-      if (lane == 0) red_add_release(p.sync, 1);
-    }
     uint32_t tphase = 0;
     for (int t = t_first; t <= t_last; ++t) {
       const long long t0 = (long long)t * sp.Ut;
@@ -715,7 +674,7 @@ __global__ void __launch_bounds__(256, 1)
       // residual rows of this tile's first 16 columns: loaded before the accumulator is
       // ready so the epilogue's critical path has no dependent global load
       float pre[16];
-      const bool have_pre = p.mode == EPI_RESID;
+      const bool have_pre = MODE == EPI_RESID;
       if (have_pre) {
         const int m = t * BM + ep_t;
 #pragma unroll
@@ -725,19 +684,15 @@ __global__ void __launch_bounds__(256, 1)
       mbar_wait(tmem_full, tphase);
       tc_fence_after();
       if (ep_t == 0) stamp(13);
-      if (nseg == 1) {
-        for (int cc = 0; cc < NT / 16; ++cc) {
-          float v[16];
-          tmem_ld16(tmem_base + lane_base + cc * 16, v);
-          finalize16<NT>(p, t, cc * 16, v, ep_t, sh, rm, (have_pre && cc == 0) ? pre : nullptr);
-        }
-        tc_fence_before();
-        mbar_arrive(tmem_empty);
-      } else {
-        // partial layout [cta][slot][128 features][NT]: each thread's 16 values of a chunk are
-        // one contiguous 64-byte run (4 x 16-byte stores / loads)
+      // Non-final stream-K segments publish their fp32 partial (layout [cta][slot][128
+      // features][NT]: a thread's 16 values of a chunk are one contiguous 64-byte run) and the
+      // last to arrive folds all partials in segment order (deterministic). One finalize call
+      // site, so the tail's code stays compact in the instruction caches.
+      bool fin = true;
+      if (nseg > 1) {
         const int slot = (t == t_first) ? 0 : 1;
         float* wsp = p.ws + (((size_t)c * 2 + slot) * BM + ep_t) * NT;
+#pragma unroll 1
         for (int cc = 0; cc < NT / 16; ++cc) {
           float v[16];
           tmem_ld16(tmem_base + lane_base + cc * 16, v);
@@ -754,14 +709,19 @@ __global__ void __launch_bounds__(256, 1)
           stamp(15);
         }
         named_bar_sync(1, 128);
-        const bool last = (sh.flag == nseg - 1);
+        fin = (sh.flag == nseg - 1);
         named_bar_sync(1, 128);
-        if (last) {
-          // the last segment to arrive folds all partials in segment order; the loads of up to
-          // SEG_BATCH segments are issued before the first add (one L2 round trip, not nseg)
-          constexpr int SEG_BATCH = 8;
-          for (int cc = 0; cc < NT / 16; ++cc) {
-            float v[16];
+      }
+      if (fin) {
+#pragma unroll 1
+        for (int cc = 0; cc < NT / 16; ++cc) {
+          float v[16];
+          if (nseg == 1) {
+            tmem_ld16(tmem_base + lane_base + cc * 16, v);
+          } else {
+            // up to SEG_BATCH segments' loads are issued before the first add
+            constexpr int SEG_BATCH = 4;
+#pragma unroll 1
             for (int s0 = 0; s0 < nseg; s0 += SEG_BATCH) {
               float4 buf[SEG_BATCH][4];
 #pragma unroll
@@ -788,11 +748,16 @@ __global__ void __launch_bounds__(256, 1)
                 }
               }
             }
-            if (ep_t == 0 && cc == 0) stamp(10);
-            finalize16<NT>(p, t, cc * 16, v, ep_t, sh, rm, (have_pre && cc == 0) ? pre : nullptr);
-            if (ep_t == 0 && cc == 0) stamp(11);
           }
-          if (ep_t == 0) p.counters[t] = 0;
+          if (ep_t == 0 && cc == 0) stamp(10);
+          finalize16<NT, MODE>(p, t, cc * 16, v, ep_t, sh, rm, (have_pre && cc == 0) ? pre : nullptr);
+          if (ep_t == 0 && cc == 0) stamp(11);
+        }
+        if (nseg == 1) {
+          tc_fence_before();
+          mbar_arrive(tmem_empty);
+        } else if (ep_t == 0) {
+          p.counters[t] = 0;
         }
       }
       if (ep_t == 0) stamp(14);
@@ -808,14 +773,16 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 // ------------------------------------------------------------------ host side
-template <int NT>
-static cudaError_t launch_nt(const CUtensorMap& tw, const CUtensorMap& tx, const CUtensorMap& tlb,
-                             const CUtensorMap& tlu, const GemmParams& p, int x_row0, int num_sms,
-                             cudaStream_t s) {
+// One kernel per (token-tile width, epilogue): each instantiation carries only its own
+// epilogue, so the code a tile's tail executes stays small and hot in the instruction caches.
+template <int NT, int MODE>
+static cudaError_t launch_ntm(const CUtensorMap& tw, const CUtensorMap& tx, const CUtensorMap& tlb,
+                              const CUtensorMap& tlu, const GemmParams& p, int x_row0, int num_sms,
+                              cudaStream_t s) {
   using C = Cfg<NT>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_streamk_kernel<NT>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_streamk_kernel<NT, MODE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
@@ -825,8 +792,22 @@ static cudaError_t launch_nt(const CUtensorMap& tw, const CUtensorMap& tx, const
   if ((unsigned long long)U * (unsigned long long)(G + 1) >= (1ull << 32)) return cudaErrorInvalidValue;
   const int NS = ring_stages<NT>(p.stages);
   const size_t smem = 1024 + (size_t)NS * C::STAGE + aux_smem<NT>();
-  return launch_pdl(gemm_streamk_kernel<NT>, dim3(G), dim3(256), smem, s, tw, tx, tlb, tlu, p,
+  return launch_pdl(gemm_streamk_kernel<NT, MODE>, dim3(G), dim3(256), smem, s, tw, tx, tlb, tlu, p,
                     x_row0);
+}
+
+template <int NT>
+static cudaError_t launch_nt(const CUtensorMap& tw, const CUtensorMap& tx, const CUtensorMap& tlb,
+                             const CUtensorMap& tlu, const GemmParams& p, int x_row0, int num_sms,
+                             cudaStream_t s) {
+  switch (p.mode) {
+    case EPI_F32: return launch_ntm<NT, EPI_F32>(tw, tx, tlb, tlu, p, x_row0, num_sms, s);
+    case EPI_RESID: return launch_ntm<NT, EPI_RESID>(tw, tx, tlb, tlu, p, x_row0, num_sms, s);
+    case EPI_SILU: return launch_ntm<NT, EPI_SILU>(tw, tx, tlb, tlu, p, x_row0, num_sms, s);
+    case EPI_QKV: return launch_ntm<NT, EPI_QKV>(tw, tx, tlb, tlu, p, x_row0, num_sms, s);
+    case EPI_ARGMAX: return launch_ntm<NT, EPI_ARGMAX>(tw, tx, tlb, tlu, p, x_row0, num_sms, s);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 int gemm_pick_nt(int rows) {

@@ -98,15 +98,6 @@ struct GemmParams {
   float* ws;                    // [grid][2][N][128]
   int* counters;                // [m_tiles]
   int max_segs;
-  // L2 prefetch of the NEXT projection's weights once this CTA has issued all its loads:
-  // next-kernel CTA c streams tile-major units [c*U'/G', (c+1)*U'/G'); its first pf_skip
-  // units come in through its own PDL pre-issue, the following <= pf_max are prefetched.
-  const uint8_t* pf_w;  // null = none
-  const uint8_t* pfa;   // the next projection's adapter A matrices (and a second target)
-  const uint8_t* pfa2;
-  long long pfa_bytes;  // bytes of each
-  long long pf_units;   // U' of the next GEMM
-  int pf_G, pf_skip, pf_max;
   // tuning / diagnostics (0 = defaults)
   unsigned long long* trace;  // per-CTA %globaltimer stamps [grid][16] (null = off)
   int stages;     // smem ring depth actually used (<= compiled maximum)

@@ -449,24 +449,6 @@ static icr_status validate_batch(icr_model* m, const icr_batch* b, const int* po
   return ICR_OK;
 }
 
-// L2 prefetch target for a GEMM tail: the next projection (tile-major) weights.
-static const int kPfMaxUnits = 24;  // per CTA: 24 x 16 KB x 148 CTAs ~= 57 MB of L2
-static void set_prefetch(const icr_model* m, GemmParams& p, const void* next_w, int next_M,
-                         int next_K, int rows) {
-  // Off by default: the tail prefetch (up to 57 MB) saturates HBM exactly while the last
-  // tiles' epilogues need low-latency L2 round trips (measured: +0.35 ms per decode step).
-  if (next_w == nullptr || rows > 256 || !getenv("ICR_L2_PREFETCH")) return;
-  const long long U = (long long)(next_M / 128) * (next_K / 64);
-  const int G = (int)std::min<long long>(U, m->num_sms);
-  const int skip = gemm_stages(gemm_pick_nt(rows));
-  const long long per = U / G;
-  if (per <= skip) return;
-  p.pf_w = (const uint8_t*)next_w;
-  p.pf_units = U;
-  p.pf_G = G;
-  p.pf_skip = skip;
-  p.pf_max = (int)std::min<long long>(per - skip, kPfMaxUnits);
-}
 
 // Enqueue the whole forward on `s` using metadata resident at m->meta_dev (layout mt).
 static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_dev, cudaStream_t s) {
@@ -486,7 +468,6 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
   // the in-kernel shrink to measure their share of the step
   static const bool diag_no_lora = getenv("ICR_DIAG_NO_LORA") != nullptr;
   const bool lora = c.lora_rank > 0 && !diag_no_lora;
-  const bool pf_a_on = getenv("ICR_L2_PREFETCH") != nullptr;
   const int d = c.hidden_dim, rp = mt.rp;
   long long launches = 0;
 
@@ -559,9 +540,7 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
   al.out_ld = m->q_dim;
 
   icr_status st;
-  auto a_bytes = [&](int K) -> long long {
-    return pf_a_on ? (long long)c.adapter_slots * c.lora_rank * K * 2 : 0;
-  };
+
   const int qkv_M = m->q_dim + 2 * m->kv_dim;
   const bool pf_on = rp <= 256 && getenv("ICR_L2_PREFETCH") != nullptr;
   CUDA_TRY(embed_launch(tokens, kind, m->embed, m->x, m->xb, m->ssq, rp, rp, d,
@@ -584,8 +563,6 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
         p.sh_a0 = (const __nv_bfloat16*)w.a_q;
         p.sync = m->sync + 0;
         p.reset_sync = m->sync + 6;  // the previous down's
-        p.pfa = (const uint8_t*)w.a_o;  // next shrink: o
-        p.pfa_bytes = a_bytes(m->q_dim);
       }
       p.out_bf16 = m->qb;
       p.q_dim = m->q_dim;
@@ -624,14 +601,10 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
         p.sh_a0 = (const __nv_bfloat16*)w.a_o;
         p.sync = m->sync + 2;
         p.reset_sync = m->sync + 0;
-        p.pfa = (const uint8_t*)w.a_gate;  // next shrink: gate | up
-        p.pfa2 = (const uint8_t*)w.a_up;
-        p.pfa_bytes = a_bytes(d);
       }
       p.resid = m->x;
       p.resid_bf16 = m->xb;
       p.out_ssq = m->ssq;
-      set_prefetch(m, p, w.w_gu, 2 * c.ffn_dim, d, rp);
       if ((st = gemm(lm.o, m->xmap_att, p, rp, lora ? &lm.lb_o : nullptr, TK_O))) return st;
       mark(m, s, TK_O);
     }
@@ -647,11 +620,8 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
         p.sh_a0 = (const __nv_bfloat16*)w.a_gate; p.sh_a1 = (const __nv_bfloat16*)w.a_up;
         p.sync = m->sync + 4;
         p.reset_sync = m->sync + 2;
-        p.pfa = (const uint8_t*)w.a_down;  // next shrink: down
-        p.pfa_bytes = a_bytes(c.ffn_dim);
       }
       p.out_bf16 = m->f;
-      set_prefetch(m, p, w.w_down, d, c.ffn_dim, rp);
       if ((st = gemm(lm.gu, m->xmap_xb, p, rp, lora ? &lm.lb_gu : nullptr, TK_GU))) return st;
       mark(m, s, TK_GU);
     }
@@ -666,18 +636,10 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
         p.sh_a0 = (const __nv_bfloat16*)w.a_down;
         p.sync = m->sync + 6;
         p.reset_sync = m->sync + 4;
-        if (l + 1 < c.num_layers) {  // next shrink: the next layer's q
-          p.pfa = (const uint8_t*)m->layers[l + 1].a_q;
-          p.pfa_bytes = a_bytes(d);
-        }
       }
       p.resid = m->x;
       p.resid_bf16 = m->xb;
       p.out_ssq = m->ssq;
-      if (l + 1 < c.num_layers)
-        set_prefetch(m, p, m->layers[l + 1].w_qkv, qkv_M, d, rp);
-      else
-        set_prefetch(m, p, m->lm_head, m->vpad, d, rp);
       if ((st = gemm(lm.down, m->xmap_f, p, rp, lora ? &lm.lb_down : nullptr, TK_DOWN))) return st;
       mark(m, s, TK_DOWN);
     }

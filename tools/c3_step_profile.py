@@ -42,6 +42,8 @@ def main(n=64, prefix=8192):
         _lib.check(rt._lib.icr_profile_ablate(rt._handle, 1 << k, 10, C.byref(avg), _lib.stream_handle()))
         out[nm] = round(full - avg.value, 3)
     print("in-graph marginal ms:", out)
+    if len(sys.argv) > 1:
+        _lib.check(rt._lib.icr_profile_trace(rt._handle, sys.argv[1].encode(), _lib.stream_handle()))
 
 
 if __name__ == "__main__":
