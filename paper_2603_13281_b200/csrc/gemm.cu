@@ -713,24 +713,78 @@ __global__ void __launch_bounds__(256, 1)
         named_bar_sync(1, 128);
       }
       if (fin) {
+        // Wide launches (NT > 16) software-pipeline the finalization: the next 16-column
+        // chunk's first PF partials and residual rows are requested before the current chunk
+        // is folded, so NT/16 chunks cost ~1 round trip instead of NT/16 of them.
+        constexpr int PF = NT > 16 ? 2 : 1;
+        constexpr bool PIPE = NT > 16;
+        float4 nb[PF][4];
+        float npre[16];
+        auto seg_src = [&](int s, int cc) {
+          const int cs = c_first + s;
+          const int sl = (sp.ubegin(cs) >= t0) ? 0 : 1;  // tile t is cs's first tile
+          return reinterpret_cast<const float4*>(p.ws + (((size_t)cs * 2 + sl) * BM + ep_t) * NT + cc * 16);
+        };
+        auto fetch = [&](int cc) {
+          if (nseg > 1) {
+#pragma unroll
+            for (int s = 0; s < PF; ++s)
+              if (s < nseg) {
+                const float4* src = seg_src(s, cc);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) nb[s][q] = __ldcg(src + q);
+              }
+          }
+          if (MODE == EPI_RESID) {
+            const int m = t * BM + ep_t;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int n = cc * 16 + j;
+              npre[j] = (n < p.n_rows) ? __ldcg(p.resid + (size_t)(p.row0 + n) * p.M + m) : 0.f;
+            }
+          }
+        };
+        if (PIPE) fetch(0);
 #pragma unroll 1
         for (int cc = 0; cc < NT / 16; ++cc) {
+          float4 cb[PF][4];
+          float cpre[16];
+          if (PIPE) {
+#pragma unroll
+            for (int s = 0; s < PF; ++s)
+#pragma unroll
+              for (int q = 0; q < 4; ++q) cb[s][q] = nb[s][q];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) cpre[j] = npre[j];
+            if (cc + 1 < NT / 16) fetch(cc + 1);
+          }
           float v[16];
           if (nseg == 1) {
             tmem_ld16(tmem_base + lane_base + cc * 16, v);
           } else {
-            // up to SEG_BATCH segments' loads are issued before the first add
+            // segments [0, PF) were prefetched (wide launches); the rest are loaded SEG_BATCH
+            // at a time with every load of a batch issued before its first add
             constexpr int SEG_BATCH = 4;
+            const int s_start = PIPE ? min(PF, nseg) : 0;
+            if (PIPE) {
+#pragma unroll
+              for (int s = 0; s < PF; ++s)
+                if (s < nseg) {
+#pragma unroll
+                  for (int q = 0; q < 4; ++q) {
+                    const float x[4] = {cb[s][q].x, cb[s][q].y, cb[s][q].z, cb[s][q].w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) v[4 * q + e] = (s == 0) ? x[e] : __fadd_rn(v[4 * q + e], x[e]);
+                  }
+                }
+            }
 #pragma unroll 1
-            for (int s0 = 0; s0 < nseg; s0 += SEG_BATCH) {
+            for (int s0 = s_start; s0 < nseg; s0 += SEG_BATCH) {
               float4 buf[SEG_BATCH][4];
 #pragma unroll
               for (int s = 0; s < SEG_BATCH; ++s) {
                 if (s0 + s < nseg) {
-                  const int cs = c_first + s0 + s;
-                  const int sl = (sp.ubegin(cs) >= t0) ? 0 : 1;  // tile t is cs's first tile
-                  const float4* src = reinterpret_cast<const float4*>(
-                      p.ws + (((size_t)cs * 2 + sl) * BM + ep_t) * NT + cc * 16);
+                  const float4* src = seg_src(s0 + s, cc);
 #pragma unroll
                   for (int q = 0; q < 4; ++q) buf[s][q] = __ldcg(src + q);
                 }
@@ -750,7 +804,8 @@ __global__ void __launch_bounds__(256, 1)
             }
           }
           if (ep_t == 0 && cc == 0) stamp(10);
-          finalize16<NT, MODE>(p, t, cc * 16, v, ep_t, sh, rm, (have_pre && cc == 0) ? pre : nullptr);
+          const float* prow = PIPE ? (MODE == EPI_RESID ? cpre : nullptr) : ((have_pre && cc == 0) ? pre : nullptr);
+          finalize16<NT, MODE>(p, t, cc * 16, v, ep_t, sh, rm, prow);
           if (ep_t == 0 && cc == 0) stamp(11);
         }
         if (nseg == 1) {
