@@ -9,12 +9,14 @@ missing, compute entry points raise DeviceError.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 from .errors import (CapacityError, ConfigError, ContractViolationError, DeviceError,
                      ModeError, ShapeError, StateError)
 
-LIB_PATH = Path(__file__).resolve().parent / "libicarus_b200.so"
+# ICR_LIB_PATH: tuning A/B runs only (tools/); the product loads the in-tree build
+LIB_PATH = Path(os.environ.get("ICR_LIB_PATH") or Path(__file__).resolve().parent / "libicarus_b200.so")
 
 _STATUS = {
     1: ShapeError, 2: ConfigError, 3: ModeError, 4: StateError, 5: CapacityError,

@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
   // attention moves few bytes: use the idle HBM to pull the o-projection weights into L2
   prefetch_slice_l2(pf_base, pf_bytes, blockIdx.y * gridDim.x + blockIdx.x, gridDim.x * gridDim.y);
   pdl_launch();
-  const int item_id = blockIdx.x;
+  const int item_id = blockIdx.y;  // grid (KV head, item): long items' heads in the first wave
   if (item_id >= *n_items_dev) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
   __syncthreads();
   // the plan (items, pages) was uploaded before the forward: readable before the wait
   const AttnItem it = items[item_id];
-  const int g = blockIdx.y;
+  const int g = blockIdx.x;
 
   if (warp == 0) {
     // ---------------- producer: TMA page ring ----------------
@@ -353,8 +353,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
 }
 
 // Fixed-order merge of chunk partials: one CTA per (row, KV group), one thread per
-// (head-in-group, dim); per head the chunk weights exp(m_c - M) and L are computed once
-// (sequentially, chunk order) and shared through smem.
+// (head-in-group, dim); the chunk weights exp(m_c - M), L and O are folded in chunk order.
 template <int HD>
 __global__ void __launch_bounds__(512)
     attn_merge_kernel(const float* __restrict__ part_o, const float2* __restrict__ part_ml,
@@ -362,62 +361,70 @@ __global__ void __launch_bounds__(512)
                       int num_heads, int group, int max_chunks, int chunk_tokens,
                       __nv_bfloat16* __restrict__ out, int out_ld,
                       unsigned long long* __restrict__ trace) {
-  extern __shared__ float merge_smem[];  // [group][max_chunks] weights + [group] L
   const int cta_id = blockIdx.y * gridDim.x + blockIdx.x;
   if (trace != nullptr && threadIdx.x == 0 && cta_id < 4096) trace[(size_t)cta_id * 16 + 6] = globaltimer();
   pdl_launch();
+  // the row table is uploaded before the forward: read it while the partials run
+  const int r = blockIdx.x, g = blockIdx.y;
+  const int kind = row_kind[r], nch = row_pos[r] / chunk_tokens + 1;
   pdl_wait();
   if (trace != nullptr && threadIdx.x == 0 && cta_id < 4096) trace[(size_t)cta_id * 16 + 7] = globaltimer();
-  const int r = blockIdx.x, g = blockIdx.y;
-  if (row_kind[r] < 0) return;
-  const int nch = row_pos[r] / chunk_tokens + 1;
-  float* wts = merge_smem;
-  float* Ls = merge_smem + group * max_chunks;
-  const int tid = threadIdx.x;
-  // Chunk partials are loaded MB at a time before they are folded (in chunk order): one L2
-  // round trip per MB chunks instead of one per chunk.
-  constexpr int MB = 16;
-  if (tid < group) {
-    const size_t base = ((size_t)r * num_heads + g * group + tid) * max_chunks;
-    float M = -INFINITY;
-    for (int c0 = 0; c0 < nch; c0 += MB) {
-      float2 ml[MB];
-#pragma unroll
-      for (int k = 0; k < MB; ++k) ml[k] = (c0 + k < nch) ? part_ml[base + c0 + k] : make_float2(-INFINITY, 0.f);
-#pragma unroll
-      for (int k = 0; k < MB; ++k) M = fmaxf(M, ml[k].x);
-    }
-    float L = 0.f;
-    for (int c0 = 0; c0 < nch; c0 += MB) {
-      float2 ml[MB];
-#pragma unroll
-      for (int k = 0; k < MB; ++k) ml[k] = (c0 + k < nch) ? part_ml[base + c0 + k] : make_float2(-INFINITY, 0.f);
-#pragma unroll
-      for (int k = 0; k < MB; ++k) {
-        if (c0 + k < nch) {
-          const float w = exp2f(ml[k].x - M);  // partial maxima are in the log2 domain
-          wts[tid * max_chunks + c0 + k] = w;
-          L = fmaf(ml[k].y, w, L);
-        }
-      }
-    }
-    Ls[tid] = L;
-  }
-  __syncthreads();
-  for (int idx = tid; idx < group * HD; idx += blockDim.x) {
+  if (kind < 0) return;
+  // Every thread folds one (head, dim) column over the row's chunks in chunk order; the
+  // per-chunk weights are recomputed per thread from (m, l) (same-address loads broadcast
+  // within a warp), so no shared memory or block barrier sits between the loads and the fold.
+  // Rows with at most MB chunks issue all their loads in one round trip.
+  constexpr int MB = 32;
+  for (int idx = threadIdx.x; idx < group * HD; idx += blockDim.x) {
     const int hg = idx / HD, d = idx % HD;
     const int head = g * group + hg;
     const size_t base = ((size_t)r * num_heads + head) * max_chunks;
-    float O = 0.f;
-    for (int c0 = 0; c0 < nch; c0 += MB) {
+    float M = -INFINITY, L = 0.f, O = 0.f;
+    if (nch <= MB) {
+      float2 ml[MB];
       float po[MB];
 #pragma unroll
-      for (int k = 0; k < MB; ++k) po[k] = (c0 + k < nch) ? part_o[(base + c0 + k) * HD + d] : 0.f;
+      for (int k = 0; k < MB; ++k) {
+        ml[k] = k < nch ? part_ml[base + k] : make_float2(-INFINITY, 0.f);
+        po[k] = k < nch ? part_o[(base + k) * HD + d] : 0.f;
+      }
 #pragma unroll
-      for (int k = 0; k < MB; ++k)
-        if (c0 + k < nch) O = fmaf(po[k], wts[hg * max_chunks + c0 + k], O);
+      for (int k = 0; k < MB; ++k) M = fmaxf(M, ml[k].x);
+#pragma unroll
+      for (int k = 0; k < MB; ++k) {
+        if (k < nch) {
+          const float w = exp2f(ml[k].x - M);  // partial maxima are in the log2 domain
+          L = fmaf(ml[k].y, w, L);
+          O = fmaf(po[k], w, O);
+        }
+      }
+    } else {
+      for (int c0 = 0; c0 < nch; c0 += MB) {
+        float2 ml[MB];
+#pragma unroll
+        for (int k = 0; k < MB; ++k) ml[k] = (c0 + k < nch) ? part_ml[base + c0 + k] : make_float2(-INFINITY, 0.f);
+#pragma unroll
+        for (int k = 0; k < MB; ++k) M = fmaxf(M, ml[k].x);
+      }
+      for (int c0 = 0; c0 < nch; c0 += MB) {
+        float2 ml[MB];
+        float po[MB];
+#pragma unroll
+        for (int k = 0; k < MB; ++k) {
+          ml[k] = (c0 + k < nch) ? part_ml[base + c0 + k] : make_float2(-INFINITY, 0.f);
+          po[k] = (c0 + k < nch) ? part_o[(base + c0 + k) * HD + d] : 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < MB; ++k) {
+          if (c0 + k < nch) {
+            const float w = exp2f(ml[k].x - M);
+            L = fmaf(ml[k].y, w, L);
+            O = fmaf(po[k], w, O);
+          }
+        }
+      }
     }
-    out[(size_t)r * out_ld + head * HD + d] = __float2bfloat16_rn(__fdiv_rn(O, Ls[hg]));
+    out[(size_t)r * out_ld + head * HD + d] = __float2bfloat16_rn(__fdiv_rn(O, L));
   }
   if (trace != nullptr && threadIdx.x == 0 && cta_id < 4096) trace[(size_t)cta_id * 16 + 5] = globaltimer();
 }
@@ -435,8 +442,7 @@ static cudaError_t attn_launch_hd(const AttnLaunch& a, cudaStream_t s) {
     cudaError_t e = attn_tc_partial_launch(a, a.chunk_tokens / 16, s);
     if (e != cudaSuccess) return e;
     const int mthreads = std::min(512, ((a.group * HD + 31) / 32) * 32);
-    const size_t msmem = (size_t)a.group * (a.max_chunks + 1) * sizeof(float);
-    return launch_pdl(attn_merge_kernel<HD>, dim3(a.n_rows, a.num_kv_heads), dim3(mthreads), msmem, s,
+    return launch_pdl(attn_merge_kernel<HD>, dim3(a.n_rows, a.num_kv_heads), dim3(mthreads), 0, s,
                       a.part_o, a.part_ml, a.row_pos, a.row_kind, a.num_heads, a.group,
                       a.max_chunks, a.chunk_tokens, a.out, a.out_ld,
                       a.trace ? a.trace + 4096 * 16 : nullptr);
@@ -449,15 +455,14 @@ static cudaError_t attn_launch_hd(const AttnLaunch& a, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  dim3 grid(a.n_items_cap, a.num_kv_heads);
+  dim3 grid(a.num_kv_heads, a.n_items_cap);
   cudaError_t e = launch_pdl(attn_partial_kernel<HD>, grid, dim3(ATTN_THREADS), attn_smem<HD>(), s,
                              a.tm_k, a.tm_v, a.q, a.q_ld, a.num_kv_heads, a.group, a.items,
                              a.item_pages, a.item_rows, a.row_pos, a.num_heads, a.max_chunks,
                              a.scale, a.part_o, a.part_ml, a.n_items_dev, a.pf_base, a.pf_bytes, a.trace);
   if (e != cudaSuccess) return e;
   const int mthreads = std::min(512, ((a.group * HD + 31) / 32) * 32);
-  const size_t msmem = (size_t)a.group * (a.max_chunks + 1) * sizeof(float);
-  return launch_pdl(attn_merge_kernel<HD>, dim3(a.n_rows, a.num_kv_heads), dim3(mthreads), msmem, s,
+  return launch_pdl(attn_merge_kernel<HD>, dim3(a.n_rows, a.num_kv_heads), dim3(mthreads), 0, s,
                     a.part_o, a.part_ml, a.row_pos, a.row_kind, a.num_heads, a.group,
                     a.max_chunks, a.chunk_tokens, a.out, a.out_ld,
                     a.trace ? a.trace + 4096 * 16 : nullptr);

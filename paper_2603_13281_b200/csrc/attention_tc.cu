@@ -121,7 +121,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (threadIdx.x == 0) stamp(6);
   if ((smem_u32(tc_smem) & 1023) != 0) __trap();  // SW128 tiles need a 1024-byte base
   pdl_launch();
-  const int item_id = blockIdx.x;
+  // grid (KV head, item): consecutive CTAs are the KV heads of one item, so with items in
+  // longest-first order every head of the long items is dispatched in the first wave
+  const int item_id = blockIdx.y;
   if (item_id >= *n_items_dev) return;
   const int warp = warp_id(), lane = lane_id();
   if (threadIdx.x == 0) {
@@ -146,7 +148,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
   const uint32_t tmem_o = tmem_base + 256;
   const AttnItem it = items[item_id];  // uploaded before the forward
-  const int g = blockIdx.y;
+  const int g = blockIdx.x;
   const int np = it.n_pages;
   const int nsub = (np + SUBP - 1) / SUBP;
 
@@ -231,23 +233,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
   } else {
     // ---------------- Q gather (warps 3-11) ----------------
-    pdl_wait();  // q comes from the q/k/v GEMM
     const int t = threadIdx.x - 96;  // 0..287
     // entry e sits in M row / TMEM lane r(e) = (e % 4) * 32 + e / 4: the entries of a partly
     // filled item spread over all four lane quarters
     // all of a thread's loads are issued before its first store: one round trip, not eight
     constexpr int QPT = (TC_ROWS * 16 + 287) / 288;  // 16-byte chunks per thread
-    uint4 qv[QPT];
+    int qoff[QPT];  // the item's row table is uploaded before the forward: read it before the wait
 #pragma unroll
     for (int k = 0; k < QPT; ++k) {
       const int idx = t + k * 288;
       const int e = idx >> 4, c = idx & 15;
-      qv[k] = make_uint4(0, 0, 0, 0);
+      qoff[k] = -1;
       if (idx < TC_ROWS * 16 && e < it.n_rows) {
         const int2 rr = item_rows[it.row_off + e];
-        qv[k] = __ldg(reinterpret_cast<const uint4*>(q + (size_t)rr.x * q_ld + (g * group + rr.y) * 128 + c * 8));
+        qoff[k] = rr.x * q_ld + (g * group + rr.y) * 128 + c * 8;
       }
     }
+    pdl_wait();  // q comes from the q/k/v GEMM
+    uint4 qv[QPT];
+#pragma unroll
+    for (int k = 0; k < QPT; ++k)
+      qv[k] = qoff[k] >= 0 ? __ldg(reinterpret_cast<const uint4*>(q + qoff[k])) : make_uint4(0, 0, 0, 0);
 #pragma unroll
     for (int k = 0; k < QPT; ++k) {
       const int idx = t + k * 288;
@@ -441,7 +447,7 @@ cudaError_t attn_tc_partial_launch(const AttnLaunch& a, int /*chunk_pages*/, cud
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  return launch_pdl(attn_tc_kernel, dim3(a.n_items_cap, a.num_kv_heads), dim3(TC_THREADS), L::SMEM, s,
+  return launch_pdl(attn_tc_kernel, dim3(a.num_kv_heads, a.n_items_cap), dim3(TC_THREADS), L::SMEM, s,
                     a.tm_k, a.tm_v, a.q, a.q_ld, a.num_kv_heads, a.group, a.items, a.item_pages,
                     a.item_rows, a.row_pos, a.num_heads, a.max_chunks, a.scale, a.part_o, a.part_ml,
                     a.n_items_dev, a.trace);
