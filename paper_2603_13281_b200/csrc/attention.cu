@@ -353,9 +353,13 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
 }
 
 // Fixed-order merge of chunk partials: one CTA per (row, KV group), one thread per
-// (head-in-group, dim); the chunk weights exp(m_c - M), L and O are folded in chunk order.
+// (head-in-group, 4 dims); the chunk weights exp(m_c - M), L and O are folded in chunk order.
+// Few threads and no shared memory: a merge CTA fits beside the next GEMM's CTA, which can
+// then start streaming its weights while the merge runs.
+constexpr int MERGE_THREADS = 128;
+
 template <int HD>
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(MERGE_THREADS, 5)  // <= 96 registers: fits beside a GEMM CTA
     attn_merge_kernel(const float* __restrict__ part_o, const float2* __restrict__ part_ml,
                       const int* __restrict__ row_pos, const int* __restrict__ row_kind,
                       int num_heads, int group, int max_chunks, int chunk_tokens,
@@ -370,61 +374,55 @@ __global__ void __launch_bounds__(512)
   pdl_wait();
   if (trace != nullptr && threadIdx.x == 0 && cta_id < 4096) trace[(size_t)cta_id * 16 + 7] = globaltimer();
   if (kind < 0) return;
-  // Every thread folds one (head, dim) column over the row's chunks in chunk order; the
-  // per-chunk weights are recomputed per thread from (m, l) (same-address loads broadcast
-  // within a warp), so no shared memory or block barrier sits between the loads and the fold.
-  // Rows with at most MB chunks issue all their loads in one round trip.
-  constexpr int MB = 32;
-  for (int idx = threadIdx.x; idx < group * HD; idx += blockDim.x) {
-    const int hg = idx / HD, d = idx % HD;
+  // The (m, l) loads of one head are the same address across its threads (broadcast).
+  constexpr int MB = 12, V = HD / 4;
+  for (int idx = threadIdx.x; idx < group * V; idx += blockDim.x) {
+    const int hg = idx / V, d = (idx % V) * 4;
     const int head = g * group + hg;
     const size_t base = ((size_t)r * num_heads + head) * max_chunks;
-    float M = -INFINITY, L = 0.f, O = 0.f;
-    if (nch <= MB) {
+    float M = -INFINITY, L = 0.f;
+    float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
+    auto fold = [&](const float2& ml, const float4& po) {
+      const float w = exp2f(ml.x - M);  // partial maxima are in the log2 domain
+      L = fmaf(ml.y, w, L);
+      O.x = fmaf(po.x, w, O.x);
+      O.y = fmaf(po.y, w, O.y);
+      O.z = fmaf(po.z, w, O.z);
+      O.w = fmaf(po.w, w, O.w);
+    };
+    // batches of MB chunks, one round trip each; the running maximum rescales what was
+    // folded so far when a later batch raises it (rows with <= MB chunks: one batch)
+    for (int c0 = 0; c0 < nch; c0 += MB) {
       float2 ml[MB];
-      float po[MB];
+      float4 po[MB];
 #pragma unroll
       for (int k = 0; k < MB; ++k) {
-        ml[k] = k < nch ? part_ml[base + k] : make_float2(-INFINITY, 0.f);
-        po[k] = k < nch ? part_o[(base + k) * HD + d] : 0.f;
+        ml[k] = (c0 + k < nch) ? part_ml[base + c0 + k] : make_float2(-INFINITY, 0.f);
+        po[k] = (c0 + k < nch) ? *reinterpret_cast<const float4*>(part_o + (base + c0 + k) * HD + d)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
       }
+      float Mn = M;
 #pragma unroll
-      for (int k = 0; k < MB; ++k) M = fmaxf(M, ml[k].x);
-#pragma unroll
-      for (int k = 0; k < MB; ++k) {
-        if (k < nch) {
-          const float w = exp2f(ml[k].x - M);  // partial maxima are in the log2 domain
-          L = fmaf(ml[k].y, w, L);
-          O = fmaf(po[k], w, O);
-        }
+      for (int k = 0; k < MB; ++k) Mn = fmaxf(Mn, ml[k].x);
+      if (c0 > 0 && Mn != M) {
+        const float sc = exp2f(M - Mn);
+        L *= sc;
+        O.x *= sc;
+        O.y *= sc;
+        O.z *= sc;
+        O.w *= sc;
       }
-    } else {
-      for (int c0 = 0; c0 < nch; c0 += MB) {
-        float2 ml[MB];
+      M = Mn;
 #pragma unroll
-        for (int k = 0; k < MB; ++k) ml[k] = (c0 + k < nch) ? part_ml[base + c0 + k] : make_float2(-INFINITY, 0.f);
-#pragma unroll
-        for (int k = 0; k < MB; ++k) M = fmaxf(M, ml[k].x);
-      }
-      for (int c0 = 0; c0 < nch; c0 += MB) {
-        float2 ml[MB];
-        float po[MB];
-#pragma unroll
-        for (int k = 0; k < MB; ++k) {
-          ml[k] = (c0 + k < nch) ? part_ml[base + c0 + k] : make_float2(-INFINITY, 0.f);
-          po[k] = (c0 + k < nch) ? part_o[(base + c0 + k) * HD + d] : 0.f;
-        }
-#pragma unroll
-        for (int k = 0; k < MB; ++k) {
-          if (c0 + k < nch) {
-            const float w = exp2f(ml[k].x - M);
-            L = fmaf(ml[k].y, w, L);
-            O = fmaf(po[k], w, O);
-          }
-        }
-      }
+      for (int k = 0; k < MB; ++k)
+        if (c0 + k < nch) fold(ml[k], po[k]);
     }
-    out[(size_t)r * out_ld + head * HD + d] = __float2bfloat16_rn(__fdiv_rn(O, L));
+    __nv_bfloat162 lo = __floats2bfloat162_rn(__fdiv_rn(O.x, L), __fdiv_rn(O.y, L));
+    __nv_bfloat162 hi = __floats2bfloat162_rn(__fdiv_rn(O.z, L), __fdiv_rn(O.w, L));
+    uint2 pk;
+    pk.x = *reinterpret_cast<uint32_t*>(&lo);
+    pk.y = *reinterpret_cast<uint32_t*>(&hi);
+    *reinterpret_cast<uint2*>(out + (size_t)r * out_ld + head * HD + d) = pk;
   }
   if (trace != nullptr && threadIdx.x == 0 && cta_id < 4096) trace[(size_t)cta_id * 16 + 5] = globaltimer();
 }
@@ -441,7 +439,7 @@ static cudaError_t attn_launch_hd(const AttnLaunch& a, cudaStream_t s) {
   if (use_tc(HD)) {
     cudaError_t e = attn_tc_partial_launch(a, a.chunk_tokens / 16, s);
     if (e != cudaSuccess) return e;
-    const int mthreads = std::min(512, ((a.group * HD + 31) / 32) * 32);
+    const int mthreads = std::min(MERGE_THREADS, ((a.group * HD / 4 + 31) / 32) * 32);
     return launch_pdl(attn_merge_kernel<HD>, dim3(a.n_rows, a.num_kv_heads), dim3(mthreads), 0, s,
                       a.part_o, a.part_ml, a.row_pos, a.row_kind, a.num_heads, a.group,
                       a.max_chunks, a.chunk_tokens, a.out, a.out_ld,
@@ -461,7 +459,7 @@ static cudaError_t attn_launch_hd(const AttnLaunch& a, cudaStream_t s) {
                              a.item_pages, a.item_rows, a.row_pos, a.num_heads, a.max_chunks,
                              a.scale, a.part_o, a.part_ml, a.n_items_dev, a.pf_base, a.pf_bytes, a.trace);
   if (e != cudaSuccess) return e;
-  const int mthreads = std::min(512, ((a.group * HD + 31) / 32) * 32);
+  const int mthreads = std::min(MERGE_THREADS, ((a.group * HD / 4 + 31) / 32) * 32);
   return launch_pdl(attn_merge_kernel<HD>, dim3(a.n_rows, a.num_kv_heads), dim3(mthreads), 0, s,
                     a.part_o, a.part_ml, a.row_pos, a.row_kind, a.num_heads, a.group,
                     a.max_chunks, a.chunk_tokens, a.out, a.out_ld,
