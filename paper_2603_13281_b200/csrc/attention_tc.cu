@@ -249,7 +249,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         qoff[k] = rr.x * q_ld + (g * group + rr.y) * 128 + c * 8;
       }
     }
+    // P rows of padding entries stay zero for the whole item (the softmax skips them); this
+    // does not depend on the previous kernel, so it runs before the wait
+    for (int idx = t; idx < TC_ROWS * 2 * 2 * 8; idx += 288) {
+      const int r = idx & 127, chunk = idx >> 7;  // chunk: buffer (2) x K-block (2) x 16 B (8)
+      const int e = (r & 31) * 4 + (r >> 5);
+      if (e >= it.n_rows)
+        *reinterpret_cast<uint4*>(smem + L::P_OFF + (chunk >> 3) * (TC_ROWS * 128) + r * 128 + (chunk & 7) * 16) =
+            make_uint4(0, 0, 0, 0);
+    }
     pdl_wait();  // q comes from the q/k/v GEMM
+    if (threadIdx.x == 96) stamp(3);
     uint4 qv[QPT];
 #pragma unroll
     for (int k = 0; k < QPT; ++k)
@@ -262,14 +272,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int r = (e & 3) * 32 + (e >> 2);
         *reinterpret_cast<uint4*>(sQ + (c >> 3) * (TC_ROWS * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4)) = qv[k];
       }
-    }
-    // P rows of padding entries stay zero for the whole item (the softmax skips them)
-    for (int idx = t; idx < TC_ROWS * 2 * 2 * 8; idx += 288) {
-      const int r = idx & 127, chunk = idx >> 7;  // chunk: buffer (2) x K-block (2) x 16 B (8)
-      const int e = (r & 31) * 4 + (r >> 5);
-      if (e >= it.n_rows)
-        *reinterpret_cast<uint4*>(smem + L::P_OFF + (chunk >> 3) * (TC_ROWS * 128) + r * 128 + (chunk & 7) * 16) =
-            make_uint4(0, 0, 0, 0);
     }
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     mbar_arrive(q_full);
