@@ -174,7 +174,7 @@ struct RowMeta {
 template <int NT, int MODE>
 __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0, float (&v)[16],
                                            int ep_t, EpiShared& sh, const RowMeta& rm,
-                                           const float* pre = nullptr) {
+                                           const float* pre = nullptr, const float2* cs_pre = nullptr) {
   const int m = tile * BM + ep_t;
   // ---- RMSNorm of the input rows (X was the raw residual stream) ----
   if (p.in_ssq != nullptr) {
@@ -240,12 +240,14 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
       const int i = (m - base) % hd;
       const int head = (m - base) / hd;
       __nv_bfloat16* pages = region == 1 ? p.k_pages : p.v_pages;
-      // RoPE factors of all 16 rows loaded up front (one round trip, not one per row)
+      // RoPE factors of all 16 rows loaded up front (one round trip, not one per row), or
+      // already prefetched by the caller while the tile was streaming
       float2 csv[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int n = n0 + j;
-        csv[j] = (region < 2 && n < p.n_rows && rm.kind[n] >= 0)
+        csv[j] = cs_pre != nullptr ? cs_pre[j]
+                 : (region < 2 && n < p.n_rows && rm.kind[n] >= 0)
                      ? __ldg(p.rope + (size_t)rm.pos[n] * (hd >> 1) + (i >> 1))
                      : make_float2(1.f, 0.f);
       }
@@ -681,6 +683,20 @@ __global__ void __launch_bounds__(256, 1)
         for (int j = 0; j < 16; ++j)
           pre[j] = (j < p.n_rows && rm.kind[j] >= 0) ? __ldcg(p.resid + (size_t)(p.row0 + j) * p.M + m) : 0.f;
       }
+      // likewise the RoPE factors of the first 16 rows (the table lines are evicted by the
+      // weight stream between layers: an HBM round trip under load)
+      float2 cs_pre[MODE == EPI_QKV ? 16 : 1];
+      if constexpr (MODE == EPI_QKV) {
+        const int m = t * BM + ep_t;
+        const int region = m < p.q_dim ? 0 : (m < p.q_dim + p.kv_dim ? 1 : 2);
+        const int base = region == 0 ? 0 : (region == 1 ? p.q_dim : p.q_dim + p.kv_dim);
+        const int i = (m - base) % p.head_dim;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          cs_pre[j] = (region < 2 && j < p.n_rows && rm.kind[j] >= 0)
+                          ? __ldg(p.rope + (size_t)rm.pos[j] * (p.head_dim >> 1) + (i >> 1))
+                          : make_float2(1.f, 0.f);
+      }
       mbar_wait(tmem_full, tphase);
       tc_fence_after();
       if (ep_t == 0) stamp(13);
@@ -805,7 +821,8 @@ __global__ void __launch_bounds__(256, 1)
           }
           if (ep_t == 0 && cc == 0) stamp(10);
           const float* prow = PIPE ? (MODE == EPI_RESID ? cpre : nullptr) : ((have_pre && cc == 0) ? pre : nullptr);
-          finalize16<NT, MODE>(p, t, cc * 16, v, ep_t, sh, rm, prow);
+          finalize16<NT, MODE>(p, t, cc * 16, v, ep_t, sh, rm, prow,
+                               (MODE == EPI_QKV && cc == 0) ? cs_pre : nullptr);
           if (ep_t == 0 && cc == 0) stamp(11);
         }
         if (nseg == 1) {
