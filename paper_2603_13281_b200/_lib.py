@@ -81,7 +81,7 @@ def load():
         "icr_gemm_bf16": [p, p, p, i, i, i, p],
         "icr_bench_attention": [p, p, p, i, i, i, i, i, C.POINTER(C.c_int32),
                                 C.POINTER(C.c_int32), C.POINTER(C.c_int32), i, i, p, p,
-                                C.c_longlong, i, C.POINTER(C.c_float), C.POINTER(C.c_int32), p],
+                                C.c_longlong, i, i, C.POINTER(C.c_float), C.POINTER(C.c_int32), p],
         "icr_paged_attention": [p, p, p, i, i, i, i, i, C.POINTER(C.c_int32),
                                 C.POINTER(C.c_int32), C.POINTER(C.c_int32), i, i, p,
                                 C.POINTER(C.c_int32), p],

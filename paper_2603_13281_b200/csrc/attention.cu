@@ -358,8 +358,10 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
 // then start streaming its weights while the merge runs.
 constexpr int MERGE_THREADS = 128;
 
-template <int HD>
-__global__ void __launch_bounds__(MERGE_THREADS, 5)  // <= 96 registers: fits beside a GEMM CTA
+// MB chunks per batch: 12 (<= 96 registers, fits beside a GEMM CTA) when every row has at
+// most 12 chunks (decode steps), else 24 (long contexts: fewer round trips).
+template <int HD, int MB>
+__global__ void __launch_bounds__(MERGE_THREADS, MB <= 12 ? 5 : 1)
     attn_merge_kernel(const float* __restrict__ part_o, const float2* __restrict__ part_ml,
                       const int* __restrict__ row_pos, const int* __restrict__ row_kind,
                       int num_heads, int group, int max_chunks, int chunk_tokens,
@@ -375,7 +377,7 @@ __global__ void __launch_bounds__(MERGE_THREADS, 5)  // <= 96 registers: fits be
   if (trace != nullptr && threadIdx.x == 0 && cta_id < 4096) trace[(size_t)cta_id * 16 + 7] = globaltimer();
   if (kind < 0) return;
   // The (m, l) loads of one head are the same address across its threads (broadcast).
-  constexpr int MB = 12, V = HD / 4;
+  constexpr int V = HD / 4;
   for (int idx = threadIdx.x; idx < group * V; idx += blockDim.x) {
     const int hg = idx / V, d = (idx % V) * 4;
     const int head = g * group + hg;
@@ -427,6 +429,14 @@ __global__ void __launch_bounds__(MERGE_THREADS, 5)  // <= 96 registers: fits be
   if (trace != nullptr && threadIdx.x == 0 && cta_id < 4096) trace[(size_t)cta_id * 16 + 5] = globaltimer();
 }
 
+// MB = 12 (<= 96 registers: a merge CTA shares an SM with the next kernel's CTA) when every
+// row has at most 12 chunks -- decode steps at moderate context; 24 (one round trip fewer)
+// for long contexts
+template <int HD>
+static auto merge_kernel(int max_chunks) {
+  return max_chunks > 12 ? attn_merge_kernel<HD, 24> : attn_merge_kernel<HD, 12>;
+}
+
 static bool use_tc(int head_dim) {
   static const bool mma_only = getenv("ICR_ATTN_MMA") != nullptr;
   return head_dim == 128 && !mma_only;
@@ -440,7 +450,8 @@ static cudaError_t attn_launch_hd(const AttnLaunch& a, cudaStream_t s) {
     cudaError_t e = attn_tc_partial_launch(a, a.chunk_tokens / 16, s);
     if (e != cudaSuccess) return e;
     const int mthreads = std::min(MERGE_THREADS, ((a.group * HD / 4 + 31) / 32) * 32);
-    return launch_pdl(attn_merge_kernel<HD>, dim3(a.n_rows, a.num_kv_heads), dim3(mthreads), 0, s,
+    return launch_pdl(merge_kernel<HD>(a.max_chunks),
+                      dim3(a.n_rows, a.num_kv_heads), dim3(mthreads), 0, s,
                       a.part_o, a.part_ml, a.row_pos, a.row_kind, a.num_heads, a.group,
                       a.max_chunks, a.chunk_tokens, a.out, a.out_ld,
                       a.trace ? a.trace + 4096 * 16 : nullptr);
@@ -460,7 +471,8 @@ static cudaError_t attn_launch_hd(const AttnLaunch& a, cudaStream_t s) {
                              a.scale, a.part_o, a.part_ml, a.n_items_dev, a.pf_base, a.pf_bytes, a.trace);
   if (e != cudaSuccess) return e;
   const int mthreads = std::min(MERGE_THREADS, ((a.group * HD / 4 + 31) / 32) * 32);
-  return launch_pdl(attn_merge_kernel<HD>, dim3(a.n_rows, a.num_kv_heads), dim3(mthreads), 0, s,
+  return launch_pdl(merge_kernel<HD>(a.max_chunks),
+                    dim3(a.n_rows, a.num_kv_heads), dim3(mthreads), 0, s,
                     a.part_o, a.part_ml, a.row_pos, a.row_kind, a.num_heads, a.group,
                     a.max_chunks, a.chunk_tokens, a.out, a.out_ld,
                     a.trace ? a.trace + 4096 * 16 : nullptr);

@@ -342,23 +342,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (r == 0 && half == 0) sstamp(j, 5);
         // P buffer b was last read by P.V(j - 2)
         if (j >= 2) mbar_wait(&p_free[b], ((j >> 1) - 1) & 1);
-        if (j > 0 && __any_sync(0xffffffffu, valid && corr != 1.f)) {
-          // the max moved: rescale this half's 64 O columns once P.V(j - 1) has landed
-          mbar_wait(o_done, (j - 1) & 1);
-          tc_fence_after();
-          uint32_t o[4][16];
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) tmem_ld16_nowait(tmem_o + lane_base + half * 64 + q4 * 16, o[q4]);
-          tmem_wait_ld();
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) {
-            tmem_reg_fence(o[q4]);
-#pragma unroll
-            for (int jj = 0; jj < 16; ++jj) o[q4][jj] = __float_as_uint(__uint_as_float(o[q4][jj]) * corr);
-            tmem_st16(tmem_o + lane_base + half * 64 + q4 * 16, o[q4]);
-          }
-          asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-        }
         if (r == 0 && half == 0) sstamp(j, 6);
         const long long clk0 = clock64();
         uint8_t* rowp0 = smem + L::P_OFF + b * L::P_BYTES + half * (TC_ROWS * 128) + r * 128;
@@ -401,6 +384,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         m_run = m_new;
         if (trace != nullptr && cta_id == 0 && r == 0 && half == 0 && j < 256)
           trace[(size_t)2 * 4096 * 16 + j * 8 + 7] = (unsigned long long)(clock64() - clk0);
+        if (j > 0 && __any_sync(0xffffffffu, valid && corr != 1.f)) {
+          // the max moved: rescale this half's 64 O columns once P.V(j - 1) has landed
+          mbar_wait(o_done, (j - 1) & 1);
+          tc_fence_after();
+          uint32_t o[4][16];
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) tmem_ld16_nowait(tmem_o + lane_base + half * 64 + q4 * 16, o[q4]);
+          tmem_wait_ld();
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            tmem_reg_fence(o[q4]);
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) o[q4][jj] = __float_as_uint(__uint_as_float(o[q4][jj]) * corr);
+            tmem_st16(tmem_o + lane_base + half * 64 + q4 * 16, o[q4]);
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        }
         tc_fence_before();
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         mbar_arrive(p_full);

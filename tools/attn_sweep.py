@@ -19,15 +19,20 @@ import numpy as np
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 
-def run(ctx, n_adapters, chunk_pages, iters=5):
+def run(ctx, n_adapters, chunk_pages, iters=5, pipelined=False):
+    """pipelined: `iters` launches back to back alternating between two copies of the K/V
+    (each larger than L2 at 32K), no flush -- the attention as it runs inside a decode step,
+    its page loads overlapping the previous launch's tail. Otherwise L2 is flushed and every
+    launch is timed alone."""
     import torch
     from paper_2603_13281_b200 import _lib
     lib = _lib.load()
     H, Hkv, hd = 32, 8, 128
     shared_pages = ctx // 16
     n_pages = shared_pages + n_adapters * 2
-    kp = torch.randn(n_pages, Hkv, 16, hd, device="cuda").to(torch.bfloat16)
-    vp = torch.randn(n_pages, Hkv, 16, hd, device="cuda").to(torch.bfloat16)
+    copies = 2 if pipelined else 1
+    kp = torch.randn(copies * n_pages, Hkv, 16, hd, device="cuda").to(torch.bfloat16)
+    vp = torch.randn(copies * n_pages, Hkv, 16, hd, device="cuda").to(torch.bfloat16)
     mpps = shared_pages + 2
     bt = np.full((n_adapters, mpps), -1, np.int32)
     for s in range(n_adapters):
@@ -37,20 +42,25 @@ def run(ctx, n_adapters, chunk_pages, iters=5):
     rows_pos = np.full(2 * n_adapters, ctx, np.int32)
     q = torch.randn(2 * n_adapters, H * hd, device="cuda").to(torch.bfloat16)
     out = torch.empty_like(q)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush = None if pipelined else torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    if pipelined:
+        iters = max(iters, 20)
     ms = C.c_float()
     nitems = np.zeros(1, np.int32)
     _lib.check(lib.icr_bench_attention(
         q.data_ptr(), kp.data_ptr(), vp.data_ptr(), H, Hkv, hd, chunk_pages, 2 * n_adapters,
         _lib.i32_ptr(rows_seq), _lib.i32_ptr(rows_pos), _lib.i32_ptr(bt), n_adapters, mpps,
-        out.data_ptr(), flush.data_ptr(), flush.numel(), iters, C.byref(ms), _lib.i32_ptr(nitems),
+        out.data_ptr(), flush.data_ptr() if flush is not None else None,
+        flush.numel() if flush is not None else 0, iters, n_pages if pipelined else 0,
+        C.byref(ms), _lib.i32_ptr(nitems),
         _lib.stream_handle()))
     kv_bytes = (ctx + 1) * Hkv * hd * 2 * 2 + (n_adapters - 1) * Hkv * hd * 2 * 2
     gbs = kv_bytes / (ms.value / 1e3) / 1e9
     del kp, vp, flush
     torch.cuda.empty_cache()
     return {"context": ctx, "adapters": n_adapters, "ms": ms.value, "unique_kv_bytes": kv_bytes,
-            "gbs": gbs, "items": int(nitems[0]), "chunk_pages": chunk_pages}
+            "gbs": gbs, "items": int(nitems[0]), "chunk_pages": chunk_pages,
+            "mode": "pipelined" if pipelined else "cold"}
 
 
 def main():
@@ -59,9 +69,10 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--ctx", type=int, default=0, help="single config (profiling)")
     ap.add_argument("--adapters", type=int, default=8)
+    ap.add_argument("--pipelined", action="store_true")
     args = ap.parse_args()
     if args.ctx:
-        print(json.dumps(run(args.ctx, args.adapters, args.chunk_pages, iters=1)))
+        print(json.dumps(run(args.ctx, args.adapters, args.chunk_pages, iters=1, pipelined=args.pipelined)))
         return
     peak = json.loads((Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]
     res = []
