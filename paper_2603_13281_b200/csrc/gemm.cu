@@ -380,23 +380,34 @@ __device__ __forceinline__ void lora_shrink_tasks(const GemmParams& p, int gwarp
           p.sh_part[(size_t)ks * p.rows_total * 2 * p.rank + slot] = acc;
       }
     }
-    if (splits > 1 && lane == 0) {
-      int* cnt = p.sh_cnt + combo;
-      if (atom_add_acq_rel(cnt, 1) == splits - 1) {
+    if (splits > 1) {
+      // the last split to arrive folds every split of every row of the segment: lanes cover
+      // (row, split) pairs -- all loads in flight at once -- and the split sums are gathered
+      // to the row's first lane and added in split order
+      int last = 0;
+      if (lane == 0) last = atom_add_acq_rel(p.sh_cnt + combo, 1) == splits - 1;
+      if (__shfl_sync(0xffffffffu, last, 0)) {
+        fence_acq_rel_gpu();  // every lane reads the other splits' partials
+        const int per = 32 / splits;  // rows per pass (splits <= 32)
+        const int q = lane % splits, g0 = (lane / splits) * splits;
 #pragma unroll 1
-        for (int rr = r0; rr < r1; ++rr) {
-          const int gr = s_rows[rr];
-          if (gr < p.row0 || gr >= p.row0 + p.n_rows) continue;
-          const size_t slot = ((size_t)gr * 2 + t) * p.rank + j;
-          float s = 0.f;
+        for (int rb = r0; rb < r1; rb += per) {
+          const int rr = rb + lane / splits;
+          const int gr = (lane < per * splits && rr < r1) ? s_rows[rr] : -1;
+          const bool act = gr >= p.row0 && gr < p.row0 + p.n_rows;
+          const size_t slot = act ? ((size_t)gr * 2 + t) * p.rank + j : 0;
+          const float v = act ? __ldcg(p.sh_part + (size_t)q * p.rows_total * 2 * p.rank + slot) : 0.f;
+          float sum = 0.f;
 #pragma unroll 1
-          for (int q = 0; q < splits; ++q)
-            s = (q == 0) ? __ldcg(p.sh_part + slot)
-                         : __fadd_rn(s, __ldcg(p.sh_part + (size_t)q * p.rows_total * 2 * p.rank + slot));
-          p.ubd[(size_t)gr * p.ubd_ld + (size_t)t * p.slots * p.rank + a * p.rank + j] =
-              __float2bfloat16_rn(s);
+          for (int qq = 0; qq < splits; ++qq) {
+            const float x = __shfl_sync(0xffffffffu, v, min(g0 + qq, 31));
+            sum = qq == 0 ? x : __fadd_rn(sum, x);
+          }
+          if (act && q == 0)
+            p.ubd[(size_t)gr * p.ubd_ld + (size_t)t * p.slots * p.rank + a * p.rank + j] =
+                __float2bfloat16_rn(sum);
         }
-        *cnt = 0;
+        if (lane == 0) p.sh_cnt[combo] = 0;
       }
     }
   }

@@ -46,6 +46,7 @@ class PageArena:
         self.k = torch.zeros(shape, dtype=torch.bfloat16, device=device)
         self.v = torch.zeros(shape, dtype=torch.bfloat16, device=device)
         self.refs = np.zeros(num_pages, dtype=np.int32)
+        self.gen = np.zeros(num_pages, dtype=np.int64)  # bumped per allocation: page identity
         self._free = list(range(num_pages - 1, -1, -1))
 
     @classmethod
@@ -68,6 +69,7 @@ class PageArena:
             raise CapacityError(f"KV page arena exhausted ({self.num_pages} pages)")
         pid = self._free.pop()
         self.refs[pid] = 1
+        self.gen[pid] += 1
         return pid
 
     def incref(self, pid: int) -> None:
@@ -84,6 +86,32 @@ class PageArena:
 
     def refcount(self, pid: int) -> int:
         return int(self.refs[pid])
+
+    # swap (pool eviction policy "swap", src/kvpool.py:282-356) ----------------------
+    def save_page(self, pid: int):
+        """Copy page pid's K/V (every layer) into host memory -- pinned, queued on the current
+        stream, so a later writer of the recycled page is ordered after the copy."""
+        torch = _torch()
+        pin = self.k.is_cuda
+        shape = (self.config.num_layers, self.config.num_kv_heads, BLOCK_TOKENS, self.config.head_dim)
+        kh = torch.empty(shape, dtype=torch.bfloat16, pin_memory=pin)
+        vh = torch.empty(shape, dtype=torch.bfloat16, pin_memory=pin)
+        kh.copy_(self.k[:, pid], non_blocking=pin)
+        vh.copy_(self.v[:, pid], non_blocking=pin)
+        return kh, vh
+
+    def load_page(self, pid: int, saved) -> None:
+        """Inverse of save_page into (freshly allocated) page pid."""
+        self.k[:, pid].copy_(saved[0], non_blocking=True)
+        self.v[:, pid].copy_(saved[1], non_blocking=True)
+
+    def host_rows(self, saved, layer: int):
+        """[16, Hkv, hd] float K and V rows of one layer of a saved page."""
+        torch = _torch()
+        if self.k.is_cuda:
+            torch.cuda.current_stream().synchronize()  # the D2H copy was queued asynchronously
+        return (saved[0][layer].transpose(0, 1).float().numpy(),
+                saved[1][layer].transpose(0, 1).float().numpy())
 
     # host-side row access (tests, copy-in, fingerprints) --------------------------
     def _index(self, pages, start, stop):

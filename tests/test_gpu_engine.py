@@ -261,3 +261,44 @@ def test_session_guards_and_ledger(cuda):
     assert q.ledger.param_matrix_reads - (7 * L + 1) == 6 * (7 * L + 5 * L + 1)
     assert f.ledger.kv_bytes_written == 11 * bpt
     assert f.ledger.kv_bytes_read == sum(p + 1 for p in range(5, 11)) * bpt
+
+
+@pytest.mark.gpu
+def test_swap_eviction_moves_pages_to_host_and_back_bitwise(c1_setup):
+    """Pool eviction policy "swap" on the device arena: the evicted prefix's pages go back to
+    the arena while their K/V wait in pinned host memory; a later hit swaps them into fresh
+    pages byte for byte, and the reader decodes bitwise like a cold session."""
+    E, P, M = _mods()
+    base, agents, rt = c1_setup
+    rng = np.random.default_rng(11)
+    prompt = [int(t) for t in rng.integers(1, 1024, 64)]
+    pool = P.KvCachePool(base.config, 64 << 20, "icarus", eviction="swap", swap_budget_bytes=64 << 20)
+    writer = E.new_session(base, None, 256, runtime=rt)
+    first = E.prefill(writer, prompt)
+    blocks = pool.commit(None, prompt, writer.cache, next_token_fn=lambda p: E.base_next_token_at(writer, p))
+    arena = writer.cache.arena
+    pages = [b.page for b in blocks]
+    raw = [arena.read_raw(layer, pages, 0, 64) for layer in range(base.config.num_layers)]
+    writer.close()
+    free0 = arena.free_pages()
+    in_use = pool.budget.in_use
+    assert pool.evict(in_use) == in_use
+    assert all(b.residency == "swapped" and b.page == -1 for b in blocks)
+    assert arena.free_pages() == free0 + len(blocks)
+    # recycle the freed pages so the swap-in cannot find its old pages intact
+    filler = E.new_session(base, None, 256, runtime=rt)
+    E.prefill(filler, [int(t) for t in rng.integers(1, 1024, 64)])
+    reader = E.new_session(base, agents[1], 256, runtime=rt, capture_logits=True)
+    cold = E.new_session(base, agents[1], 256, runtime=rt, capture_logits=True)
+    t = E.prefill(reader, prompt, pool=pool, reader="x")
+    tc = E.prefill(cold, prompt)
+    assert t == tc == first
+    assert pool.counters["swap_in_blocks"] == len(blocks)
+    new_pages = reader.cache.pages[:len(blocks)]
+    assert [arena.read_raw(layer, new_pages, 0, 64) for layer in range(base.config.num_layers)] == raw
+    for _ in range(4):
+        t, tc = E.decode_step_fused(reader, t), E.decode_step_fused(cold, tc)
+        assert t == tc and reader.last_logits.tobytes() == cold.last_logits.tobytes()
+    pool.release(reader.borrowed_chain)
+    for s in (filler, reader, cold):
+        s.close()
