@@ -302,3 +302,28 @@ def test_swap_eviction_moves_pages_to_host_and_back_bitwise(c1_setup):
     pool.release(reader.borrowed_chain)
     for s in (filler, reader, cold):
         s.close()
+
+
+@pytest.mark.gpu
+def test_checkpointed_base_and_adapter_drive_the_decode_bitwise(c1_setup, tmp_path):
+    """§8 f-4: a base and an adapter written as `icarus-ckpt 1` containers and loaded back
+    (base memory-mapped, freeze hash re-verified) decode bitwise like the in-memory ones."""
+    from paper_2603_13281_b200 import checkpoint as CK
+    E, P, M = _mods()
+    base, agents, rt = c1_setup
+    CK.save_base(tmp_path / "base.ckpt", base)
+    CK.save_adapters(tmp_path / "agent1.ckpt", agents[1])
+    base2 = CK.load_base(tmp_path / "base.ckpt", mmap=True)
+    agent2 = CK.load_adapters(tmp_path / "agent1.ckpt")
+    assert base2.freeze_hash == base.freeze_hash
+    rt2 = base2.runtime(max_seqs=4, max_context=256, max_rows=16, adapter_slots=2, lora_rank=8)
+    prompt = [int(t) for t in np.random.default_rng(21).integers(1, 1024, 40)]
+    a = E.new_session(base, agents[1], 256, runtime=rt, capture_logits=True)
+    b = E.new_session(base2, agent2, 256, runtime=rt2, capture_logits=True)
+    ta, tb = E.prefill(a, prompt), E.prefill(b, prompt)
+    assert ta == tb
+    for _ in range(6):
+        ta, tb = E.decode_step_fused(a, ta), E.decode_step_fused(b, tb)
+        assert ta == tb and a.last_logits.tobytes() == b.last_logits.tobytes()
+    a.close()
+    b.close()
