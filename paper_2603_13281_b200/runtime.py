@@ -365,13 +365,26 @@ class AdapterSlots:
 
 
 # ----------------------------------------------------------------------------- runtime
+def auto_chunk_pages(max_context: int) -> int:
+    """Attention work-item length for a runtime serving contexts up to max_context: the
+    smallest of 16 / 32 / 64 / 128 pages that splits a full context into at most 16 chunks
+    (enough (chunk, KV head) items to fill the SMs, few enough that each item amortises its
+    start-up over several sub-chunks). Fixed per runtime, so a row's attention never depends
+    on which other rows share its step."""
+    pages = -(-max_context // BLOCK_TOKENS)
+    cp = 16
+    while cp < 128 and cp * 16 < pages:
+        cp *= 2
+    return cp
+
+
 class Runtime:
     """The device side of one BaseWeights: page arena, adapter slots, block table and the
     C model handle. Sessions borrow a block-table row (sequence slot) each."""
 
     def __init__(self, base, max_seqs: int = 64, max_context: int = 4096,
                  num_pages: Optional[int] = None, max_rows: int = 512, adapter_slots: int = 8,
-                 lora_rank: int = 16, chunk_pages: int = 16, device="cuda"):
+                 lora_rank: int = 16, chunk_pages: Optional[int] = None, device="cuda"):
         torch = _torch()
         if not torch.cuda.is_available():
             raise DeviceError("no CUDA device: the B200 path has no CPU fallback")
@@ -386,6 +399,8 @@ class Runtime:
         if num_pages is None:
             num_pages = min(max_seqs * self.max_pages_per_seq, 1 << 16)
         self.max_rows = max_rows
+        if chunk_pages is None:
+            chunk_pages = auto_chunk_pages(max_context)
         self.chunk_pages = chunk_pages
         self.dw = base.device(device)
         self.arena = PageArena(cfg, num_pages, device)

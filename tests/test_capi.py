@@ -39,3 +39,17 @@ def test_status_codes_map_to_reference_exceptions():
 def test_sources_target_sm100a_only():
     from paper_2603_13281_b200 import build
     assert build.ARCH == ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def test_auto_chunk_pages_rule():
+    """Attention chunk length chosen per runtime from its context capacity (fixed per runtime:
+    batch invariance): C1/C2 contexts keep 16-page chunks, the 8k-prefix workflow (C3) gets
+    64, the 32k context (C4) 128."""
+    from paper_2603_13281_b200.runtime import auto_chunk_pages
+    assert auto_chunk_pages(1024) == 16
+    assert auto_chunk_pages(2418) == 16      # bench.py C2 capacity
+    assert auto_chunk_pages(4096) == 16
+    assert auto_chunk_pages(4112) == 32
+    assert auto_chunk_pages(8976) == 64      # C3 workflow capacity
+    assert auto_chunk_pages(32800) == 128
+    assert auto_chunk_pages(1 << 20) == 128

@@ -7,7 +7,7 @@ from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 
-def main(n=64, prefix=8192):
+def main(n=64, prefix=8192, chunk_pages=None):
     import numpy as np
     import torch
     import bench
@@ -20,7 +20,7 @@ def main(n=64, prefix=8192):
     ads = [AdapterSet.on_device(cfg, 16, 32.0, seed=1 + i) for i in range(8)]
     ctx = prefix + 256
     rt = base.runtime(max_seqs=n + 2, max_context=ctx, max_rows=512, adapter_slots=8, lora_rank=16,
-                      num_pages=prefix // 16 + n * 24 + 32)
+                      num_pages=prefix // 16 + n * 24 + 32, chunk_pages=chunk_pages)
     pool = KvCachePool(cfg, 64 << 30, "icarus")
     prompt = [int(t) for t in np.random.default_rng(0).integers(1, cfg.vocab_size, prefix)]
     ss = [E.new_session(base, ads[i % 8], ctx, runtime=rt) for i in range(n)]
@@ -42,9 +42,11 @@ def main(n=64, prefix=8192):
         _lib.check(rt._lib.icr_profile_ablate(rt._handle, 1 << k, 10, C.byref(avg), _lib.stream_handle()))
         out[nm] = round(full - avg.value, 3)
     print("in-graph marginal ms:", out)
-    if len(sys.argv) > 1:
-        _lib.check(rt._lib.icr_profile_trace(rt._handle, sys.argv[1].encode(), _lib.stream_handle()))
+    trace = [a for a in sys.argv[1:] if not a.startswith("--")]
+    if trace:
+        _lib.check(rt._lib.icr_profile_trace(rt._handle, trace[0].encode(), _lib.stream_handle()))
 
 
 if __name__ == "__main__":
-    main()
+    cp = [int(a.split("=")[1]) for a in sys.argv[1:] if a.startswith("--chunk-pages=")]
+    main(chunk_pages=cp[0] if cp else None)

@@ -21,7 +21,7 @@ def main():
     ap.add_argument("--requests", type=int, default=64)
     ap.add_argument("--prefix", type=int, default=8192)
     ap.add_argument("--layers", type=int, default=32)
-    ap.add_argument("--chunk-pages", type=int, default=16)
+    ap.add_argument("--chunk-pages", type=int, default=None, help="default: the runtime's auto rule")
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
     import torch
@@ -59,7 +59,7 @@ def main():
         "turns": rep.turns, "decode_steps": rep.decode_steps, "decoder_tokens": rep.decoder_tokens,
         "prefill_tokens": rep.prefill_tokens, "prefix_hit_tokens": rep.prefix_hit_tokens,
         "cross_model_hit_tokens": rep.cross_model_hit_tokens, "max_live": rep.max_live,
-        "max_context": max_ctx, "chunk_pages": args.chunk_pages,
+        "max_context": max_ctx, "chunk_pages": rt.chunk_pages,
     }
     print(json.dumps(line), flush=True)
     if args.out:
