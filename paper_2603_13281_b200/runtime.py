@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from typing import Optional
 
 import numpy as np
@@ -399,8 +400,8 @@ class Runtime:
         if num_pages is None:
             num_pages = min(max_seqs * self.max_pages_per_seq, 1 << 16)
         self.max_rows = max_rows
-        if chunk_pages is None:
-            chunk_pages = auto_chunk_pages(max_context)
+        if chunk_pages is None:  # ICR_CHUNK_PAGES: tuning sweeps only (tools/)
+            chunk_pages = int(os.environ.get("ICR_CHUNK_PAGES", 0)) or auto_chunk_pages(max_context)
         self.chunk_pages = chunk_pages
         self.dw = base.device(device)
         self.arena = PageArena(cfg, num_pages, device)
