@@ -141,6 +141,7 @@ __device__ __forceinline__ void warp_argmax16(const float (&v)[16], int idx, int
 struct EpiShared {
   int flag;
   int shrink_ready;
+  int fin_last;  // the epilogue's finalize decision for the CTA's last tile (helpers read it)
   float red_val[64];
   int red_idx[64];
 };
@@ -173,7 +174,7 @@ struct RowMeta {
 
 template <int NT, int MODE>
 __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0, float (&v)[16],
-                                           int ep_t, EpiShared& sh, const RowMeta& rm,
+                                           int ep_t, EpiShared& sh, const RowMeta& rm, int bar,
                                            const float* pre = nullptr, const float2* cs_pre = nullptr) {
   const int m = tile * BM + ep_t;
   // ---- RMSNorm of the input rows (X was the raw residual stream) ----
@@ -213,7 +214,7 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
       }
       const float wsum = warp_reduce16(sq, ln);
       if ((ln & 1) == 0) sh.red_val[wq * 16 + ((ln >> 1) & 15)] = wsum;
-      named_bar_sync(1, 128);
+      named_bar_sync(bar, 128);
       if (ep_t < 16) {
         const int n = n0 + ep_t;
         if (n < p.n_rows) {
@@ -222,7 +223,7 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
           p.out_ssq[(size_t)tile * p.ss_stride + p.row0 + n] = s;
         }
       }
-      named_bar_sync(1, 128);
+      named_bar_sync(bar, 128);
   } else if constexpr (MODE == EPI_SILU) {
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
@@ -282,7 +283,7 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
       int bi;
       warp_argmax16(vals, m, ln, bv, bi);
       if ((ln & 1) == 0) { sh.red_val[wq * 16 + ((ln >> 1) & 15)] = bv; sh.red_idx[wq * 16 + ((ln >> 1) & 15)] = bi; }
-      named_bar_sync(1, 128);
+      named_bar_sync(bar, 128);
       if (ep_t < 16) {
         float val = sh.red_val[ep_t];
         int idx = sh.red_idx[ep_t];
@@ -296,7 +297,7 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
           p.tile_best[(size_t)tile * p.best_stride + p.row0 + n] =
               make_float2(val, __int_as_float(idx));
       }
-      named_bar_sync(1, 128);
+      named_bar_sync(bar, 128);
   }
 }
 
@@ -493,6 +494,114 @@ __global__ void __launch_bounds__(256, 1)
   pdl_launch();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) stamp(0);
+  // Finalization of 16-column chunks [cc0, cc1) of tile t by one 128-thread group (thread
+  // ep_t owns output feature t * 128 + ep_t; TMEM lane quarter = warp % 4): fold the stream-K
+  // partials in segment order (or read the accumulator when the tile is this CTA's alone) and
+  // run the fused epilogue. Wide launches software-pipeline it: the next chunk's first PF
+  // partials and residual rows are requested before the current chunk is folded.
+  auto fin_chunks = [&](int t, int cc0, int cc1, int ep_t, EpiShared& shx, int bar, const float* pre0,
+                        const float2* cs0) {
+    const long long t0 = (long long)t * sp.Ut;
+    const int c_first = sp.owner(t0), c_last = sp.owner(t0 + sp.Ut - 1);
+    const int nseg = c_last - c_first + 1;
+    const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+    const bool stamps = ep_t == 0 && bar == 1;
+      constexpr int PF = NT > 16 ? 2 : 1;
+      constexpr bool PIPE = NT > 16;
+      float4 nb[PF][4];
+      float npre[16];
+      auto seg_src = [&](int s, int cc) {
+        const int cs = c_first + s;
+        const int sl = (sp.ubegin(cs) >= t0) ? 0 : 1;  // tile t is cs's first tile
+        return reinterpret_cast<const float4*>(p.ws + (((size_t)cs * 2 + sl) * BM + ep_t) * NT + cc * 16);
+      };
+      auto fetch = [&](int cc) {
+        if (nseg > 1) {
+#pragma unroll
+          for (int s = 0; s < PF; ++s)
+            if (s < nseg) {
+              const float4* src = seg_src(s, cc);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) nb[s][q] = __ldcg(src + q);
+            }
+        }
+        if (MODE == EPI_RESID) {
+          const int m = t * BM + ep_t;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int n = cc * 16 + j;
+            npre[j] = (n < p.n_rows) ? __ldcg(p.resid + (size_t)(p.row0 + n) * p.M + m) : 0.f;
+          }
+        }
+      };
+      if (PIPE) fetch(cc0);
+#pragma unroll 1
+      for (int cc = cc0; cc < cc1; ++cc) {
+        float4 cb[PF][4];
+        float cpre[16];
+        if (PIPE) {
+#pragma unroll
+          for (int s = 0; s < PF; ++s)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) cb[s][q] = nb[s][q];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) cpre[j] = npre[j];
+          if (cc + 1 < cc1) fetch(cc + 1);
+        }
+        float v[16];
+        if (nseg == 1) {
+          tmem_ld16(tmem_base + lane_base + cc * 16, v);
+        } else {
+          // segments [0, PF) were prefetched (wide launches); the rest are loaded SEG_BATCH
+          // at a time with every load of a batch issued before its first add
+          constexpr int SEG_BATCH = 4;
+          const int s_start = PIPE ? min(PF, nseg) : 0;
+          if (PIPE) {
+#pragma unroll
+            for (int s = 0; s < PF; ++s)
+              if (s < nseg) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const float x[4] = {cb[s][q].x, cb[s][q].y, cb[s][q].z, cb[s][q].w};
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) v[4 * q + e] = (s == 0) ? x[e] : __fadd_rn(v[4 * q + e], x[e]);
+                }
+              }
+          }
+#pragma unroll 1
+          for (int s0 = s_start; s0 < nseg; s0 += SEG_BATCH) {
+            float4 buf[SEG_BATCH][4];
+#pragma unroll
+            for (int s = 0; s < SEG_BATCH; ++s) {
+              if (s0 + s < nseg) {
+                const float4* src = seg_src(s0 + s, cc);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) buf[s][q] = __ldcg(src + q);
+              }
+            }
+#pragma unroll
+            for (int s = 0; s < SEG_BATCH; ++s) {
+              if (s0 + s < nseg) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const float x[4] = {buf[s][q].x, buf[s][q].y, buf[s][q].z, buf[s][q].w};
+#pragma unroll
+                  for (int e = 0; e < 4; ++e)
+                    v[4 * q + e] = (s0 + s == 0) ? x[e] : __fadd_rn(v[4 * q + e], x[e]);
+                }
+              }
+            }
+          }
+        }
+        if (stamps && cc == 0) stamp(10);
+        const float* prow = PIPE ? (MODE == EPI_RESID ? cpre : nullptr) : (cc == 0 ? pre0 : nullptr);
+        finalize16<NT, MODE>(p, t, cc * 16, v, ep_t, shx, rm, bar, prow,
+                             (MODE == EPI_QKV && cc == 0) ? cs0 : nullptr);
+        if (stamps && cc == 0) stamp(11);
+      }
+  };
+  constexpr bool HELPERS = NT >= 32;
+
   // pull the NEXT projection's adapter A matrices into L2 so its shrink loads hit L2
 
   if (warp == 0) {
@@ -739,103 +848,16 @@ __global__ void __launch_bounds__(256, 1)
         fin = (sh.flag == nseg - 1);
         named_bar_sync(1, 128);
       }
+      // wide launches: warps 0-3 (their roles are over once the last tile's MMAs are issued)
+      // finalize the upper half of the last tile's 16-column chunks
+      const bool helped = HELPERS && t == t_last;
+      if (helped) {
+        if (ep_t == 0) sh.fin_last = fin ? 1 : 0;
+        named_bar_sync(4, 256);
+      }
       if (fin) {
-        // Wide launches (NT > 16) software-pipeline the finalization: the next 16-column
-        // chunk's first PF partials and residual rows are requested before the current chunk
-        // is folded, so NT/16 chunks cost ~1 round trip instead of NT/16 of them.
-        constexpr int PF = NT > 16 ? 2 : 1;
-        constexpr bool PIPE = NT > 16;
-        float4 nb[PF][4];
-        float npre[16];
-        auto seg_src = [&](int s, int cc) {
-          const int cs = c_first + s;
-          const int sl = (sp.ubegin(cs) >= t0) ? 0 : 1;  // tile t is cs's first tile
-          return reinterpret_cast<const float4*>(p.ws + (((size_t)cs * 2 + sl) * BM + ep_t) * NT + cc * 16);
-        };
-        auto fetch = [&](int cc) {
-          if (nseg > 1) {
-#pragma unroll
-            for (int s = 0; s < PF; ++s)
-              if (s < nseg) {
-                const float4* src = seg_src(s, cc);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) nb[s][q] = __ldcg(src + q);
-              }
-          }
-          if (MODE == EPI_RESID) {
-            const int m = t * BM + ep_t;
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const int n = cc * 16 + j;
-              npre[j] = (n < p.n_rows) ? __ldcg(p.resid + (size_t)(p.row0 + n) * p.M + m) : 0.f;
-            }
-          }
-        };
-        if (PIPE) fetch(0);
-#pragma unroll 1
-        for (int cc = 0; cc < NT / 16; ++cc) {
-          float4 cb[PF][4];
-          float cpre[16];
-          if (PIPE) {
-#pragma unroll
-            for (int s = 0; s < PF; ++s)
-#pragma unroll
-              for (int q = 0; q < 4; ++q) cb[s][q] = nb[s][q];
-#pragma unroll
-            for (int j = 0; j < 16; ++j) cpre[j] = npre[j];
-            if (cc + 1 < NT / 16) fetch(cc + 1);
-          }
-          float v[16];
-          if (nseg == 1) {
-            tmem_ld16(tmem_base + lane_base + cc * 16, v);
-          } else {
-            // segments [0, PF) were prefetched (wide launches); the rest are loaded SEG_BATCH
-            // at a time with every load of a batch issued before its first add
-            constexpr int SEG_BATCH = 4;
-            const int s_start = PIPE ? min(PF, nseg) : 0;
-            if (PIPE) {
-#pragma unroll
-              for (int s = 0; s < PF; ++s)
-                if (s < nseg) {
-#pragma unroll
-                  for (int q = 0; q < 4; ++q) {
-                    const float x[4] = {cb[s][q].x, cb[s][q].y, cb[s][q].z, cb[s][q].w};
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) v[4 * q + e] = (s == 0) ? x[e] : __fadd_rn(v[4 * q + e], x[e]);
-                  }
-                }
-            }
-#pragma unroll 1
-            for (int s0 = s_start; s0 < nseg; s0 += SEG_BATCH) {
-              float4 buf[SEG_BATCH][4];
-#pragma unroll
-              for (int s = 0; s < SEG_BATCH; ++s) {
-                if (s0 + s < nseg) {
-                  const float4* src = seg_src(s0 + s, cc);
-#pragma unroll
-                  for (int q = 0; q < 4; ++q) buf[s][q] = __ldcg(src + q);
-                }
-              }
-#pragma unroll
-              for (int s = 0; s < SEG_BATCH; ++s) {
-                if (s0 + s < nseg) {
-#pragma unroll
-                  for (int q = 0; q < 4; ++q) {
-                    const float x[4] = {buf[s][q].x, buf[s][q].y, buf[s][q].z, buf[s][q].w};
-#pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                      v[4 * q + e] = (s0 + s == 0) ? x[e] : __fadd_rn(v[4 * q + e], x[e]);
-                  }
-                }
-              }
-            }
-          }
-          if (ep_t == 0 && cc == 0) stamp(10);
-          const float* prow = PIPE ? (MODE == EPI_RESID ? cpre : nullptr) : ((have_pre && cc == 0) ? pre : nullptr);
-          finalize16<NT, MODE>(p, t, cc * 16, v, ep_t, sh, rm, prow,
-                               (MODE == EPI_QKV && cc == 0) ? cs_pre : nullptr);
-          if (ep_t == 0 && cc == 0) stamp(11);
-        }
+        fin_chunks(t, 0, helped ? NT / 32 : NT / 16, ep_t, sh, 1, have_pre ? pre : nullptr, cs_pre);
+        if (helped) named_bar_sync(5, 256);
         if (nseg == 1) {
           tc_fence_before();
           mbar_arrive(tmem_empty);
@@ -848,6 +870,17 @@ __global__ void __launch_bounds__(256, 1)
     }
   }
 
+  if (HELPERS && warp < 4) {
+    __syncwarp();
+    named_bar_sync(4, 256);  // the epilogue has decided whether this CTA finalizes t_last
+    if (sh.fin_last) {
+      tc_fence_after();
+      EpiShared& sh2 = *reinterpret_cast<EpiShared*>(rm.kind + 5 * NT + 64 + 1 + 512);
+      fin_chunks(t_last, NT / 32, NT / 16, threadIdx.x, sh2, 2, nullptr, nullptr);
+      tc_fence_before();
+      named_bar_sync(5, 256);
+    }
+  }
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) stamp(5);
