@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(256, 1)
       auto seg_src = [&](int s, int cc) {
         const int cs = c_first + s;
         const int sl = (sp.ubegin(cs) >= t0) ? 0 : 1;  // tile t is cs's first tile
-        return reinterpret_cast<const float4*>(p.ws + (((size_t)cs * 2 + sl) * BM + ep_t) * NT + cc * 16);
+        return reinterpret_cast<const float4*>(p.ws) + ((((size_t)cs * 2 + sl) * (NT / 16) + cc) * 4) * BM + ep_t;
       };
       auto fetch = [&](int cc) {
         if (nseg > 1) {
@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(256, 1)
             if (s < nseg) {
               const float4* src = seg_src(s, cc);
 #pragma unroll
-              for (int q = 0; q < 4; ++q) nb[s][q] = __ldcg(src + q);
+              for (int q = 0; q < 4; ++q) nb[s][q] = __ldcg(src + q * BM);
             }
         }
         if (MODE == EPI_RESID) {
@@ -576,7 +576,7 @@ __global__ void __launch_bounds__(256, 1)
               if (s0 + s < nseg) {
                 const float4* src = seg_src(s0 + s, cc);
 #pragma unroll
-                for (int q = 0; q < 4; ++q) buf[s][q] = __ldcg(src + q);
+                for (int q = 0; q < 4; ++q) buf[s][q] = __ldcg(src + q * BM);
               }
             }
 #pragma unroll
@@ -820,22 +820,22 @@ __global__ void __launch_bounds__(256, 1)
       mbar_wait(tmem_full, tphase);
       tc_fence_after();
       if (ep_t == 0) stamp(13);
-      // Non-final stream-K segments publish their fp32 partial (layout [cta][slot][128
-      // features][NT]: a thread's 16 values of a chunk are one contiguous 64-byte run) and the
-      // last to arrive folds all partials in segment order (deterministic). One finalize call
-      // site, so the tail's code stays compact in the instruction caches.
+      // Non-final stream-K segments publish their fp32 partial (layout [cta][slot][16-column
+      // chunk][4 float4][128 features]: a warp's float4 access is 512 contiguous bytes, so
+      // publish and fold move whole lines) and the last to arrive folds all partials in
+      // segment order (deterministic). One finalize call site, so the tail's code stays
+      // compact in the instruction caches.
       bool fin = true;
       if (nseg > 1) {
         const int slot = (t == t_first) ? 0 : 1;
-        float* wsp = p.ws + (((size_t)c * 2 + slot) * BM + ep_t) * NT;
+        float4* wsp = reinterpret_cast<float4*>(p.ws) + ((size_t)c * 2 + slot) * (NT / 16) * 4 * BM + ep_t;
 #pragma unroll 1
         for (int cc = 0; cc < NT / 16; ++cc) {
           float v[16];
           tmem_ld16(tmem_base + lane_base + cc * 16, v);
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            __stcg(reinterpret_cast<float4*>(wsp + cc * 16) + q,
-                   make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+            __stcg(wsp + (cc * 4 + q) * BM, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
         }
         tc_fence_before();
         mbar_arrive(tmem_empty);
