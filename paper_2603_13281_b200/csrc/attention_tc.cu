@@ -83,6 +83,7 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
       : "memory");
 }
 
+static_assert(128 * 132 * 4 <= 2 * TcLayout::STAGE_BYTES, "O staging must fit in the K/V stages");
 static_assert(TcLayout::SMEM <= 232448 - 1024, "exceeds the per-block shared memory limit");
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
@@ -416,7 +417,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       named_bar_sync(1 + quarter, 64);
       const float l = rl[r] + rl[128 + r];
       const size_t slot = valid ? ((size_t)rr.x * num_heads + g * group + rr.y) * max_chunks + it.chunk_idx : 0;
-      float* dst = part_o + slot * 128 + half * 64;
+      // O leaves through shared memory (the K/V stages are idle once the last P.V landed):
+      // rows padded to 528 B so a quarter-warp's 16-byte stores hit distinct banks, then each
+      // warp writes one entry's 512 contiguous bytes per instruction
+      float* stg = reinterpret_cast<float*>(smem + L::STAGE0);
+      constexpr int STG_LD = 132;  // floats per staged row: 128 + 4 padding
       uint32_t o[4][16];
 #pragma unroll
       for (int q4 = 0; q4 < 4; ++q4) tmem_ld16_nowait(tmem_o + lane_base + half * 64 + q4 * 16, o[q4]);
@@ -424,15 +429,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
       for (int q4 = 0; q4 < 4; ++q4) {
         tmem_reg_fence(o[q4]);
-        if (valid) {
 #pragma unroll
-          for (int jj = 0; jj < 16; jj += 4)
-            *reinterpret_cast<float4*>(dst + q4 * 16 + jj) =
-                make_float4(__uint_as_float(o[q4][jj]), __uint_as_float(o[q4][jj + 1]),
-                            __uint_as_float(o[q4][jj + 2]), __uint_as_float(o[q4][jj + 3]));
-        }
+        for (int jj = 0; jj < 16; jj += 4)
+          *reinterpret_cast<float4*>(stg + r * STG_LD + half * 64 + q4 * 16 + jj) =
+              make_float4(__uint_as_float(o[q4][jj]), __uint_as_float(o[q4][jj + 1]),
+                          __uint_as_float(o[q4][jj + 2]), __uint_as_float(o[q4][jj + 3]));
       }
       if (valid && half == 0) part_ml[slot] = make_float2(m_run, l);
+      named_bar_sync(5, 256);
+      for (int idx = threadIdx.x - 128; idx < it.n_rows * 32; idx += 256) {
+        const int e = idx >> 5, f = idx & 31;
+        const int2 re = item_rows[it.row_off + e];
+        const size_t sl = ((size_t)re.x * num_heads + g * group + re.y) * max_chunks + it.chunk_idx;
+        const int rw = (e & 3) * 32 + (e >> 2);
+        reinterpret_cast<float4*>(part_o + sl * 128)[f] = *reinterpret_cast<const float4*>(stg + rw * STG_LD + f * 4);
+      }
       if (r == 0 && half == 0) stamp(5);
     }
   }
