@@ -41,20 +41,6 @@ struct TcLayout {
   static constexpr uint32_t TMEM_COLS = 512;               // S0 [0,128) S1 [128,256) O [256,384)
 };
 
-// 2^x on the FMA / integer pipes (FA4-style split of the exponentials between the SFU and
-// the FMA units): round-to-nearest split x = i + f with the 1.5 * 2^23 magic constant (no
-// F2I / FRND, which would go through the SFU pipe), cubic minimax for 2^f on [-1/2, 1/2]
-// (max rel. error 1.0e-4, below the bf16 rounding P gets next), exponent added as an
-// integer. Valid for -126 <= x <= 8 (x is clamped below; P <= 256 above).
-__device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -126.f);
-  const float t = x + 12582912.f;           // 1.5 * 2^23: round(x) lands in the low mantissa bits
-  const float fi = t - 12582912.f;
-  const float f = x - fi;                   // [-1/2, 1/2]
-  const float p = fmaf(f, fmaf(f, fmaf(f, 0.05500831f, 0.24220971f), 0.69328286f), 1.0f);
-  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
-}
-
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -346,7 +332,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (r == 0 && half == 0) sstamp(j, 6);
         const long long clk0 = clock64();
         uint8_t* rowp0 = smem + L::P_OFF + b * L::P_BYTES + half * (TC_ROWS * 128) + r * 128;
-        float ls0 = 0.f, ls1 = 0.f;
+        float ls[4] = {0.f, 0.f, 0.f, 0.f};  // four short row-sum chains instead of two long ones
         if (nvis > 0) {  // padding rows, rows past their position: P stays zero
           const float nm = -m_new;
 #pragma unroll
@@ -356,17 +342,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
               for (int jj = 0; jj < 16; jj += 2) {
                 const int c = q4 * 16 + jj;
-                // 3 of 4 keys on the SFU, 1 of 4 by polynomial on the FMA pipe: balances the
-                // two pipes (SFU: 8 cycles per warp op, polynomial: ~9 FMA-pipe ops)
+                // every exponential on the SFU: measured faster than moving a quarter or a
+                // half of them to an FMA-pipe polynomial (the FMA/ALU issue slots are the
+                // scarcer resource in this loop: 1430 vs 1520 / 1800 cycles per sub-chunk)
                 float p0 = ex2_approx(fmaf(__uint_as_float(v[q4][jj]), sl2, nm));
                 const float x1 = fmaf(__uint_as_float(v[q4][jj + 1]), sl2, nm);
-                float p1 = (jj & 2) ? ex2_poly(x1) : ex2_approx(x1);
+                float p1 = ex2_approx(x1);
                 if (!full) {
                   p0 = c < nvis ? p0 : 0.f;
                   p1 = c + 1 < nvis ? p1 : 0.f;
                 }
-                ls0 += p0;
-                ls1 += p1;
+                ls[(jj >> 1) & 3] += p0 + p1;
                 __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
                 pk[jj >> 1] = *reinterpret_cast<uint32_t*>(&h2);
               }
@@ -381,7 +367,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           for (int c = 0; c < 8; ++c)
             *reinterpret_cast<uint4*>(rowp0 + ((c ^ (r & 7)) << 4)) = make_uint4(0, 0, 0, 0);
         }
-        l_part = l_part * corr + (ls0 + ls1);
+        l_part = l_part * corr + ((ls[0] + ls[1]) + (ls[2] + ls[3]));
         m_run = m_new;
         if (trace != nullptr && cta_id == 0 && r == 0 && half == 0 && j < 256)
           trace[(size_t)2 * 4096 * 16 + j * 8 + 7] = (unsigned long long)(clock64() - clk0);
