@@ -187,6 +187,39 @@ def test_batched_step_equals_single_session_steps(c1_setup):
         x.close(), y.close()
 
 
+def test_wide_batched_step_equals_single_session_steps(c1_setup):
+    """24 sessions (40 rows: the 64-column GEMM tiles, the 8-warp finalization, wide attention
+    items) stepped in one batch == each session stepped alone, bitwise."""
+    E, P, M = _mods()
+    base, agents, rt = c1_setup
+    rng = np.random.default_rng(12)
+    n = 24
+    prompts = [[int(t) for t in rng.integers(1, 1024, int(rng.integers(17, 61)))] for _ in range(n)]
+    ads = [(agents[0], agents[1], None)[i % 3] for i in range(n)]
+    want_tok, want_lg = [], []
+    for ad, pr in zip(ads, prompts):
+        s = E.new_session(base, ad, 256, runtime=rt, capture_logits=True)
+        t = E.prefill(s, pr)
+        toks, lgs = [t], []
+        for _ in range(4):
+            t = E.decode_step_fused(s, t)
+            toks.append(t)
+            lgs.append(s.last_logits.tobytes())
+        want_tok.append(toks)
+        want_lg.append(lgs)
+        s.close()
+    batch = [E.new_session(base, ad, 256, runtime=rt, capture_logits=True) for ad in ads]
+    tb = [E.prefill(s, pr) for s, pr in zip(batch, prompts)]
+    assert tb == [w[0] for w in want_tok]
+    for step in range(4):
+        tb = E.decode_step_batch(batch, tb)
+        assert tb == [w[step + 1] for w in want_tok], f"step {step}"
+        for i, s in enumerate(batch):
+            assert s.last_logits.tobytes() == want_lg[i][step], f"session {i} step {step}"
+    for s in batch:
+        s.close()
+
+
 def test_shared_prefix_pages_are_zero_copy_and_bitwise(c1_setup):
     """8 adapters on one prompt: one prefill, 7 full-prefix hits; the hits reference the
     writer's pages and continue bitwise like cold sessions."""
