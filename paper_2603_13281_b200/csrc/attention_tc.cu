@@ -35,8 +35,8 @@ struct TcLayout {
   static constexpr uint32_t STAGE0 = P_OFF + 2 * P_BYTES;  // stage s: K halves, then V halves
   static constexpr uint32_t STAGE_BYTES = 4 * HALF;        // 64 KB
   static constexpr uint32_t BAR_OFF = STAGE0 + 2 * STAGE_BYTES;
-  static constexpr uint32_t RED_OFF = BAR_OFF + 128;       // float [2 halves][128]
-  // 230,528 B: within the opt-in maximum of 232,448 less the 1 KB the driver reserves
+  static constexpr uint32_t RED_OFF = BAR_OFF + 256;       // float [2 halves][128]
+  // 230,656 B: within the opt-in maximum of 232,448 less the 1 KB the driver reserves
   static constexpr size_t SMEM = RED_OFF + 256 * 4;
   static constexpr uint32_t TMEM_COLS = 512;               // S0 [0,128) S1 [128,256) O [256,384)
 };
@@ -92,7 +92,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t* v_empty = bars + 14;  // [2] V consumed by P.V
   uint64_t* s_full = bars + 5;    // [2]
   uint64_t* p_full = bars + 7;
-  uint64_t* o_done = bars + 8;
+  uint64_t* o_done = bars + 8;    // one phase per P.V (the lazy rescale waits on it)
+  uint64_t* o_final = bars + 16;  // the last P.V only: the epilogue's single-phase wait
   uint64_t* p_free = bars + 9;    // [2]: P buffer b consumed by its P.V
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
   float* red = reinterpret_cast<float*>(smem + L::RED_OFF);
@@ -124,6 +125,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     mbar_init(p_full, 256);
     mbar_init(o_done, 1);
+    mbar_init(o_final, 1);
     mbar_init(&p_free[0], 1);
     mbar_init(&p_free[1], 1);
     fence_barrier_init();
@@ -213,6 +215,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         sstamp(j, 3);
         tc_commit(o_done);
+        if (j == nsub - 1) tc_commit(o_final);
         tc_commit(&p_free[j & 1]);
         tc_commit(&v_empty[j & 1]);
       }
@@ -397,7 +400,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       // ---------------- epilogue: unnormalised partial O and (m, l) ----------------
       float* rl = red;  // free: both partners passed the last iteration's second barrier
       rl[half * 128 + r] = l_part;
-      mbar_wait(o_done, (nsub - 1) & 1);
+      // not o_done: the last softmax iteration only knows P.V(nsub - 3) finished, so o_done
+      // may still be two phases behind and a parity wait would alias an older phase
+      mbar_wait(o_final, 0);
       tc_fence_after();
       if (r == 0 && half == 0) stamp(0);
       named_bar_sync(1 + quarter, 64);

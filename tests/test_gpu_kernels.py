@@ -152,6 +152,47 @@ def test_tc_attention_chunkings_match_torch(cuda, chunk_pages):
     assert err < 3e-2, err
 
 
+@pytest.mark.parametrize("chunk_pages", [16, 64])
+def test_tc_attention_workflow_shaped_prefill_and_decode(cuda, chunk_pages):
+    """The C3 shape in miniature: many sequences on one long shared prefix (not a multiple of
+    the chunk), each with private pages; prefill-style rows (consecutive positions, causal
+    inside the last chunk, > 128 entries per chunk -> several items per chunk) and
+    decode-style rows (encoder + decoder per sequence) in one launch."""
+    import torch
+    g = torch.Generator(device="cpu").manual_seed(100 + chunk_pages)
+    H, Hkv, hd = 32, 8, 128
+    shared = 70  # 1120-token shared prefix
+    n_seq = 12
+    priv = 4
+    n_pages = shared + n_seq * priv
+    kp = torch.randn(n_pages, Hkv, 16, hd, generator=g).to(torch.bfloat16)
+    vp = torch.randn(n_pages, Hkv, 16, hd, generator=g).to(torch.bfloat16)
+    bt = np.full((n_seq, shared + priv), -1, np.int32)
+    for s_ in range(n_seq):
+        bt[s_, :shared] = np.arange(shared)
+        bt[s_, shared:] = shared + priv * s_ + np.arange(priv)
+    row_seq, row_pos = [], []
+    for s_ in range(n_seq):
+        if s_ % 3 == 0:  # prefill-style: 20 new rows after the prefix
+            for i in range(20):
+                row_seq.append(s_)
+                row_pos.append(shared * 16 + i)
+        else:  # decode-style: encoder + decoder row at one position
+            for _ in range(2):
+                row_seq.append(s_)
+                row_pos.append(shared * 16 + 5 + s_)
+    q = torch.randn(len(row_seq), H * hd, generator=g)
+    q[1::2] *= 3.0
+    q = q.to(torch.bfloat16)
+    ref = _attention_ref(q, kp, vp, bt, row_seq, row_pos, H, Hkv, hd)
+    got, _ = _run_attn(q.to(cuda), kp.to(cuda), vp.to(cuda), bt, row_seq, row_pos, H, Hkv, hd,
+                       chunk_pages=chunk_pages)
+    got = got.float().cpu()
+    assert torch.isfinite(got).all()
+    err = (got - ref).abs().max().item()
+    assert err < 3e-2, err
+
+
 def test_tc_attention_prefill_rows_causal_and_many_entries(cuda):
     """Prefill-shaped work: 48 rows of one sequence at consecutive positions (causal mask
     inside the chunk, rows sharing pages at different positions), 48 x 4 heads = 192 query
