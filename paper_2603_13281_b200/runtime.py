@@ -367,16 +367,19 @@ class AdapterSlots:
 
 # ----------------------------------------------------------------------------- runtime
 def auto_chunk_pages(max_context: int) -> int:
-    """Attention work-item length for a runtime serving contexts up to max_context: the
-    smallest of 16 / 32 / 64 / 128 pages that splits a full context into at most 16 chunks
-    (enough (chunk, KV head) items to fill the SMs, few enough that each item amortises its
-    start-up over several sub-chunks). Fixed per runtime, so a row's attention never depends
-    on which other rows share its step."""
+    """Attention work-item length (pages) for a runtime serving contexts up to max_context:
+    16 up to 2.5k tokens (the C2 decode regime), 32 up to 5k, 64 up to 17k, 128 beyond --
+    enough (chunk, KV head) items to fill the SMs at long context while each item keeps
+    enough 8-page sub-chunks to amortise its start-up, and few enough items that a wide
+    shared-prefix batch (C3: 512 query entries per KV head) is not split into many short
+    ones. Measured with tools/attn_sweep.py, tools/ablate.py and tools/c3_step_profile.py
+    (ICR_CHUNK_PAGES). Fixed per runtime, so a row's attention never depends on which other
+    rows share its step."""
     pages = -(-max_context // BLOCK_TOKENS)
-    cp = 16
-    while cp < 128 and cp * 16 < pages:
-        cp *= 2
-    return cp
+    for cp, limit in ((16, 160), (32, 320), (64, 1088)):
+        if pages <= limit:
+            return cp
+    return 128
 
 
 class Runtime:

@@ -43,13 +43,17 @@ def test_sources_target_sm100a_only():
 
 def test_auto_chunk_pages_rule():
     """Attention chunk length chosen per runtime from its context capacity (fixed per runtime:
-    batch invariance): C1/C2 contexts keep 16-page chunks, the 8k-prefix workflow (C3) gets
-    64, the 32k context (C4) 128."""
+    batch invariance): C1/C2 contexts keep 16-page chunks, 4k gets 32, the 8k-prefix workflow
+    (C3) and 16k get 64, the 32k context (C4) 128."""
     from paper_2603_13281_b200.runtime import auto_chunk_pages
     assert auto_chunk_pages(1024) == 16
     assert auto_chunk_pages(2418) == 16      # bench.py C2 capacity
-    assert auto_chunk_pages(4096) == 16
+    assert auto_chunk_pages(2560) == 16
+    assert auto_chunk_pages(2576) == 32
     assert auto_chunk_pages(4112) == 32
+    assert auto_chunk_pages(8448) == 64      # tools/c3_step_profile.py capacity
     assert auto_chunk_pages(8976) == 64      # C3 workflow capacity
+    assert auto_chunk_pages(16400) == 64     # 16k context: 17 chunks x 8 KV heads fill the SMs
+    assert auto_chunk_pages(17424) == 128
     assert auto_chunk_pages(32800) == 128
     assert auto_chunk_pages(1 << 20) == 128

@@ -64,21 +64,24 @@ def run(ctx, n_adapters, chunk_pages, iters=5, pipelined=False):
 
 
 def main():
+    from paper_2603_13281_b200.runtime import auto_chunk_pages
     ap = argparse.ArgumentParser()
-    ap.add_argument("--chunk-pages", type=int, default=16)
+    ap.add_argument("--chunk-pages", type=int, default=0,
+                    help="0: the runtime's rule for the context (runtime.auto_chunk_pages)")
     ap.add_argument("--out", default=None)
     ap.add_argument("--ctx", type=int, default=0, help="single config (profiling)")
     ap.add_argument("--adapters", type=int, default=8)
     ap.add_argument("--pipelined", action="store_true")
     args = ap.parse_args()
     if args.ctx:
-        print(json.dumps(run(args.ctx, args.adapters, args.chunk_pages, iters=1, pipelined=args.pipelined)))
+        cp = args.chunk_pages or auto_chunk_pages(args.ctx + 16)
+        print(json.dumps(run(args.ctx, args.adapters, cp, iters=1, pipelined=args.pipelined)))
         return
     peak = json.loads((Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]
     res = []
     for ctx in (1024, 2048, 4096, 8192, 16384, 32768):
         for n in (1, 2, 4, 8):
-            r = run(ctx, n, args.chunk_pages)
+            r = run(ctx, n, args.chunk_pages or auto_chunk_pages(ctx + 16))
             r["frac_of_measured_hbm"] = r["gbs"] / peak
             res.append(r)
             print(json.dumps(r), flush=True)
