@@ -91,7 +91,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t* v_full = bars + 12;   // [2] V landed
   uint64_t* v_empty = bars + 14;  // [2] V consumed by P.V
   uint64_t* s_full = bars + 5;    // [2]
-  uint64_t* p_full = bars + 7;
+  // P(j) written (+ O rescaled): one barrier per P buffer, so the MMA warp's parity wait can
+  // never alias -- softmax(j + 2) needs P.V(j), i.e. the MMA warp past its wait for P(j)
+  uint64_t* p_full_b[2] = {bars + 7, bars + 17};
   uint64_t* o_done = bars + 8;    // one phase per P.V (the lazy rescale waits on it)
   uint64_t* o_final = bars + 16;  // the last P.V only: the epilogue's single-phase wait
   uint64_t* p_free = bars + 9;    // [2]: P buffer b consumed by its P.V
@@ -123,7 +125,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_init(&v_empty[b], 1);
       mbar_init(&s_full[b], 1);
     }
-    mbar_init(p_full, 256);
+    mbar_init(p_full_b[0], 256);
+    mbar_init(p_full_b[1], 256);
     mbar_init(o_done, 1);
     mbar_init(o_final, 1);
     mbar_init(&p_free[0], 1);
@@ -200,7 +203,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     issue_s(0);
     for (int j = 0; j < nsub; ++j) {
       if (j + 1 < nsub) issue_s(j + 1);
-      mbar_wait(p_full, j & 1);  // softmax j wrote P and rescaled O
+      mbar_wait(p_full_b[j & 1], (j >> 1) & 1);  // softmax j wrote P and rescaled O
       mbar_wait(&v_full[j & 1], (j >> 1) & 1);
       tc_fence_after();
       if (elect_one()) {
@@ -393,7 +396,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         tc_fence_before();
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        mbar_arrive(p_full);
+        mbar_arrive(p_full_b[b]);
         if (r == 0 && half == 0) sstamp(j, 2);
       }
       if (r == 0 && half == 0) stamp(4);
