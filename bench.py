@@ -349,6 +349,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-attention", action="store_true", help="skip the C4 attention line")
     args = ap.parse_args()
+    bad = [k for k in ("ICR_DIAG_NO_LORA", "ICR_SKIP", "ICR_CHUNK_PAGES", "ICR_STAGES", "ICR_PREISSUE",
+                       "ICR_LIB_PATH", "ICR_ATTN_MMA") if os.environ.get(k)]
+    if bad:  # tuning / diagnostic switches would change (or skip) measured work
+        raise SystemExit(f"bench.py refuses to run with {', '.join(bad)} set")
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
