@@ -308,19 +308,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         // visible keys of this half: [kbase, kbase + nvis); max of raw scores x sl2 (> 0)
         // equals the max of the scaled scores (rounding is monotonic)
         const int nvis = valid ? max(0, min(hkeys, pos + 1 - kbase)) : 0;
-        const bool full = nvis == 64;
-        float mx = -INFINITY;
-        if (full) {
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4)
-#pragma unroll
-            for (int jj = 0; jj < 16; ++jj) mx = fmaxf(mx, __uint_as_float(v[q4][jj]));
-        } else if (nvis > 0) {
+        if (nvis > 0 && nvis < 64) {
+          // rare (the row's causal edge or a short last sub-chunk): invisible keys become
+          // -inf once, so the max and exp loops below carry no per-key predicates (the
+          // volatile asm keeps this a branch instead of 64 if-converted selects)
+          asm volatile("" ::: "memory");
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4)
 #pragma unroll
             for (int jj = 0; jj < 16; ++jj)
-              if (q4 * 16 + jj < nvis) mx = fmaxf(mx, __uint_as_float(v[q4][jj]));
+              if (q4 * 16 + jj >= nvis) v[q4][jj] = 0xff800000u;  // -inf
+        }
+        float mx = -INFINITY;
+        if (nvis > 0) {
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4)
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) mx = fmaxf(mx, __uint_as_float(v[q4][jj]));
         }
         // exchange with the partner thread (same row, other half); the second barrier lets
         // the buffer be rewritten next iteration
@@ -351,13 +355,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 // every exponential on the SFU: measured faster than moving a quarter or a
                 // half of them to an FMA-pipe polynomial (the FMA/ALU issue slots are the
                 // scarcer resource in this loop: 1430 vs 1520 / 1800 cycles per sub-chunk)
-                float p0 = ex2_approx(fmaf(__uint_as_float(v[q4][jj]), sl2, nm));
-                const float x1 = fmaf(__uint_as_float(v[q4][jj + 1]), sl2, nm);
-                float p1 = ex2_approx(x1);
-                if (!full) {
-                  p0 = c < nvis ? p0 : 0.f;
-                  p1 = c + 1 < nvis ? p1 : 0.f;
-                }
+                // masked keys hold -inf: exp2(-inf) = +0
+                const float p0 = ex2_approx(fmaf(__uint_as_float(v[q4][jj]), sl2, nm));
+                const float p1 = ex2_approx(fmaf(__uint_as_float(v[q4][jj + 1]), sl2, nm));
                 ls[(jj >> 1) & 3] += p0 + p1;
                 __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
                 pk[jj >> 1] = *reinterpret_cast<uint32_t*>(&h2);
