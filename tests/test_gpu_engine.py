@@ -220,6 +220,50 @@ def test_wide_batched_step_equals_single_session_steps(c1_setup):
         s.close()
 
 
+def test_zero_adapter_fused_collapses_to_base(c1_setup):
+    """Reference tests/test_engine.py:63-75 on the GPU: an adapter with B = 0 (AdapterSet.init)
+    decodes bitwise like the bare base model (LoRA K-chunks add exact zeros)."""
+    E, P, M = _mods()
+    base, agents, rt = c1_setup
+    zero = M.AdapterSet.init(base.config, rank=8, alpha=16.0, seed=2)
+    prompt = [int(t) for t in np.random.default_rng(13).integers(1, 1024, 30)]
+    adapted = E.new_session(base, zero, 256, runtime=rt, capture_logits=True)
+    bare = E.new_session(base, None, 256, runtime=rt, capture_logits=True)
+    ta, tb = E.prefill(adapted, prompt), E.prefill(bare, prompt)
+    assert ta == tb
+    for _ in range(6):
+        ta, tb = E.decode_step_fused(adapted, ta), E.decode_step_base(bare, tb)
+        assert ta == tb
+        assert adapted.last_logits.tobytes() == bare.last_logits.tobytes()
+    adapted.close(), bare.close()
+
+
+def test_partial_prefix_reuse_is_bitwise_and_counts_only_the_suffix(c1_setup):
+    """Reference tests/test_engine.py:125-149 on the GPU: a 40-token prompt over a pool holding
+    its first 32 tokens computes only the 8-token suffix, writes the writer's exact K/V bytes
+    and continues bitwise like a cold session."""
+    E, P, M = _mods()
+    base, agents, rt = c1_setup
+    prompt = [int(t) for t in np.random.default_rng(14).integers(1, 1024, 40)]
+    pool = P.KvCachePool(base.config, 64 << 20, "icarus")
+    writer = E.new_session(base, None, 256, runtime=rt)
+    E.prefill(writer, prompt)
+    pool.commit(None, prompt, writer.cache, next_token_fn=lambda p: E.base_next_token_at(writer, p))
+    reader = E.new_session(base, None, 256, runtime=rt, capture_logits=True)
+    tok = E.prefill(reader, prompt, pool=pool, namespace=None, reader="other")
+    assert reader.ledger.prefix_hit_tokens == 32 and reader.ledger.prefill_tokens == 8
+    assert reader.cache.fingerprint() == writer.cache.fingerprint()
+    cold = E.new_session(base, None, 256, runtime=rt, capture_logits=True)
+    tok_cold = E.prefill(cold, prompt)
+    assert tok == tok_cold
+    for _ in range(4):
+        tok, tok_cold = E.decode_step_fused(reader, tok), E.decode_step_fused(cold, tok_cold)
+        assert tok == tok_cold and reader.last_logits.tobytes() == cold.last_logits.tobytes()
+    pool.release(reader.borrowed_chain)
+    for s_ in (writer, reader, cold):
+        s_.close()
+
+
 def test_shared_prefix_pages_are_zero_copy_and_bitwise(c1_setup):
     """8 adapters on one prompt: one prefill, 7 full-prefix hits; the hits reference the
     writer's pages and continue bitwise like cold sessions."""
