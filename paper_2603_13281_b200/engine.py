@@ -58,6 +58,7 @@ class GenerationSession:
         self.capture_logits = capture_logits
         self.adapter_slot = self.runtime.slots.slot_of(adapter) if adapter is not None else -1
         self.seq = self.runtime.acquire_seq()
+        self._bt_len = -1  # pages mirrored into the block table row (-1: row not written yet)
         self.cache = KvCacheTensor(base.config, max_context, arena=self.runtime.arena)
         self.prompt: list[int] = []
         self.produced: list[int] = []
@@ -83,6 +84,17 @@ class GenerationSession:
 
     def _sync_block_table(self) -> None:
         self.runtime.set_pages(self.seq, self.cache.pages)
+        self._bt_len = len(self.cache.pages)
+
+    def _sync_appended_pages(self) -> None:
+        """Decode steps only ever append pages: mirror just the new tail (a full rewrite of the
+        row per session per step was most of the step's host-side Python time)."""
+        n = len(self.cache.pages)
+        if self._bt_len < 0 or n < self._bt_len:
+            self._sync_block_table()
+        elif n > self._bt_len:
+            self.runtime.block_table[self.seq, self._bt_len:n] = self.cache.pages[self._bt_len:n]
+            self._bt_len = n
 
 
 def new_session(base: BaseWeights, adapter: Optional[AdapterSet] = None, max_context: int = 512,
@@ -207,7 +219,7 @@ def _prepare_write(session: GenerationSession, pos: int) -> None:
     page = session.cache.pages[pos // BLOCK_TOKENS]
     if session.runtime.arena.refcount(page) != 1:
         raise ContractViolationError(f"position {pos} would be written into shared page {page}")
-    session._sync_block_table()
+    session._sync_appended_pages()
 
 
 def decode_step_batch(sessions: Sequence[GenerationSession], tokens: Sequence[int]) -> list[int]:

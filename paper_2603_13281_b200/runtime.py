@@ -475,11 +475,12 @@ class Runtime:
         """One fused forward over token rows (see include/icarus_b200.h icr_batch).
         Returns (tokens for emitting rows, logits tensor or None)."""
         torch = _torch()
-        arrs = [np.ascontiguousarray(a, dtype=np.int32) for a in (tokens, kind, seq, pos, adapter, emit)]
-        n = arrs[0].shape[0]
-        n_seqs = int(max(arrs[2].max(), 0)) + 1
-        b = _lib.BatchC(n, *[_lib.i32_ptr(a) for a in arrs], _lib.i32_ptr(self.block_table), n_seqs)
-        n_emit = int(arrs[5].sum())
+        rows = np.array((tokens, kind, seq, pos, adapter, emit), dtype=np.int32)  # one [6, n] block
+        n = rows.shape[1]
+        n_seqs = int(max(rows[2].max(), 0)) + 1
+        base, stride = _lib.addr(rows), rows.strides[0]
+        b = _lib.BatchC(n, *[base + i * stride for i in range(6)], _lib.addr(self.block_table), n_seqs)
+        n_emit = int(rows[5].sum())
         out = np.zeros(max(n_emit, 1), dtype=np.int32)
         lg = None
         if logits and n_emit:
@@ -498,7 +499,7 @@ class Runtime:
         n = arrs[0].shape[0]
         n_seqs = int(max(arrs[2].max(), 0)) + 1
         fb = np.ascontiguousarray(feedback, dtype=np.int32)
-        b = _lib.BatchC(n, *[_lib.i32_ptr(a) for a in arrs], _lib.i32_ptr(self.block_table), n_seqs)
+        b = _lib.BatchC(n, *[_lib.addr(a) for a in arrs], _lib.addr(self.block_table), n_seqs)
         ms = np.zeros(steps, dtype=np.float32)
         last = np.zeros(max(int(arrs[5].sum()), 1), dtype=np.int32)
         _lib.check(self._lib.icr_decode_loop(self._handle, C.byref(b), _lib.i32_ptr(fb), steps,
