@@ -75,7 +75,7 @@ def load():
         "icr_model_create": [C.POINTER(ModelConfigC), C.POINTER(LayerWeightsC), p, p, f,
                              C.POINTER(p)],
         "icr_model_destroy": [p],
-        "icr_forward": [p, C.POINTER(BatchC), C.POINTER(C.c_int32), p, p],
+        "icr_forward": [p, C.POINTER(BatchC), p, p, p],
         "icr_decode_loop": [p, C.POINTER(BatchC), C.POINTER(C.c_int32), i,
                             C.POINTER(C.c_int32), C.POINTER(C.c_float), p],
         "icr_model_stats": [p, C.POINTER(C.c_int64)],

@@ -485,7 +485,7 @@ class Runtime:
         lg = None
         if logits and n_emit:
             lg = torch.empty(n_emit, self.dw.vocab_pad, dtype=torch.float32, device=self.device)
-        _lib.check(self._lib.icr_forward(self._handle, C.byref(b), _lib.i32_ptr(out),
+        _lib.check(self._lib.icr_forward(self._handle, C.byref(b), _lib.addr(out),
                                          lg.data_ptr() if lg is not None else None,
                                          _lib.stream_handle()))
         if lg is not None:
