@@ -170,25 +170,112 @@ def prefill(session: GenerationSession, prompt, pool=None, namespace: Optional[s
         led.param_matrix_reads += _reads_per_step(session)
         session.last_logits = last_lg
     else:
-        stored = chain[-1].next_token if chain else None
-        if stored is not None:
-            token = int(stored)
-            session.last_logits = None
-        else:
-            # Older blocks lack the chunk-end prediction: replay the last position through a
-            # read-only (decoder-kind, no adapter) row -- it cannot write KV (engine.py:140-148).
-            session._sync_block_table()
-            out, lg = rt.forward(tokens=[toks[-1]], kind=[1], seq=[session.seq], pos=[n - 1],
-                                 adapter=[-1], emit=[1], logits=session.capture_logits)
-            token = int(out[0])
-            session.base_next[n - 1] = token
-            session.last_logits = _logits_np(lg, 0)
-            led.prefill_tokens += 1
-            led.param_matrix_reads += 5 * cfg.num_layers + 1
+        token = _full_hit_token(session, toks, chain)
     session.prompt = toks
     session.produced = [token]
     session._prefilled = True
     return token
+
+
+def _full_hit_token(session: GenerationSession, toks: list, chain: list) -> int:
+    """The whole prompt was pooled: emit the stored chunk-end prediction, or replay the last
+    position through a read-only (decoder-kind, no adapter) row -- it cannot write KV
+    (src/engine.py:135-148)."""
+    stored = chain[-1].next_token if chain else None
+    if stored is not None:
+        session.last_logits = None
+        return int(stored)
+    n = len(toks)
+    session._sync_block_table()
+    out, lg = session.runtime.forward(tokens=[toks[-1]], kind=[1], seq=[session.seq], pos=[n - 1],
+                                      adapter=[-1], emit=[1], logits=session.capture_logits)
+    token = int(out[0])
+    session.base_next[n - 1] = token
+    session.last_logits = _logits_np(lg, 0)
+    session.ledger.prefill_tokens += 1
+    session.ledger.param_matrix_reads += 5 * session.config.num_layers + 1
+    return token
+
+
+def prefill_batch(sessions: Sequence[GenerationSession], prompts, pool=None,
+                  namespace: Optional[str] = None, readers: Optional[Sequence] = None) -> list[int]:
+    """`prefill` for many sessions at once: each session's pool lookup, then the uncached
+    suffixes of all of them as encoder rows of shared forwards (max_rows rows each), so a
+    batch of new turns streams the base weights once per forward instead of once per session.
+    Per session the tokens, KV bytes, ledger and stored chunk-end predictions equal those of
+    `prefill` (a row's result does not depend on the rows it shares a forward with)."""
+    if len(prompts) != len(sessions):
+        raise ValueError("one prompt per session")
+    if not sessions:
+        return []
+    rt = sessions[0].runtime
+    if any(s.runtime is not rt for s in sessions):
+        raise ConfigError("sessions in one batch must share a runtime")
+    if len({s.seq for s in sessions}) != len(sessions):
+        raise StateError("a session appears twice in one batch")
+    readers = list(readers) if readers is not None else [None] * len(sessions)
+    firsts: list = [None] * len(sessions)
+    rows = []  # (session index, token, position, emit)
+    for i, (session, prompt) in enumerate(zip(sessions, prompts)):
+        toks = _check_tokens(session, prompt)
+        if session._prefilled:
+            raise StateError("session already prefilled")
+        if not toks:
+            raise ValueError("prompt must contain at least one token")
+        if len(toks) > session.max_context:
+            raise CapacityError(f"prompt length {len(toks)} exceeds max context {session.max_context}")
+        matched, chain = 0, []
+        if pool is not None:
+            matched, chain = pool.lookup(namespace, toks, reader=readers[i])
+            if chain:
+                if any(b.arena is not rt.arena for b in chain):
+                    pool.release(chain)
+                    raise ContractViolationError("pooled blocks live in another page arena")
+                session.cache.attach_shared([b.page for b in chain])
+                session.borrowed_chain = chain
+            session.ledger.prefix_hit_tokens += matched
+        n = len(toks)
+        session.prompt = toks
+        if matched == n:  # the whole prompt was pooled
+            firsts[i] = _full_hit_token(session, toks, chain)
+            continue
+        session.cache.ensure_pages(n - 1)
+        session._sync_block_table()
+        for pos in range(matched, n):
+            rows.append((i, toks[pos], pos, pos % BLOCK_TOKENS == BLOCK_TOKENS - 1 or pos == n - 1))
+        session.ledger.prefill_tokens += n - matched
+        session.ledger.kv_bytes_written += (n - matched) * session.config.kv_bytes_per_token
+        session.ledger.param_matrix_reads += _reads_per_step(session)
+    step = rt.max_rows
+    last_row = {}
+    for k, r in enumerate(rows):
+        last_row[r[0]] = k
+    for c0 in range(0, len(rows), step):
+        chunk = rows[c0:c0 + step]
+        want = [sessions[r[0]].capture_logits and last_row[r[0]] == c0 + j for j, r in enumerate(chunk)]
+        out, lg = rt.forward(tokens=[r[1] for r in chunk], kind=[0] * len(chunk),
+                             seq=[sessions[r[0]].seq for r in chunk], pos=[r[2] for r in chunk],
+                             adapter=[-1] * len(chunk), emit=[int(r[3]) for r in chunk], logits=any(want))
+        e = 0
+        for j, r in enumerate(chunk):
+            if not r[3]:
+                continue
+            session = sessions[r[0]]
+            session.base_next[r[2]] = int(out[e])
+            if last_row[r[0]] == c0 + j:
+                firsts[r[0]] = int(out[e])
+                session.last_logits = _logits_np(lg, e) if want[j] else None
+            e += 1
+        counts = {}
+        for r in chunk:
+            counts[r[0]] = counts.get(r[0], 0) + 1
+        for i, c in counts.items():
+            sessions[i].cache.advance(c)
+    for i, session in enumerate(sessions):
+        if not session._prefilled:
+            session.produced = [firsts[i]]
+            session._prefilled = True
+    return firsts
 
 
 def _pre_step(session: GenerationSession, token: int) -> int:

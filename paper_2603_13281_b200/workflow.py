@@ -150,15 +150,22 @@ def serve(base, adapters: Sequence, pool, prefix: Sequence[int], reqs: Sequence[
     next_turn = {r.rid: 0 for r in reqs}
     t0 = time.perf_counter()
 
-    def start_turn(req: Request) -> _Live:
-        j = next_turn[req.rid]
-        turn = req.turns[j]
-        ctx = contexts[req.rid] + list(turn.new_tokens)
-        s = E.new_session(base, adapters[turn.agent], max_context, runtime=runtime)
-        first = E.prefill(s, ctx, pool=pool, namespace=None, reader=f"agent{turn.agent}")
-        rep.prefill_tokens += s.ledger.prefill_tokens
-        rep.prefix_hit_tokens += s.ledger.prefix_hit_tokens
-        return _Live(req, j, ctx, s, [first])
+    def start_turns(reqs_: list) -> list:
+        """Open the next turn of each request and prefill all of them together
+        (engine.prefill_batch: the base weights stream once per shared forward)."""
+        ss, ctxs, readers = [], [], []
+        for req in reqs_:
+            turn = req.turns[next_turn[req.rid]]
+            ctxs.append(contexts[req.rid] + list(turn.new_tokens))
+            ss.append(E.new_session(base, adapters[turn.agent], max_context, runtime=runtime))
+            readers.append(f"agent{turn.agent}")
+        firsts = E.prefill_batch(ss, ctxs, pool=pool, namespace=None, readers=readers)
+        out = []
+        for req, s, ctx, first in zip(reqs_, ss, ctxs, firsts):
+            rep.prefill_tokens += s.ledger.prefill_tokens
+            rep.prefix_hit_tokens += s.ledger.prefix_hit_tokens
+            out.append(_Live(req, next_turn[req.rid], ctx, s, [first]))
+        return out
 
     def finish_turn(lv: _Live) -> None:
         s, turn = lv.session, lv.req.turns[lv.turn]
@@ -180,8 +187,11 @@ def serve(base, adapters: Sequence, pool, prefix: Sequence[int], reqs: Sequence[
             pending.append(lv.req)
 
     while live or pending:
-        while pending and len(live) < cfg.max_batch:
-            live.append(start_turn(pending.pop(0)))
+        starting = []
+        while pending and len(live) + len(starting) < cfg.max_batch:
+            starting.append(pending.pop(0))
+        if starting:
+            live.extend(start_turns(starting))
         rep.max_live = max(rep.max_live, len(live))
         # a turn whose output is a single token is complete after prefill
         done = [lv for lv in live if len(lv.out) >= lv.req.turns[lv.turn].output_len]

@@ -264,6 +264,42 @@ def test_partial_prefix_reuse_is_bitwise_and_counts_only_the_suffix(c1_setup):
         s_.close()
 
 
+def test_prefill_batch_equals_single_prefills(c1_setup):
+    """engine.prefill_batch: many sessions' uncached suffixes in shared forwards (split at
+    max_rows across sessions) give the tokens, KV bytes, chunk-end predictions and ledgers of
+    one `prefill` per session -- including a partial pool hit and a full hit."""
+    E, P, M = _mods()
+    base, agents, rt = c1_setup
+    rng = np.random.default_rng(15)
+    shared = [int(t) for t in rng.integers(1, 1024, 48)]
+    prompts = [shared + [int(t) for t in rng.integers(1, 1024, int(k))] for k in (5, 40, 0, 120, 77, 200)]
+    ads = [agents[0], None, agents[1], agents[0], agents[1], None]
+
+    def run(batched):
+        pool = P.KvCachePool(base.config, 64 << 20, "icarus")
+        w = E.new_session(base, None, 512, runtime=rt)
+        E.prefill(w, shared)
+        pool.commit(None, shared, w.cache, next_token_fn=lambda p: E.base_next_token_at(w, p))
+        ss = [E.new_session(base, ad, 512, runtime=rt, capture_logits=True) for ad in ads]
+        if batched:
+            toks = E.prefill_batch(ss, prompts, pool=pool, readers=["r"] * len(ss))
+        else:
+            toks = [E.prefill(s_, pr, pool=pool, reader="r") for s_, pr in zip(ss, prompts)]
+        res = (toks, [s_.cache.fingerprint() for s_ in ss], [dict(s_.base_next) for s_ in ss],
+               [(s_.ledger.prefill_tokens, s_.ledger.prefix_hit_tokens, s_.ledger.param_matrix_reads)
+                for s_ in ss],
+               [None if s_.last_logits is None else s_.last_logits.tobytes() for s_ in ss])
+        nxt = E.decode_step_batch(ss, toks)
+        for s_ in ss:
+            if s_.borrowed_chain:
+                pool.release(s_.borrowed_chain)
+            s_.close()
+        w.close()
+        return res, nxt
+
+    assert run(True) == run(False)
+
+
 def test_shared_prefix_pages_are_zero_copy_and_bitwise(c1_setup):
     """8 adapters on one prompt: one prefill, 7 full-prefix hits; the hits reference the
     writer's pages and continue bitwise like cold sessions."""
