@@ -197,25 +197,13 @@ def _full_hit_token(session: GenerationSession, toks: list, chain: list) -> int:
     return token
 
 
-def prefill_batch(sessions: Sequence[GenerationSession], prompts, pool=None,
-                  namespace: Optional[str] = None, readers: Optional[Sequence] = None) -> list[int]:
-    """`prefill` for many sessions at once: each session's pool lookup, then the uncached
-    suffixes of all of them as encoder rows of shared forwards (max_rows rows each), so a
-    batch of new turns streams the base weights once per forward instead of once per session.
-    Per session the tokens, KV bytes, ledger and stored chunk-end predictions equal those of
-    `prefill` (a row's result does not depend on the rows it shares a forward with)."""
-    if len(prompts) != len(sessions):
-        raise ValueError("one prompt per session")
-    if not sessions:
-        return []
-    rt = sessions[0].runtime
-    if any(s.runtime is not rt for s in sessions):
-        raise ConfigError("sessions in one batch must share a runtime")
-    if len({s.seq for s in sessions}) != len(sessions):
-        raise StateError("a session appears twice in one batch")
+def _prefill_setup(sessions, prompts, pool, namespace, readers, rt):
+    """prefill_batch's per-session part: checks, pool lookup + page attach, page mapping and
+    ledger; returns the suffix rows (session index, token, position, emit) and the first
+    tokens of fully pooled prompts."""
     readers = list(readers) if readers is not None else [None] * len(sessions)
     firsts: list = [None] * len(sessions)
-    rows = []  # (session index, token, position, emit)
+    rows = []
     for i, (session, prompt) in enumerate(zip(sessions, prompts)):
         toks = _check_tokens(session, prompt)
         if session._prefilled:
@@ -241,40 +229,66 @@ def prefill_batch(sessions: Sequence[GenerationSession], prompts, pool=None,
             continue
         session.cache.ensure_pages(n - 1)
         session._sync_block_table()
-        for pos in range(matched, n):
-            rows.append((i, toks[pos], pos, pos % BLOCK_TOKENS == BLOCK_TOKENS - 1 or pos == n - 1))
+        for p in range(matched, n):
+            rows.append((i, toks[p], p, p % BLOCK_TOKENS == BLOCK_TOKENS - 1 or p == n - 1))
         session.ledger.prefill_tokens += n - matched
         session.ledger.kv_bytes_written += (n - matched) * session.config.kv_bytes_per_token
         session.ledger.param_matrix_reads += _reads_per_step(session)
-    step = rt.max_rows
-    last_row = {}
-    for k, r in enumerate(rows):
-        last_row[r[0]] = k
-    for c0 in range(0, len(rows), step):
-        chunk = rows[c0:c0 + step]
-        want = [sessions[r[0]].capture_logits and last_row[r[0]] == c0 + j for j, r in enumerate(chunk)]
-        out, lg = rt.forward(tokens=[r[1] for r in chunk], kind=[0] * len(chunk),
-                             seq=[sessions[r[0]].seq for r in chunk], pos=[r[2] for r in chunk],
-                             adapter=[-1] * len(chunk), emit=[int(r[3]) for r in chunk], logits=any(want))
-        e = 0
-        for j, r in enumerate(chunk):
-            if not r[3]:
-                continue
-            session = sessions[r[0]]
-            session.base_next[r[2]] = int(out[e])
-            if last_row[r[0]] == c0 + j:
-                firsts[r[0]] = int(out[e])
-                session.last_logits = _logits_np(lg, e) if want[j] else None
-            e += 1
-        counts = {}
-        for r in chunk:
-            counts[r[0]] = counts.get(r[0], 0) + 1
-        for i, c in counts.items():
-            sessions[i].cache.advance(c)
+    return rows, firsts
+
+
+def _collect_prefill_outputs(sessions, chunk, r0, last_row, want, out, lg, e, firsts):
+    """Record one forward's results for its prefill rows (emitted outputs start at out[e])."""
+    counts = {}
+    for j, r in enumerate(chunk):
+        counts[r[0]] = counts.get(r[0], 0) + 1
+        if not r[3]:
+            continue
+        session = sessions[r[0]]
+        session.base_next[r[2]] = int(out[e])
+        if last_row[r[0]] == r0 + j:
+            firsts[r[0]] = int(out[e])
+            session.last_logits = _logits_np(lg, e) if want[j] else None
+        e += 1
+    for i, c in counts.items():
+        sessions[i].cache.advance(c)
+
+
+def _finish_prefill(sessions, firsts):
     for i, session in enumerate(sessions):
         if not session._prefilled:
             session.produced = [firsts[i]]
             session._prefilled = True
+
+
+def prefill_batch(sessions: Sequence[GenerationSession], prompts, pool=None,
+                  namespace: Optional[str] = None, readers: Optional[Sequence] = None) -> list[int]:
+    """`prefill` for many sessions at once: each session's pool lookup, then the uncached
+    suffixes of all of them as encoder rows of shared forwards (max_rows rows each), so a
+    batch of new turns streams the base weights once per forward instead of once per session.
+    Per session the tokens, KV bytes, ledger and stored chunk-end predictions equal those of
+    `prefill` (a row's result does not depend on the rows it shares a forward with)."""
+    if len(prompts) != len(sessions):
+        raise ValueError("one prompt per session")
+    if not sessions:
+        return []
+    rt = sessions[0].runtime
+    if any(s.runtime is not rt for s in sessions):
+        raise ConfigError("sessions in one batch must share a runtime")
+    if len({s.seq for s in sessions}) != len(sessions):
+        raise StateError("a session appears twice in one batch")
+    rows, firsts = _prefill_setup(sessions, prompts, pool, namespace, readers, rt)
+    last_row = {}
+    for k, r in enumerate(rows):
+        last_row[r[0]] = k
+    for c0 in range(0, len(rows), rt.max_rows):
+        chunk = rows[c0:c0 + rt.max_rows]
+        want = [sessions[r[0]].capture_logits and last_row[r[0]] == c0 + j for j, r in enumerate(chunk)]
+        out, lg = rt.forward(tokens=[r[1] for r in chunk], kind=[0] * len(chunk),
+                             seq=[sessions[r[0]].seq for r in chunk], pos=[r[2] for r in chunk],
+                             adapter=[-1] * len(chunk), emit=[int(r[3]) for r in chunk], logits=any(want))
+        _collect_prefill_outputs(sessions, chunk, c0, last_row, want, out, lg, 0, firsts)
+    _finish_prefill(sessions, firsts)
     return firsts
 
 
@@ -344,6 +358,79 @@ def decode_step_batch(sessions: Sequence[GenerationSession], tokens: Sequence[in
         _account_step(s, p, passes=1, reads=_reads_per_step(s))
         nxt.append(int(out[dec]))
     return nxt
+
+
+def step_batch(sessions: Sequence[GenerationSession], tokens: Sequence[int],
+               new_sessions: Sequence[GenerationSession] = (), prompts=(), pool=None,
+               namespace: Optional[str] = None, readers: Optional[Sequence] = None):
+    """One decode step for `sessions` fused with the prefill of `new_sessions` (continuous
+    batching with piggybacked prefill): the decode rows and the first prefill suffix rows
+    share one forward (further prefill rows follow in max_rows forwards). Returns (next token
+    per decoding session, first token per new session); each equals what decode_step_batch
+    and prefill_batch return separately, bitwise."""
+    if len(sessions) != len(tokens) or len(new_sessions) != len(prompts):
+        raise ValueError("one token per session and one prompt per new session")
+    everyone = list(sessions) + list(new_sessions)
+    if not everyone:
+        return [], []
+    if not new_sessions:
+        return decode_step_batch(sessions, tokens), []
+    if not sessions:
+        return [], prefill_batch(new_sessions, prompts, pool=pool, namespace=namespace, readers=readers)
+    rt = everyone[0].runtime
+    if any(s.runtime is not rt for s in everyone):
+        raise ConfigError("sessions in one batch must share a runtime")
+    if len({s.seq for s in everyone}) != len(everyone):
+        raise StateError("a session appears twice in one batch")
+    # decode rows (as decode_step_batch)
+    tok, kind, seq, pos, ad, emit = [], [], [], [], [], []
+    plan = []
+    for s, t in zip(sessions, tokens):
+        p = _pre_step(s, int(t))
+        _prepare_write(s, p)
+        enc = len(tok)
+        tok.append(int(t)); kind.append(0); seq.append(s.seq); pos.append(p); ad.append(-1); emit.append(1)
+        dec = enc
+        if s.adapter is not None:
+            dec = len(tok)
+            tok.append(int(t)); kind.append(1); seq.append(s.seq); pos.append(p)
+            ad.append(s.adapter_slot); emit.append(1)
+        plan.append((s, p, enc, dec))
+    n_dec = len(tok)
+    if n_dec > rt.max_rows:
+        raise CapacityError(f"{n_dec} decode rows exceed max_rows {rt.max_rows}")
+    # prefill rows (as prefill_batch)
+    rows, firsts = _prefill_setup(new_sessions, prompts, pool, namespace, readers, rt)
+    last_row = {}
+    for k, r in enumerate(rows):
+        last_row[r[0]] = k
+    first_take = rt.max_rows - n_dec
+    spans = [(0, min(first_take, len(rows)))]
+    spans += [(c0, min(c0 + rt.max_rows, len(rows))) for c0 in range(first_take, len(rows), rt.max_rows)]
+    nxt = []
+    for ci, (r0, r1) in enumerate(spans):
+        chunk = rows[r0:r1]
+        want = [new_sessions[r[0]].capture_logits and last_row[r[0]] == r0 + j for j, r in enumerate(chunk)]
+        head = (tok, kind, seq, pos, ad, emit) if ci == 0 else ([], [], [], [], [], [])
+        if not chunk and ci > 0:
+            continue
+        out, lg = rt.forward(tokens=head[0] + [r[1] for r in chunk], kind=head[1] + [0] * len(chunk),
+                             seq=head[2] + [new_sessions[r[0]].seq for r in chunk],
+                             pos=head[3] + [r[2] for r in chunk], adapter=head[4] + [-1] * len(chunk),
+                             emit=head[5] + [int(r[3]) for r in chunk],
+                             logits=any(want) or (ci == 0 and any(s.capture_logits for s in sessions)))
+        e = 0
+        if ci == 0:
+            for s, p, enc, dec in plan:
+                s.cache.advance(1)
+                s.base_next[p] = int(out[enc])
+                s.last_logits = _logits_np(lg, dec) if s.capture_logits else None
+                _account_step(s, p, passes=1, reads=_reads_per_step(s))
+                nxt.append(int(out[dec]))
+            e = n_dec  # every decode row emits
+        _collect_prefill_outputs(new_sessions, chunk, r0, last_row, want, out, lg, e, firsts)
+    _finish_prefill(new_sessions, firsts)
+    return nxt, firsts
 
 
 def decode_step_fused(session: GenerationSession, token: int) -> int:

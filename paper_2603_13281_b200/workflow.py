@@ -9,9 +9,10 @@ output lengths drawn uniformly from one `SeedSequence([seed, 0])` stream), cross
 reuse through the pool between turns (src/simulate.py:306-335: lookup, decode, commit with the
 base chunk-end token, release), `RunReport`-style counters and nearest-rank P95
 (src/simulate.py:226-231) -- and replaces simulated time with real continuous batching: every
-live turn of every request advances in ONE `decode_step_batch` per step (encoder + decoder row
-per session, each session its own adapter, KV shared through the pool), new turns join as
-soon as their context is ready, finished turns commit their blocks and release their pins.
+live turn of every request advances in ONE fused forward per step (encoder + decoder row per
+session, each session its own adapter, KV shared through the pool); new turns join as soon as
+their context is ready, their prefill riding in the same forward (`engine.step_batch`);
+finished turns commit their blocks and release their pins.
 
 C3 extension (SURVEY.md §8 "C3"): all requests share one `prefix_len`-token prefix that is
 prefilled once by the base model and committed before serving, so every first turn is a
@@ -150,21 +151,14 @@ def serve(base, adapters: Sequence, pool, prefix: Sequence[int], reqs: Sequence[
     next_turn = {r.rid: 0 for r in reqs}
     t0 = time.perf_counter()
 
-    def start_turns(reqs_: list) -> list:
-        """Open the next turn of each request and prefill all of them together
-        (engine.prefill_batch: the base weights stream once per shared forward)."""
-        ss, ctxs, readers = [], [], []
+    def open_turns(reqs_: list) -> list:
+        """Open the next turn of each request (sessions not yet prefilled)."""
+        out = []
         for req in reqs_:
             turn = req.turns[next_turn[req.rid]]
-            ctxs.append(contexts[req.rid] + list(turn.new_tokens))
-            ss.append(E.new_session(base, adapters[turn.agent], max_context, runtime=runtime))
-            readers.append(f"agent{turn.agent}")
-        firsts = E.prefill_batch(ss, ctxs, pool=pool, namespace=None, readers=readers)
-        out = []
-        for req, s, ctx, first in zip(reqs_, ss, ctxs, firsts):
-            rep.prefill_tokens += s.ledger.prefill_tokens
-            rep.prefix_hit_tokens += s.ledger.prefix_hit_tokens
-            out.append(_Live(req, next_turn[req.rid], ctx, s, [first]))
+            ctx = contexts[req.rid] + list(turn.new_tokens)
+            s = E.new_session(base, adapters[turn.agent], max_context, runtime=runtime)
+            out.append(_Live(req, next_turn[req.rid], ctx, s, []))
         return out
 
     def finish_turn(lv: _Live) -> None:
@@ -190,20 +184,30 @@ def serve(base, adapters: Sequence, pool, prefix: Sequence[int], reqs: Sequence[
         starting = []
         while pending and len(live) + len(starting) < cfg.max_batch:
             starting.append(pending.pop(0))
-        if starting:
-            live.extend(start_turns(starting))
-        rep.max_live = max(rep.max_live, len(live))
+        new = open_turns(starting)
         # a turn whose output is a single token is complete after prefill
         done = [lv for lv in live if len(lv.out) >= lv.req.turns[lv.turn].output_len]
         active = [lv for lv in live if len(lv.out) < lv.req.turns[lv.turn].output_len]
-        if active:
-            nxt = E.decode_step_batch([lv.session for lv in active], [lv.out[-1] for lv in active])
-            rep.decode_steps += 1
-            rep.decoder_tokens += len(active)
+        if active or new:
+            # one decode step of the running turns, the new turns' prefill riding in the same
+            # forward (engine.step_batch): the base weights stream once for both
+            nxt, firsts = E.step_batch([lv.session for lv in active], [lv.out[-1] for lv in active],
+                                       [lv.session for lv in new], [lv.context for lv in new],
+                                       pool=pool, namespace=None,
+                                       readers=[f"agent{lv.req.turns[lv.turn].agent}" for lv in new])
+            if active:
+                rep.decode_steps += 1
+                rep.decoder_tokens += len(active)
             for lv, t in zip(active, nxt):
                 lv.out.append(t)
                 if len(lv.out) >= lv.req.turns[lv.turn].output_len:
                     done.append(lv)
+            for lv, first in zip(new, firsts):
+                lv.out.append(first)
+                rep.prefill_tokens += lv.session.ledger.prefill_tokens
+                rep.prefix_hit_tokens += lv.session.ledger.prefix_hit_tokens
+                live.append(lv)
+        rep.max_live = max(rep.max_live, len(live))
         for lv in done:
             live.remove(lv)
             finish_turn(lv)

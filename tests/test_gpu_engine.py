@@ -300,6 +300,45 @@ def test_prefill_batch_equals_single_prefills(c1_setup):
     assert run(True) == run(False)
 
 
+def test_step_batch_fuses_decode_and_prefill_bitwise(c1_setup):
+    """engine.step_batch: a decode step of running sessions and the prefill of new ones in
+    shared forwards == decode_step_batch then prefill_batch, bitwise (tokens, logits, KV)."""
+    E, P, M = _mods()
+    base, agents, rt = c1_setup
+    rng = np.random.default_rng(16)
+    shared = [int(t) for t in rng.integers(1, 1024, 32)]
+    old_prompts = [[int(t) for t in rng.integers(1, 1024, int(k))] for k in (20, 37, 50, 9)]
+    new_prompts = [shared + [int(t) for t in rng.integers(1, 1024, int(k))] for k in (70, 3, 150)]
+    old_ads = [agents[0], agents[1], None, agents[1]]
+    new_ads = [agents[1], None, agents[0]]
+
+    def run(fused):
+        pool = P.KvCachePool(base.config, 64 << 20, "icarus")
+        w = E.new_session(base, None, 512, runtime=rt)
+        E.prefill(w, shared)
+        pool.commit(None, shared, w.cache, next_token_fn=lambda p: E.base_next_token_at(w, p))
+        old = [E.new_session(base, ad, 512, runtime=rt, capture_logits=True) for ad in old_ads]
+        toks = E.prefill_batch(old, old_prompts)
+        new = [E.new_session(base, ad, 512, runtime=rt, capture_logits=True) for ad in new_ads]
+        if fused:
+            nxt, firsts = E.step_batch(old, toks, new, new_prompts, pool=pool, readers=["r"] * 3)
+        else:
+            nxt = E.decode_step_batch(old, toks)
+            firsts = E.prefill_batch(new, new_prompts, pool=pool, readers=["r"] * 3)
+        res = (nxt, firsts, [s_.cache.fingerprint() for s_ in old + new],
+               [None if s_.last_logits is None else s_.last_logits.tobytes() for s_ in old + new],
+               [dict(s_.base_next) for s_ in new])
+        nxt2 = E.decode_step_batch(old + new, nxt + firsts)
+        for s_ in old + new:
+            if s_.borrowed_chain:
+                pool.release(s_.borrowed_chain)
+            s_.close()
+        w.close()
+        return res, nxt2
+
+    assert run(True) == run(False)
+
+
 def test_shared_prefix_pages_are_zero_copy_and_bitwise(c1_setup):
     """8 adapters on one prompt: one prefill, 7 full-prefix hits; the hits reference the
     writer's pages and continue bitwise like cold sessions."""
