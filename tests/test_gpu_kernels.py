@@ -193,6 +193,43 @@ def test_tc_attention_workflow_shaped_prefill_and_decode(cuda, chunk_pages):
     assert err < 3e-2, err
 
 
+def test_tc_attention_long_context_c4_shape(cuda):
+    """C4 in miniature-free form: 16k shared context + a private page per sequence, 8
+    sequences x (encoder, decoder) rows, 128-page chunks -> items of 16 pipelined sub-chunks
+    (the regime where the epilogue once read O before the last P.V MMAs had finished). fp32
+    torch reference on the device over the same bf16 K/V."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(21)
+    H, Hkv, hd = 32, 8, 128
+    shared, n_seq = 1024, 8
+    n_pages = shared + n_seq
+    kp = torch.randn(n_pages, Hkv, 16, hd, device="cuda", generator=g).to(torch.bfloat16)
+    vp = torch.randn(n_pages, Hkv, 16, hd, device="cuda", generator=g).to(torch.bfloat16)
+    bt = np.full((n_seq, shared + 1), -1, np.int32)
+    for s_ in range(n_seq):
+        bt[s_, :shared] = np.arange(shared)
+        bt[s_, shared] = shared + s_
+    row_seq = [s_ for s_ in range(n_seq) for _ in range(2)]
+    row_pos = [shared * 16 + 3 + s_ for s_ in range(n_seq) for _ in range(2)]
+    q = torch.randn(len(row_seq), H * hd, device="cuda", generator=g)
+    q[1::2] *= 2.0
+    q = q.to(torch.bfloat16)
+    got, _ = _run_attn(q, kp, vp, bt, row_seq, row_pos, H, Hkv, hd, chunk_pages=128)
+    # reference: [Hkv, T, hd] K/V of the shared prefix, plus each sequence's private page
+    Kp = kp[:shared].float().permute(1, 0, 2, 3).reshape(Hkv, shared * 16, hd)
+    Vp = vp[:shared].float().permute(1, 0, 2, 3).reshape(Hkv, shared * 16, hd)
+    ref = torch.empty(len(row_seq), H * hd, device="cuda")
+    for r, (s_, p_) in enumerate(zip(row_seq, row_pos)):
+        tail = p_ - shared * 16 + 1
+        K = torch.cat([Kp, kp[shared + s_].float()[:, :tail]], dim=1)
+        V = torch.cat([Vp, vp[shared + s_].float()[:, :tail]], dim=1)
+        qh = q[r].float().view(Hkv, H // Hkv, hd)
+        w = torch.softmax(torch.einsum("gjd,gtd->gjt", qh, K) / math.sqrt(hd), dim=-1)
+        ref[r] = torch.einsum("gjt,gtd->gjd", w, V).reshape(-1)
+    err = (got.float() - ref).abs().max().item()
+    assert torch.isfinite(got.float()).all() and err < 3e-2, err
+
+
 def test_tc_attention_prefill_rows_causal_and_many_entries(cuda):
     """Prefill-shaped work: 48 rows of one sequence at consecutive positions (causal mask
     inside the chunk, rows sharing pages at different positions), 48 x 4 heads = 192 query
