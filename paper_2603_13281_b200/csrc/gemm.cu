@@ -30,9 +30,9 @@ struct Cfg {
 // Stream-K partition of U units over G CTAs. 32-bit arithmetic (the host guarantees
 // U * (G + 1) < 2^32): 64-bit division is a ~100-instruction software sequence, and the
 // epilogue's critical path evaluates these per tile and per reduced segment.
-// Ring depth: 6 x (16 KB W + X) in flight per SM measured fastest for the decode step
-// (4.12 ms vs 4.32 ms at the 12-stage maximum); p.stages > 0 overrides (tuning tools).
-constexpr int DEFAULT_STAGES = 6;
+// Ring depth: 5 x (16 KB W + X) in flight per SM measured fastest for the decode step
+// (3.594 ms vs 3.625 at 6 stages, 3.68 at 4 and 8; ICR_STAGES sweep); p.stages > 0 overrides.
+constexpr int DEFAULT_STAGES = 5;
 template <int NT>
 __host__ __device__ constexpr int ring_stages(int requested) {
   const int want = requested > 0 ? requested : DEFAULT_STAGES;
