@@ -57,3 +57,25 @@ def test_auto_chunk_pages_rule():
     assert auto_chunk_pages(17424) == 128
     assert auto_chunk_pages(32800) == 128
     assert auto_chunk_pages(1 << 20) == 128
+
+
+def test_missing_library_or_device_fails_loudly():
+    """No CPU fallback: without the built library the product path raises DeviceError, and a
+    runtime refuses to start without a CUDA device (this container has none)."""
+    import subprocess
+    import sys
+    code = ("import os, sys\n"
+            "os.environ['ICR_LIB_PATH'] = '/nonexistent/libicarus_b200.so'\n"
+            "from paper_2603_13281_b200 import _lib\n"
+            "from paper_2603_13281_b200.errors import DeviceError\n"
+            "try:\n    _lib.load()\nexcept DeviceError:\n    sys.exit(0)\nsys.exit(1)\n")
+    root = __import__("pathlib").Path(__file__).resolve().parents[1]
+    assert subprocess.run([sys.executable, "-c", code], cwd=root).returncode == 0
+    import torch
+    if not torch.cuda.is_available():
+        from paper_2603_13281_b200.errors import DeviceError
+        from paper_2603_13281_b200.model import ModelConfig, init_base
+        base = init_base(ModelConfig(num_layers=1, hidden_dim=128, num_heads=2, num_kv_heads=1,
+                                     head_dim=64, ffn_dim=256, vocab_size=256), seed=0)
+        with pytest.raises(DeviceError):
+            base.runtime(max_seqs=2, max_context=64)
