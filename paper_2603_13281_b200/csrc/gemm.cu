@@ -658,7 +658,9 @@ __global__ void __launch_bounds__(256, 1)
         uint8_t* dst = smem + (size_t)stage * C::STAGE + W_BYTES;
         if (lo) {
           if (!lora_ready) {  // U is produced by this grid's shrink warps (2 per CTA)
-            const int target = gridDim.x * 2;  // every shrink warp (2 per CTA) published
+            // every shrink warp (2 per CTA) of this launch published; earlier row-group
+            // launches of the same projection already added their own 2 x grid arrivals
+            const int target = gridDim.x * 2 * (p.sync_round > 0 ? p.sync_round : 1);
             stamp(2);
             while (ld_acquire(p.sync) < target) __nanosleep(32);
             stamp(3);

@@ -73,7 +73,9 @@ struct GemmParams {
   int slots;
   __nv_bfloat16* ubd;           // block-diagonal U [rows_total][ubd_ld] (bf16, TMA operand)
   int ubd_ld;
-  int* sync;                    // shrink-done counter (target: 6 warps x grid)
+  int* sync;                    // shrink-done counter: 2 shrink warps x grid per launch
+  int sync_round;               // 1-based launch index within this projection (row groups of
+                                // <= 256 share the counter, so launch g waits for g x 2 x grid)
   int* reset_sync;              // counter of an EARLIER launch to zero after griddepcontrol.wait
   float* sh_part;               // [SHRINK_SPLITS][rows_total][2][rank] K-split partials
   int* sh_cnt;                  // [2][slots][rank] split arrivals per adapter row (self-resetting)

@@ -53,11 +53,39 @@ def test_llama8b_width_layer_batched_decode_matches_oracle(cuda):
     _check(sess[0].last_logits, ref0.last_logits, "prefill")
     toks = [first, first]
     worst = 0.0
+    oracle_toks, oracle_logits = [], []
     for step in range(2):
         E.decode_step_batch(sess, toks)
         toks = [r.decode_fused(t) for r, t in zip(refs, toks)]  # teacher-forced on the oracle
+        oracle_toks.append(list(toks))
+        oracle_logits.append([r.last_logits.copy() for r in refs])
         for i, (s, r) in enumerate(zip(sess, refs)):
             worst = max(worst, _check(s.last_logits, r.last_logits, f"agent{i} step {step}"))
+    # pin the torch-fp32 oracle (the full-depth checker of tests/test_gpu_c2_full.py) to the
+    # bitwise oracle at this width: same weights, prefill + the same two teacher-forced steps
+    import torch
+    from oracle import torch_ref as R
+    with R.fp32_matmul():
+        tr = R.TorchRef(R.Weights.from_oracle(R.Shape(**C8), w, device="cuda"), max_pos=64)
+        t0 = tr.session(None)
+        assert tr.prefill(t0, prompt) == first
+        pin = [float(np.abs(t0.last_logits.double().cpu().numpy() - ref0.last_logits).max()
+                     / np.abs(ref0.last_logits).max())]
+        ts = []
+        for ad in ads:
+            t = tr.session(R.Adapter.from_oracle(ad, device="cuda"))
+            t.copy_prefix(t0, len(prompt))
+            ts.append(t)
+        feed = [first, first]
+        for step, want_toks in enumerate(oracle_toks):
+            got = tr.decode_fused(ts, feed)
+            for t, r in zip(ts, oracle_logits[step]):
+                pin.append(float(np.abs(t.last_logits.double().cpu().numpy() - r).max() / np.abs(r).max()))
+            assert got == want_toks
+            feed = want_toks
+        assert max(pin) <= 1e-4, pin
+        del tr, t0, ts
+        torch.cuda.empty_cache()
     k, v = sess[0].cache.rows(0, 0, sess[0].cache.position_count)
     rk = refs[0].k[0].reshape(k.shape)
     assert np.abs(k - rk).max() <= 2e-2 * np.abs(rk).max() + 1e-2

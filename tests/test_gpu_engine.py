@@ -108,18 +108,38 @@ def test_c1_two_agents_match_reference(c1_setup):
 
 
 def test_c1_free_running_greedy_matches_reference(c1_setup):
+    """Free-running greedy over the full 33-token horizon (prefill token + 32 steps), every
+    token checked. The oracle (bitwise = reference) is fed the GPU's own tokens, so a
+    reference tie (oracle top-1 vs the GPU's pick within the logit tolerance, the rule of
+    tests/test_acceptance.py:103-108) is logged and the comparison continues on the same
+    trajectory instead of stopping at the first divergence. Without ties the GPU tokens must
+    equal the reference goldens exactly."""
     E, P, M = _mods()
     base, agents, rt = c1_setup
     g = np.load(GOLD / "c1_decode.npz")
+    shape = O.Shape(**C1)
+    w = O.bf16_weights(O.init_base(shape, 0))
+    ad = O.bf16_adapter(O.make_agents(shape, 2, seed=1)[0])
+    prompt = [int(t) for t in g["prompt"]]
     s = E.new_session(base, agents[0], 512, runtime=rt)
-    out = E.generate(s, [int(t) for t in g["prompt"]], max_new=33)
-    want = [int(t) for t in g["a0_tokens"]]
-    # exact unless a reference tie (within tolerance) flips a token; report first divergence
-    first = next((i for i, (a, b) in enumerate(zip(out, want)) if a != b), None)
-    if first is not None:
-        scale = float(np.abs(g["a0_logits"][first - 1]).max())
-        lg = g["a0_logits"][first - 1]
-        assert abs(float(lg[want[first]] - lg[out[first]])) <= LOGIT_TOL * scale
+    out = E.generate(s, prompt, max_new=33)
+    assert len(out) == 33
+    ora = O.Session(shape, w, ad)
+    ties = []
+    want = ora.prefill(prompt)
+    for i in range(33):
+        lg = ora.last_logits
+        scale = float(np.abs(lg).max())
+        if out[i] != want:
+            gap = float(lg[want] - lg[out[i]])
+            assert gap <= LOGIT_TOL * scale, (
+                f"token {i}: GPU {out[i]} vs reference {want}, oracle gap {gap:.4g} > tie band")
+            ties.append((i, want, out[i], gap))
+        if i + 1 < 33:
+            want = ora.decode_fused(out[i])
+    if not ties:
+        assert out == [int(t) for t in g["a0_tokens"]]
+    print(f"free-running horizon 33: {len(ties)} reference ties {ties}")
     s.close()
 
 
@@ -479,3 +499,36 @@ def test_checkpointed_base_and_adapter_drive_the_decode_bitwise(c1_setup, tmp_pa
         assert ta == tb and a.last_logits.tobytes() == b.last_logits.tobytes()
     a.close()
     b.close()
+
+
+def test_over_256_row_adapted_batch_equals_single_session_steps(c1_setup):
+    """A fused step over more than 256 rows runs each projection as several 256-row launches
+    that share one LoRA-shrink counter (the second launch must wait for its own
+    shrink, not the first launch's). 136 adapted sessions = 272 rows, bitwise == alone."""
+    E, P, M = _mods()
+    from paper_2603_13281_b200.runtime import Runtime
+    base, agents, _ = c1_setup
+    rt = Runtime(base, max_seqs=140, max_context=96, max_rows=512, adapter_slots=2, lora_rank=8)
+    rng = np.random.default_rng(21)
+    n = 136
+    prompts = [[int(t) for t in rng.integers(1, 1024, int(rng.integers(5, 40)))] for _ in range(n)]
+    ads = [agents[i % 2] for i in range(n)]
+    batch = [E.new_session(base, ad, 96, runtime=rt, capture_logits=True) for ad in ads]
+    tb = E.prefill_batch(batch, prompts)
+    want = []
+    for ad, pr in zip(ads, prompts):
+        s = E.new_session(base, ad, 96, runtime=rt, capture_logits=True)
+        toks, lgs = [E.prefill(s, pr)], []
+        for _ in range(3):
+            toks.append(E.decode_step_fused(s, toks[-1]))
+            lgs.append(s.last_logits.tobytes())
+        want.append((toks, lgs))
+        s.close()
+    assert tb == [w[0][0] for w in want]
+    for step in range(3):
+        tb = E.decode_step_batch(batch, tb)
+        assert tb == [w[0][step + 1] for w in want], f"step {step}"
+        for i, s in enumerate(batch):
+            assert s.last_logits.tobytes() == want[i][1][step], f"session {i} step {step}"
+    for s in batch:
+        s.close()
