@@ -114,7 +114,9 @@ typedef struct icr_batch {
   const int32_t* row_seq;     /* host [n_rows] block-table row                         */
   const int32_t* row_pos;     /* host [n_rows] absolute position                       */
   const int32_t* row_adapter; /* host [n_rows] adapter slot for decoder rows, else -1  */
-  const int32_t* row_emit;    /* host [n_rows] 1 = run the LM head + argmax on this row */
+  const int32_t* row_emit;    /* host [n_rows] 1 = run the LM head + argmax on this row (and
+                                 keep its final hidden for icr_seq_logits), 2 = the same
+                                 without keeping it, 0 = no LM head                       */
   const int32_t* block_table; /* host [max_seqs][max_pages_per_seq] page ids           */
   int n_seqs;                 /* block-table rows referenced                           */
 } icr_batch;
@@ -191,6 +193,37 @@ icr_status icr_paged_attention(const void* q_dev, const void* k_pages, const voi
                                const int32_t* row_pos_host, const int32_t* block_table_host,
                                int n_seqs, int max_pages_per_seq, void* out_dev,
                                int32_t* n_items_out, void* stream);
+
+/* --- the reference's module-level model functions (model.py:334-538) ------------- */
+
+/* One transformer layer of the hot path (block_forward, model.py:441-506, and
+ * decoder_block_readonly, :511-538) over explicit fp32 input rows x_in_dev [n_rows][d]
+ * (device), writing the layer output rows to x_out_dev [n_rows][d]. Rows as in icr_batch
+ * (tokens are ignored; row_emit must be 0): prefill = S encoder rows, fused decode = an
+ * encoder row + a decoder row, read-only decoder pass = one decoder row. Encoder rows write
+ * their K/V into this layer's pages. The same kernels, in the same order, as icr_forward's
+ * layer `layer`. Synchronises the stream. */
+icr_status icr_layer_forward(icr_model* m, const icr_batch* b, int layer, const float* x_in_dev,
+                             float* x_out_dev, void* stream);
+
+/* session.last_logits (engine.py:190-192) on demand: fp32 logits [n][vocab_pad] of the final
+ * hidden states kept by the last forward that emitted them -- store slot 2*seq + kind
+ * (kind 0 encoder row, 1 decoder row) holds the last row of that sequence and kind with
+ * row_emit == 1 (row_emit == 2 emits without replacing the stored hidden). Bitwise equal to
+ * the logits icr_forward writes when given logits_dev. Synchronises the stream. */
+icr_status icr_seq_logits(icr_model* m, const int32_t* slots_host, int n, float* logits_dev,
+                          void* stream);
+
+/* base_linear / adapted_linear / icarus_linear (model.py:334-371) for arbitrary weights:
+ * out_dev[n][m] = sum_k W[m][k] x[n][k], plus on rows with row_adapted_host[n] != 0 the
+ * low-rank term sum_j (x[n] . A[j]) * Bs[m][j] (LoRA shrink + expand inside the same tcgen05
+ * GEMM, as in the decode step). W [M][K] bf16 row-major (dev), x [n_rows][K] bf16 (dev),
+ * A [rank][K] bf16 (dev), Bs = scaling * B stored tile-major [M/128][1][128][64] bf16 (dev,
+ * columns >= rank zero). M % 128 == 0, K % 64 == 0, rank <= 32 (0 = no low-rank term).
+ * Synchronises the stream. */
+icr_status icr_linear_bf16(const void* w_dev, const void* x_dev, float* out_dev, int M, int K,
+                           int n_rows, const void* a_dev, const void* bs_blocked_dev, int rank,
+                           const int32_t* row_adapted_host, void* stream);
 
 const char* icr_last_error(void);
 int icr_abi_version(void);

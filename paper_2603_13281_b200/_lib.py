@@ -27,7 +27,8 @@ _STATUS = {
 EXPORTED = (
     "icr_model_create", "icr_model_destroy", "icr_forward", "icr_decode_loop",
     "icr_model_stats", "icr_profile_step", "icr_profile_gemm", "icr_profile_ablate", "icr_profile_trace", "icr_host_timing", "icr_bench_gemm",
-    "icr_bench_attention", "icr_gemm_bf16", "icr_paged_attention",
+    "icr_bench_attention", "icr_gemm_bf16", "icr_paged_attention", "icr_layer_forward",
+    "icr_seq_logits", "icr_linear_bf16",
     "icr_last_error", "icr_abi_version", "icr_num_sms",
 )
 
@@ -89,6 +90,9 @@ def load():
         "icr_bench_attention": [p, p, p, i, i, i, i, i, C.POINTER(C.c_int32),
                                 C.POINTER(C.c_int32), C.POINTER(C.c_int32), i, i, p, p,
                                 C.c_longlong, i, i, C.POINTER(C.c_float), C.POINTER(C.c_int32), p],
+        "icr_layer_forward": [p, C.POINTER(BatchC), i, p, p, p],
+        "icr_seq_logits": [p, C.POINTER(C.c_int32), i, p, p],
+        "icr_linear_bf16": [p, p, p, i, i, i, p, p, i, C.POINTER(C.c_int32), p],
         "icr_paged_attention": [p, p, p, i, i, i, i, i, C.POINTER(C.c_int32),
                                 C.POINTER(C.c_int32), C.POINTER(C.c_int32), i, i, p,
                                 C.POINTER(C.c_int32), p],

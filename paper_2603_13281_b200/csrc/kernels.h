@@ -104,10 +104,18 @@ __device__ __forceinline__ void prefetch_slice_l2(const uint8_t* base, long long
 }
 
 // Emitting rows for the LM head: hlm[i] = xb[lm_rows[i]], ssq_lm[c][i] = ssq[c][lm_rows[i]];
-// rows n_lm..n_pad-1 are zero.
+// rows n_lm..n_pad-1 are zero. store_slot[i] >= 0 also keeps row i in the per-sequence hidden
+// store (hid, hid_ssq); from_store = 1 gathers from the store instead (lm_rows = store slots).
 cudaError_t lm_gather_launch(const __nv_bfloat16* xb, const float* ssq, int ss_stride,
                              const int* lm_rows, int n_lm, int n_pad, int d,
-                             __nv_bfloat16* hlm, float* ssq_lm, cudaStream_t s);
+                             __nv_bfloat16* hlm, float* ssq_lm, const int* store_slot,
+                             __nv_bfloat16* hid, float* hid_ssq, int hid_stride, int from_store,
+                             cudaStream_t s);
+
+// Layer input from an explicit fp32 residual stream (same outputs as embed_launch).
+cudaError_t resid_load_launch(const float* x_in, int n_valid, int n_rows, float* x,
+                              __nv_bfloat16* xb, float* ssq, int ss_stride, int d,
+                              __nv_bfloat16* ubd, int ubd_ld, cudaStream_t s);
 
 // Final argmax over LM-head tiles (lowest index on ties, src/engine.py:75-76).
 cudaError_t argmax_reduce_launch(const float2* tile_best, int tiles, int stride, int n_rows,

@@ -251,6 +251,7 @@ struct Meta {
   size_t items_cap = 0, rows_cap = 0, pages_cap = 0;
   size_t o_tokens = 0, o_kind = 0, o_seq = 0, o_pos = 0, o_adapter = 0, o_lm_rows = 0,
          o_seg_off = 0, o_seg_rows = 0, o_n_items = 0, o_feedback = 0, o_bt = 0, o_items = 0,
+         o_lm_store = 0,
          o_item_rows = 0, o_item_pages = 0, total = 0, used = 0;
 };
 
@@ -293,6 +294,9 @@ struct icr_model {
   int ubd_ld = 0, lc1 = 0, lc2 = 0;  // U row stride; LoRA K chunks for 1 / 2 targets
   float2* tile_best = nullptr;
   int* out_tok = nullptr;
+  __nv_bfloat16* hid = nullptr;  // per-(sequence, kind) final hidden of the last emitting row
+  float* hid_ssq = nullptr;      // its per-128-feature sums of squares [ss_tiles][2*max_seqs]
+  int* slot_idx = nullptr;       // icr_seq_logits: store slots of the requested rows
   float* part_o = nullptr;
   float2* part_ml = nullptr;
   int* merge_cnt = nullptr;
@@ -357,6 +361,7 @@ static Meta layout_meta(const icr_model* m, int n_rows) {
   mt.o_pos = take(mt.rp);
   mt.o_adapter = take(mt.rp);
   mt.o_lm_rows = take(mt.rp);
+  mt.o_lm_store = take(mt.rp);
   mt.o_seg_off = take(c.adapter_slots + 1);
   mt.o_seg_rows = take(mt.rp);
   mt.o_n_items = take(1);
@@ -410,6 +415,17 @@ static icr_status pack_meta(icr_model* m, const icr_batch* b, const int* pos, co
   }
   mt.n_lm = n_lm;
   mt.n_lm_pad = (n_lm + 15) & ~15;
+  {  // hidden store: the last row with row_emit == 1 of each (sequence, kind) keeps its final
+     // hidden for on-demand logits (icr_seq_logits); row_emit == 2 emits without storing
+    std::vector<int> last((size_t)c.max_seqs * 2, -1);
+    for (int r = 0; r < n; ++r)
+      if (b->row_emit && b->row_emit[r] == 1) last[(size_t)b->row_seq[r] * 2 + b->row_kind[r]] = r;
+    for (int i = 0; i < n_lm; ++i) {
+      const int r = t[mt.o_lm_rows + i];
+      const int slot = b->row_seq[r] * 2 + b->row_kind[r];
+      t[mt.o_lm_store + i] = (b->row_emit[r] == 1 && last[slot] == r) ? slot : -1;
+    }
+  }
   mt.n_dec = n_dec;
   int* seg_off = t + mt.o_seg_off;
   int* seg_rows = t + mt.o_seg_rows;
@@ -445,13 +461,20 @@ static icr_status validate_batch(icr_model* m, const icr_batch* b, const int* po
       return fail(ICR_CONFIG, "row %d adapter slot %d invalid (kind %d, %d slots)", r, b->row_adapter[r], k, c.adapter_slots);
     if (pos[r] < 0 || pos[r] >= c.max_positions)
       return fail(ICR_CAPACITY, "row %d position %d outside [0, %d)", r, pos[r], c.max_positions);
+    if (b->row_seq[r] < 0 || b->row_seq[r] >= c.max_seqs)
+      return fail(ICR_SHAPE, "row %d sequence slot %d outside [0, %d)", r, b->row_seq[r], c.max_seqs);
+    if (b->row_emit && (b->row_emit[r] < 0 || b->row_emit[r] > 2))
+      return fail(ICR_MODE, "row %d emit flag %d must be 0, 1 or 2", r, b->row_emit[r]);
   }
   return ICR_OK;
 }
 
 
 // Enqueue the whole forward on `s` using metadata resident at m->meta_dev (layout mt).
-static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_dev, cudaStream_t s) {
+// layer_only >= 0: just that layer over the explicit fp32 input rows x_in (n_valid rows),
+// no embedding and no LM head (icr_layer_forward).
+static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_dev, cudaStream_t s,
+                                  int layer_only = -1, const float* x_in = nullptr) {
   const icr_model_config& c = m->cfg;
   int* md = m->meta_dev;
   const int* tokens = md + mt.o_tokens;
@@ -480,6 +503,7 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
       GemmParams q = p;
       q.n_rows = gr;
       q.row0 = g0;
+      q.sync_round = g0 / 256 + 1;
       if (m->trace) q.trace = m->trace + (size_t)launches * 4096 * 16;
       cudaError_t e = gemm_launch(wmap, xmaps[nt_index(nt)], lbmap,
                                   lbmap ? &m->xmap_ubd[nt_index(nt)] : nullptr, q, g0, nt,
@@ -543,12 +567,18 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
 
   const int qkv_M = m->q_dim + 2 * m->kv_dim;
   const bool pf_on = rp <= 256 && getenv("ICR_L2_PREFETCH") != nullptr;
-  CUDA_TRY(embed_launch(tokens, kind, m->embed, m->x, m->xb, m->ssq, rp, rp, d,
-                        pf_on ? (const uint8_t*)m->layers[0].w_qkv : nullptr,
-                        (long long)qkv_M * d * 2, m->ubd, m->ubd_ld, s));
+  if (layer_only >= 0) {
+    CUDA_TRY(resid_load_launch(x_in, mt.n_rows, rp, m->x, m->xb, m->ssq, rp, d, m->ubd, m->ubd_ld, s));
+  } else {
+    CUDA_TRY(embed_launch(tokens, kind, m->embed, m->x, m->xb, m->ssq, rp, rp, d,
+                          pf_on ? (const uint8_t*)m->layers[0].w_qkv : nullptr,
+                          (long long)qkv_M * d * 2, m->ubd, m->ubd_ld, s));
+  }
   ++launches;
   mark(m, s, TK_EMBED);
-  for (int l = 0; l < c.num_layers; ++l) {
+  const int l_begin = layer_only >= 0 ? layer_only : 0;
+  const int l_end = layer_only >= 0 ? layer_only + 1 : c.num_layers;
+  for (int l = l_begin; l < l_end; ++l) {
     const icr_layer_weights& w = m->layers[l];
     const LayerMaps& lm = m->maps[l];
     {  // q, k, v (src/model.py:485-496)
@@ -645,9 +675,10 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
     }
   }
   // final norm on emitting rows + LM head + argmax (src/engine.py:188-193)
-  if (mt.n_lm > 0) {
+  if (mt.n_lm > 0 && layer_only < 0) {
     CUDA_TRY(lm_gather_launch(m->xb, m->ssq, rp, lm_rows, mt.n_lm, mt.n_lm_pad, d, m->hlm,
-                              m->ssq_lm, s));
+                              m->ssq_lm, md + mt.o_lm_store, m->hid, m->hid_ssq,
+                              2 * c.max_seqs, 0, s));
     ++launches;
     mark(m, s, TK_LMG);
     GemmParams p = base;
@@ -677,10 +708,12 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
       if ((st = gemm(m->lm_map, m->xmap_hlm, q, mt.n_lm))) return st;
     }
   }
-  m->last_launches = launches;
-  m->last_items = mt.n_items;
-  m->last_mt = mt;
-  m->has_last = true;
+  if (layer_only < 0) {
+    m->last_launches = launches;
+    m->last_items = mt.n_items;
+    m->last_mt = mt;
+    m->has_last = true;
+  }
   return ICR_OK;
 }
 
@@ -719,7 +752,7 @@ static icr_status run_forward(icr_model* m, const Meta& mt, float* logits_dev, c
 extern "C" {
 
 const char* icr_last_error(void) { return g_err.c_str(); }
-int icr_abi_version(void) { return 1; }
+int icr_abi_version(void) { return 2; }
 int icr_num_sms(void) { return query_sms(); }
 
 icr_status icr_model_create(const icr_model_config* cfg, const icr_layer_weights* layers,
@@ -794,6 +827,9 @@ icr_status icr_model_create(const icr_model_config* cfg, const icr_layer_weights
   ALLOC(m->ubd, rp * m->ubd_ld * 2);
   ALLOC(m->tile_best, (size_t)(m->vpad / 128) * rp * sizeof(float2));
   ALLOC(m->out_tok, rp * sizeof(int));
+  ALLOC(m->hid, (size_t)2 * c.max_seqs * c.hidden_dim * 2);
+  ALLOC(m->hid_ssq, (size_t)m->ss_tiles * 2 * c.max_seqs * sizeof(float));
+  ALLOC(m->slot_idx, rp * sizeof(int));
   ALLOC(m->part_o, rp * c.num_heads * m->max_chunks * c.head_dim * sizeof(float));
   ALLOC(m->part_ml, rp * c.num_heads * m->max_chunks * sizeof(float2));
   ALLOC(m->merge_cnt, rp * c.num_kv_heads * sizeof(int));
@@ -871,7 +907,7 @@ icr_status icr_model_destroy(icr_model* m) {
   cudaDeviceSynchronize();
   for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
   void* bufs[] = {m->x, m->xb, m->ssq, m->ssq_lm, m->qb, m->att, m->f, m->hlm, m->ubd,
-                  m->tile_best, m->out_tok, m->part_o, m->part_ml, m->merge_cnt, m->rope, m->ws,
+                  m->tile_best, m->out_tok, m->hid, m->hid_ssq, m->slot_idx, m->part_o, m->part_ml, m->merge_cnt, m->rope, m->ws,
                   m->counters, m->sync, m->sh_part, m->sh_cnt, m->meta_dev};
   for (void* p : bufs)
     if (p) cudaFree(p);
@@ -1636,6 +1672,199 @@ icr_status icr_paged_attention(const void* q_dev, const void* k_pages, const voi
   for (void* p : bufs) cudaFree(p);
   if (e != cudaSuccess) return fail(ICR_CUDA, "attention: %s", cudaGetErrorString(e));
   if (e2 != cudaSuccess) return fail(ICR_CUDA, "attention sync: %s", cudaGetErrorString(e2));
+  return ICR_OK;
+}
+
+// ---- module-level building blocks (the reference's model.py functions) ----
+
+icr_status icr_layer_forward(icr_model* m, const icr_batch* b, int layer, const float* x_in_dev,
+                             float* x_out_dev, void* stream) {
+  if (!m || !b || !x_in_dev || !x_out_dev) return fail(ICR_CONFIG, "null argument");
+  if (layer < 0 || layer >= m->cfg.num_layers)
+    return fail(ICR_SHAPE, "layer %d outside [0, %d)", layer, m->cfg.num_layers);
+  cudaStream_t s = (cudaStream_t)stream;
+  icr_status st = validate_batch(m, b, b->row_pos);
+  if (st) return st;
+  for (int r = 0; r < b->n_rows; ++r)
+    if (b->row_emit && b->row_emit[r]) return fail(ICR_MODE, "a layer forward emits no tokens");
+  AttnPlan plan;
+  st = build_attn_plan(b->n_rows, b->row_kind, b->row_seq, b->row_pos, b->block_table, b->n_seqs,
+                       m->cfg.max_pages_per_seq, m->cfg.num_pages, plan_group(m),
+                       m->cfg.chunk_pages, plan, m->cfg.head_dim);
+  if (st) return st;
+  Meta mt = layout_meta(m, b->n_rows);
+  if ((st = ensure_meta(m, mt.total))) return st;
+  CUDA_TRY(cudaEventSynchronize(m->staging_ev[0]));
+  if ((st = pack_meta(m, b, b->row_pos, nullptr, plan, m->staging[0], mt))) return st;
+  CUDA_TRY(cudaMemcpyAsync(m->meta_dev, m->staging[0], mt.used * sizeof(int), cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaEventRecord(m->staging_ev[0], s));
+  if ((st = enqueue_forward(m, mt, nullptr, s, layer, x_in_dev))) return st;
+  CUDA_TRY(cudaMemcpyAsync(x_out_dev, m->x, (size_t)b->n_rows * m->cfg.hidden_dim * sizeof(float),
+                           cudaMemcpyDeviceToDevice, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return ICR_OK;
+}
+
+icr_status icr_seq_logits(icr_model* m, const int32_t* slots_host, int n, float* logits_dev,
+                          void* stream) {
+  if (!m || !slots_host || !logits_dev) return fail(ICR_CONFIG, "null argument");
+  if (n < 1 || n > m->rp) return fail(ICR_SHAPE, "%d rows outside [1, %d]", n, m->rp);
+  for (int i = 0; i < n; ++i)
+    if (slots_host[i] < 0 || slots_host[i] >= 2 * m->cfg.max_seqs)
+      return fail(ICR_SHAPE, "store slot %d outside [0, %d)", slots_host[i], 2 * m->cfg.max_seqs);
+  cudaStream_t s = (cudaStream_t)stream;
+  const icr_model_config& c = m->cfg;
+  CUDA_TRY(cudaMemcpyAsync(m->slot_idx, slots_host, n * sizeof(int), cudaMemcpyHostToDevice, s));
+  const int n_pad = (n + 15) & ~15;
+  CUDA_TRY(lm_gather_launch(m->xb, m->ssq, m->rp, m->slot_idx, n, n_pad, c.hidden_dim, m->hlm,
+                            m->ssq_lm, nullptr, m->hid, m->hid_ssq, 2 * c.max_seqs, 1, s));
+  GemmParams p{};
+  p.mode = EPI_F32;
+  p.w_blocked = 1;
+  p.ws = m->ws;
+  p.counters = m->counters;
+  p.rank = c.lora_rank;
+  p.M = m->vpad;
+  p.K = c.hidden_dim;
+  p.m_valid = 1 << 30;
+  p.in_ssq = m->ssq_lm;
+  p.ss_tiles = m->ss_tiles;
+  p.ss_stride = m->rp;
+  p.ss_d = (float)c.hidden_dim;
+  p.eps = c.rms_eps;
+  p.rows_total = m->rp;
+  p.out_f32 = logits_dev;
+  p.ld_out = m->vpad;
+  for (int g0 = 0; g0 < n; g0 += 256) {
+    GemmParams q = p;
+    q.n_rows = std::min(256, n - g0);
+    q.row0 = g0;
+    const int nt = gemm_pick_nt(q.n_rows);
+    cudaError_t e = gemm_launch(m->lm_map, m->xmap_hlm[nt_index(nt)], nullptr, nullptr, q, g0, nt,
+                                m->num_sms, s);
+    if (e != cudaSuccess) return fail(ICR_CUDA, "logits gemm: %s", cudaGetErrorString(e));
+  }
+  CUDA_TRY(cudaStreamSynchronize(s));
+  return ICR_OK;
+}
+
+static size_t lora_b_bytes(int rank, int M) { return rank > 0 ? 256 : (size_t)M * 64 * 2; }
+
+// out[n][m] = sum_k W[m][k] x[n][k]  (+ on rows with row_adapted[n]: the low-rank term
+// sum_j (x[n] . A[j]) * Bs[m][j], U = x A^T rounded to bf16 as in the decode step). The
+// tcgen05 stream-K kernel of every projection, with the LoRA as one extra 64-wide K chunk --
+// ALWAYS present (zero U when no row is adapted), so base_linear, adapted_linear with B = 0
+// and icarus_linear's encoder row are bitwise the same computation (src/model.py:334-371).
+icr_status icr_linear_bf16(const void* w_dev, const void* x_dev, float* out_dev, int M, int K,
+                           int n_rows, const void* a_dev, const void* bs_blocked_dev, int rank,
+                           const int32_t* row_adapted_host, void* stream) {
+  if (M % 128 || K % 64 || M <= 0 || K <= 0 || n_rows <= 0)
+    return fail(ICR_SHAPE, "icr_linear_bf16 needs M %% 128 == 0, K %% 64 == 0 (M=%d K=%d rows=%d)",
+                M, K, n_rows);
+  if (rank < 0 || rank > 32 || (rank > 0 && (!a_dev || !bs_blocked_dev || !row_adapted_host)))
+    return fail(ICR_CONFIG, "low-rank term needs 0 < rank <= 32, A, B and the adapted-row flags");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int sms = query_sms();
+  const int rp = (n_rows + 15) & ~15;
+  const int r8 = std::max(8, (rank + 7) & ~7);
+  std::vector<int> seg_off(2, 0), seg_rows;
+  std::vector<int> kind(rp, -1), adapter(rp, -1);
+  for (int r = 0; r < n_rows; ++r) {
+    const bool ad = rank > 0 && row_adapted_host[r];
+    kind[r] = ad ? 1 : 0;
+    adapter[r] = ad ? 0 : -1;
+    if (ad) seg_rows.push_back(r);
+  }
+  seg_off[1] = (int)seg_rows.size();
+  // scratch, stream ordered
+  const size_t ws_b = gemm_ws_floats(sms) * sizeof(float), cnt_b = (size_t)(M / 128) * sizeof(int);
+  const int splits = (K + 4095) / 4096;
+  const size_t shp_b = (size_t)splits * rp * 2 * r8 * sizeof(float), shc_b = (size_t)2 * r8 * sizeof(int);
+  const size_t zb_b = lora_b_bytes(rank, M), ubd_b = (size_t)rp * 64 * 2, meta_n = 2 * (size_t)rp + 2 + std::max<size_t>(seg_rows.size(), 1) + 4;
+  char* scratch = nullptr;
+  const size_t total = ws_b + cnt_b + 256 + shp_b + shc_b + ubd_b + zb_b + meta_n * sizeof(int) + 9 * 256;
+  CUDA_TRY(cudaMallocAsync((void**)&scratch, total, s));
+  size_t off = 0;
+  auto carve = [&](size_t bytes) { char* p = scratch + off; off += (bytes + 255) & ~size_t(255); return p; };
+  float* ws = (float*)carve(ws_b);
+  int* counters = (int*)carve(cnt_b);
+  int* sync = (int*)carve(256);
+  float* sh_part = (float*)carve(shp_b);
+  int* sh_cnt = (int*)carve(shc_b);
+  __nv_bfloat16* ubd = (__nv_bfloat16*)carve(ubd_b);
+  __nv_bfloat16* zb_ptr = (__nv_bfloat16*)carve(zb_b);  // all-zero B chunk (no adapter)
+  int* dmeta = (int*)carve(meta_n * sizeof(int));
+  std::vector<int> hmeta(meta_n, 0);
+  std::copy(kind.begin(), kind.end(), hmeta.begin());
+  std::copy(adapter.begin(), adapter.end(), hmeta.begin() + rp);
+  std::copy(seg_off.begin(), seg_off.end(), hmeta.begin() + 2 * rp);
+  std::copy(seg_rows.begin(), seg_rows.end(), hmeta.begin() + 2 * rp + 2);
+  icr_status st = ICR_OK;
+  cudaError_t e = cudaSuccess;
+  CUtensorMap wm, lbm, lum;
+  const bool lora = rank > 0;
+  do {
+    if ((e = cudaMemsetAsync(scratch + ws_b, 0, off - ws_b, s)) != cudaSuccess) break;
+    if ((e = cudaMemcpyAsync(dmeta, hmeta.data(), meta_n * sizeof(int), cudaMemcpyHostToDevice, s)) != cudaSuccess) break;
+    if ((st = make_map(&wm, w_dev, M, K, 128))) break;
+    // the low-rank chunk: B (tile-major, 64 columns) against the U rows; a zero chunk over a
+    // zero U when no adapter is given keeps the stream-K partition identical
+    if (lora) { if ((st = make_map_blocked(&lbm, bs_blocked_dev, M, 64))) break; }
+    for (int g0 = 0; g0 < n_rows && st == ICR_OK && e == cudaSuccess; g0 += 256) {
+      const int gr = std::min(256, n_rows - g0);
+      const int nt = gemm_pick_nt(gr);
+      CUtensorMap xm;
+      if ((st = make_map(&xm, x_dev, n_rows, K, nt))) break;
+      if ((st = make_map(&lum, ubd, rp, 64, nt))) break;
+      GemmParams p{};
+      p.mode = EPI_F32;
+      p.M = M;
+      p.K = K;
+      p.n_rows = gr;
+      p.row0 = g0;
+      p.rows_total = rp;
+      p.m_valid = M;
+      p.out_f32 = out_dev;
+      p.ld_out = M;
+      p.ws = ws;
+      p.counters = counters;
+      p.row_kind = dmeta;
+      p.row_adapter = dmeta + rp;
+      p.lora_chunks = 1;
+      p.rank = lora ? rank : 8;
+      p.ubd = ubd;
+      p.ubd_ld = 64;
+      p.slots = 1;
+      p.seg_off = dmeta + 2 * rp;
+      p.seg_rows = dmeta + 2 * rp + 2;
+      p.sync = sync;
+      p.sync_round = g0 / 256 + 1;
+      p.sh_part = sh_part;
+      p.sh_cnt = sh_cnt;
+      if (lora) {
+        p.sh_x = (const __nv_bfloat16*)x_dev;
+        p.sh_ld = K;
+        p.sh_K = K;
+        p.sh_targets = 1;
+        p.sh_a0 = (const __nv_bfloat16*)a_dev;
+      }
+      // without an adapter the LoRA chunk streams the (all-zero) U against itself as "B": any
+      // finite values times a zero U add exact zeros; with no shrink the producer's U wait is
+      // pre-satisfied below
+      CUtensorMap zb;
+      if (!lora) { if ((st = make_map_blocked(&zb, zb_ptr, M, 64))) break; }
+      if (!lora) {
+        const int big = 0x3fffffff;
+        if ((e = cudaMemcpyAsync(sync, &big, sizeof(int), cudaMemcpyHostToDevice, s)) != cudaSuccess) break;
+      }
+      e = gemm_launch(wm, xm, lora ? &lbm : &zb, &lum, p, g0, nt, sms, s);
+    }
+  } while (0);
+  cudaError_t e2 = cudaStreamSynchronize(s);
+  cudaFreeAsync(scratch, s);
+  if (st) return st;
+  if (e != cudaSuccess) return fail(ICR_CUDA, "linear: %s", cudaGetErrorString(e));
+  if (e2 != cudaSuccess) return fail(ICR_CUDA, "linear sync: %s", cudaGetErrorString(e2));
   return ICR_OK;
 }
 

@@ -32,7 +32,15 @@ class GenerationSession:
 
     `base_next` maps a computed position to the base model's greedy next token (the
     encoder row's argmax) -- what the reference derives from `final_hidden` for chunk-end
-    commits (engine.py:274-284)."""
+    commits (engine.py:274-284).
+
+    `last_logits` keeps the reference contract (engine.py:127, 191, 214, 232: the logits of
+    the last emitted token, None after a stored full-prefix hit) without paying for them on
+    every step: each emitting forward keeps the row's final hidden state on the device (one
+    slot per sequence and row kind), and the first read of `last_logits` runs the LM head
+    over it -- the same GEMM over the same inputs as the fused step, so the values are
+    bitwise those the step would have produced. `capture_logits=True` computes them eagerly
+    inside every forward instead. A closed session keeps only logits already read."""
 
     def __init__(self, base: BaseWeights, adapter: Optional[AdapterSet], max_context: int,
                  ledger: Optional[Ledger] = None, runtime=None, capture_logits: bool = False):
@@ -63,15 +71,52 @@ class GenerationSession:
         self.prompt: list[int] = []
         self.produced: list[int] = []
         self.base_next: dict[int, int] = {}
-        self.last_logits: Optional[np.ndarray] = None
+        self._ll: Optional[np.ndarray] = None
+        self._ll_kind: Optional[int] = None  # row kind whose stored hidden is pending
+        self._computed: list = []  # [lo, hi) position ranges this session computed itself
         self.borrowed_chain: list = []
         self._prefilled = False
         self._closed = False
+
+    @property
+    def last_logits(self) -> Optional[np.ndarray]:
+        if self._ll_kind is not None and not self._closed:
+            lg = self.runtime.seq_logits([2 * self.seq + self._ll_kind])
+            self._ll = lg[0].cpu().numpy()
+            self._ll_kind = None
+        return self._ll
+
+    @last_logits.setter
+    def last_logits(self, value) -> None:
+        self._ll = value
+        self._ll_kind = None
+
+    def _logits_pending(self, kind: int) -> None:
+        """The last forward kept this session's row of `kind` in the hidden store."""
+        self._ll = None
+        self._ll_kind = kind
+
+    def _set_logits(self, lg, row: int, kind: int) -> None:
+        if self.capture_logits and lg is not None:
+            self.last_logits = _logits_np(lg, row)
+        else:
+            self._logits_pending(kind)
+
+    def _note_computed(self, lo: int, hi: int) -> None:
+        if self._computed and self._computed[-1][1] == lo:
+            self._computed[-1][1] = hi
+        else:
+            self._computed.append([lo, hi])
+
+    def computed(self, pos: int) -> bool:
+        """Did this session compute position `pos` itself (the reference's final_hidden)?"""
+        return any(lo <= pos < hi for lo, hi in self._computed)
 
     def close(self) -> None:
         """Return the sequence slot and this session's page references."""
         if self._closed:
             return
+        self._ll_kind = None
         self._closed = True
         self.cache.release()
         self.runtime.release_seq(self.seq)
@@ -150,7 +195,7 @@ def prefill(session: GenerationSession, prompt, pool=None, namespace: Optional[s
         session.cache.ensure_pages(n - 1)
         session._sync_block_table()
         step = rt.max_rows
-        token, last_lg = None, None
+        token = None
         for c0 in range(matched, n, step):
             c1 = min(n, c0 + step)
             pos = np.arange(c0, c1, dtype=np.int32)
@@ -164,11 +209,11 @@ def prefill(session: GenerationSession, prompt, pool=None, namespace: Optional[s
                 session.base_next[int(p)] = int(t)
             if c1 == n:
                 token = int(out[-1])
-                last_lg = _logits_np(lg, int(emit.sum()) - 1)
+                session._set_logits(lg, int(emit.sum()) - 1, 0)
         led.prefill_tokens += len(suffix)
         led.kv_bytes_written += len(suffix) * cfg.kv_bytes_per_token
         led.param_matrix_reads += _reads_per_step(session)
-        session.last_logits = last_lg
+        session._note_computed(matched, n)
     else:
         token = _full_hit_token(session, toks, chain)
     session.prompt = toks
@@ -191,7 +236,7 @@ def _full_hit_token(session: GenerationSession, toks: list, chain: list) -> int:
                                       adapter=[-1], emit=[1], logits=session.capture_logits)
     token = int(out[0])
     session.base_next[n - 1] = token
-    session.last_logits = _logits_np(lg, 0)
+    session._set_logits(lg, 0, 1)
     session.ledger.prefill_tokens += 1
     session.ledger.param_matrix_reads += 5 * session.config.num_layers + 1
     return token
@@ -234,6 +279,7 @@ def _prefill_setup(sessions, prompts, pool, namespace, readers, rt):
         session.ledger.prefill_tokens += n - matched
         session.ledger.kv_bytes_written += (n - matched) * session.config.kv_bytes_per_token
         session.ledger.param_matrix_reads += _reads_per_step(session)
+        session._note_computed(matched, n)
     return rows, firsts
 
 
@@ -248,7 +294,7 @@ def _collect_prefill_outputs(sessions, chunk, r0, last_row, want, out, lg, e, fi
         session.base_next[r[2]] = int(out[e])
         if last_row[r[0]] == r0 + j:
             firsts[r[0]] = int(out[e])
-            session.last_logits = _logits_np(lg, e) if want[j] else None
+            session._set_logits(lg if want[j] else None, e, 0)
         e += 1
     for i, c in counts.items():
         sessions[i].cache.advance(c)
@@ -323,6 +369,14 @@ def _prepare_write(session: GenerationSession, pos: int) -> None:
     session._sync_appended_pages()
 
 
+def _finish_step(s: GenerationSession, p: int, out, lg, enc: int, dec: int) -> None:
+    s.cache.advance(1)
+    s.base_next[p] = int(out[enc])
+    s._set_logits(lg, dec, 1 if dec != enc else 0)
+    s._note_computed(p, p + 1)
+    _account_step(s, p, passes=1, reads=_reads_per_step(s))
+
+
 def decode_step_batch(sessions: Sequence[GenerationSession], tokens: Sequence[int]) -> list[int]:
     """ONE fused forward for many sessions (each its own adapter): per session an encoder
     row and -- if adapted -- a decoder row. Returns each session's next token."""
@@ -352,10 +406,7 @@ def decode_step_batch(sessions: Sequence[GenerationSession], tokens: Sequence[in
     out, lg = rt.forward(tok, kind, seq, pos, ad, emit, logits=want_logits)
     nxt = []
     for s, p, enc, dec in plan:
-        s.cache.advance(1)
-        s.base_next[p] = int(out[enc])
-        s.last_logits = _logits_np(lg, dec) if s.capture_logits else None
-        _account_step(s, p, passes=1, reads=_reads_per_step(s))
+        _finish_step(s, p, out, lg, enc, dec)
         nxt.append(int(out[dec]))
     return nxt
 
@@ -422,10 +473,7 @@ def step_batch(sessions: Sequence[GenerationSession], tokens: Sequence[int],
         e = 0
         if ci == 0:
             for s, p, enc, dec in plan:
-                s.cache.advance(1)
-                s.base_next[p] = int(out[enc])
-                s.last_logits = _logits_np(lg, dec) if s.capture_logits else None
-                _account_step(s, p, passes=1, reads=_reads_per_step(s))
+                _finish_step(s, p, out, lg, enc, dec)
                 nxt.append(int(out[dec]))
             e = n_dec  # every decode row emits
         _collect_prefill_outputs(new_sessions, chunk, r0, last_row, want, out, lg, e, firsts)
@@ -447,9 +495,10 @@ def decode_step_sequential(session: GenerationSession, token: int) -> int:
     out, _ = rt.forward([token], [0], [session.seq], [pos], [-1], [1])
     session.cache.advance(1)
     session.base_next[pos] = int(out[0])
+    session._note_computed(pos, pos + 1)
     out2, lg = rt.forward([token], [1], [session.seq], [pos], [session.adapter_slot], [1],
                           logits=session.capture_logits)
-    session.last_logits = _logits_np(lg, 0)
+    session._set_logits(lg, 0, 1)
     L = session.config.num_layers
     _account_step(session, pos, passes=2, reads=7 * L + 5 * L + 1)
     return int(out2[0])
@@ -514,16 +563,18 @@ def replay_base(base: BaseWeights, tokens, prompt_len: int, max_context: Optiona
 
 
 def base_next_token_at(session: GenerationSession, pos: int) -> int:
-    """Greedy base prediction at a computed position (engine.py:274-284)."""
-    if pos < 0 or pos >= session.cache.position_count:
+    """Greedy base prediction at a position this session computed (engine.py:274-284):
+    StateError for positions it did not compute (pooled prefix, a stored full hit)."""
+    if not session.computed(pos):
         raise StateError(f"position {pos} was not computed by this session")
     tok = session.base_next.get(pos)
     if tok is None:
         # Not emitted during prefill: a read-only row at `pos` reproduces the encoder row's
-        # prediction bit for bit (row-independent kernels, same keys 0..pos).
+        # prediction bit for bit (row-independent kernels, same keys 0..pos). Emit flag 2:
+        # it does not replace the hidden state kept for last_logits.
         session._sync_block_table()
         fed = session.prompt + session.produced
-        out, _ = session.runtime.forward([fed[pos]], [1], [session.seq], [pos], [-1], [1])
+        out, _ = session.runtime.forward([fed[pos]], [1], [session.seq], [pos], [-1], [2])
         tok = int(out[0])
         session.base_next[pos] = tok
     session.ledger.param_matrix_reads += 1

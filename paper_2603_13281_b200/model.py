@@ -397,6 +397,10 @@ class KvCacheTensor:
         """All layers gained n positions on the device (GPU forward wrote them)."""
         self._lengths = [x + n for x in self._lengths]
 
+    def advance_layer(self, layer: int, n: int) -> None:
+        """One layer gained n positions (a single-layer block_forward wrote them)."""
+        self._lengths[layer] += n
+
     def release(self) -> None:
         for pid in self.pages:
             self.arena.decref(pid)
@@ -454,3 +458,9 @@ class KvCacheTensor:
             h.update(k)
             h.update(v)
         return h.hexdigest()
+
+
+# The reference's module-level projection / attention / block functions (src/model.py:334-538),
+# computed by the B200 kernels (layers.py).
+from .layers import (adapted_linear, base_linear, block_forward, causal_mask,  # noqa: E402,F401
+                     decoder_block_readonly, icarus_linear, layer_attention)

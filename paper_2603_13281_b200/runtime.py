@@ -480,7 +480,7 @@ class Runtime:
         n_seqs = int(max(rows[2].max(), 0)) + 1
         base, stride = _lib.addr(rows), rows.strides[0]
         b = _lib.BatchC(n, *[base + i * stride for i in range(6)], _lib.addr(self.block_table), n_seqs)
-        n_emit = int(rows[5].sum())
+        n_emit = int(np.count_nonzero(rows[5]))
         out = np.zeros(max(n_emit, 1), dtype=np.int32)
         lg = None
         if logits and n_emit:
@@ -492,6 +492,34 @@ class Runtime:
             lg = lg[:, :self.config.vocab_size]
         return out[:n_emit], lg
 
+    def seq_logits(self, slots) -> "torch.Tensor":
+        """fp32 logits [n, vocab] of the hidden states the last emitting forwards kept in the
+        per-(sequence, kind) store (icr_seq_logits; slot = 2 * seq + kind)."""
+        torch = _torch()
+        sl = np.ascontiguousarray(slots, dtype=np.int32)
+        lg = torch.empty(len(sl), self.dw.vocab_pad, dtype=torch.float32, device=self.device)
+        _lib.check(self._lib.icr_seq_logits(self._handle, _lib.i32_ptr(sl), len(sl), lg.data_ptr(),
+                                            _lib.stream_handle()))
+        return lg[:, :self.config.vocab_size]
+
+    def layer_forward(self, x, layer: int, kind, seq, pos, adapter):
+        """One layer of the fused forward (icr_layer_forward) over fp32 rows x [n, d] (device
+        tensor); returns the layer's output rows. Encoder rows write this layer's K/V."""
+        torch = _torch()
+        xin = x.to(self.device, torch.float32).contiguous()
+        n = xin.shape[0]
+        if xin.ndim != 2 or xin.shape[1] != self.config.hidden_dim:
+            from .errors import ShapeError
+            raise ShapeError(f"layer input must be [rows, {self.config.hidden_dim}], got {tuple(xin.shape)}")
+        rows = np.array((np.zeros(n), kind, seq, pos, adapter, np.zeros(n)), dtype=np.int32)
+        n_seqs = int(max(rows[2].max(), 0)) + 1
+        base, stride = _lib.addr(rows), rows.strides[0]
+        b = _lib.BatchC(n, *[base + i * stride for i in range(6)], _lib.addr(self.block_table), n_seqs)
+        out = torch.empty_like(xin)
+        _lib.check(self._lib.icr_layer_forward(self._handle, C.byref(b), int(layer), xin.data_ptr(),
+                                               out.data_ptr(), _lib.stream_handle()))
+        return out
+
     def decode_loop(self, tokens, kind, seq, pos, adapter, emit, feedback, steps: int):
         """Device-resident decode loop (icr_decode_loop): returns per-step device ms and
         the last step's emitted tokens."""
@@ -501,7 +529,7 @@ class Runtime:
         fb = np.ascontiguousarray(feedback, dtype=np.int32)
         b = _lib.BatchC(n, *[_lib.addr(a) for a in arrs], _lib.addr(self.block_table), n_seqs)
         ms = np.zeros(steps, dtype=np.float32)
-        last = np.zeros(max(int(arrs[5].sum()), 1), dtype=np.int32)
+        last = np.zeros(max(int(np.count_nonzero(arrs[5])), 1), dtype=np.int32)
         _lib.check(self._lib.icr_decode_loop(self._handle, C.byref(b), _lib.i32_ptr(fb), steps,
                                              _lib.i32_ptr(last),
                                              ms.ctypes.data_as(C.POINTER(C.c_float)),

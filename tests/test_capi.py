@@ -22,7 +22,7 @@ def test_library_exports_every_symbol():
     lib = _lib.load()
     for name in _lib.EXPORTED:
         assert hasattr(lib, name), name
-    assert lib.icr_abi_version() == 1
+    assert lib.icr_abi_version() == 2
 
 
 def test_status_codes_map_to_reference_exceptions():
