@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include "attn_merge.cuh"
 #include "kernels.h"
 #include "ptx.cuh"
 
@@ -352,16 +353,14 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
   }
 }
 
-// Fixed-order merge of chunk partials: one CTA per (row, KV group), one thread per
-// (head-in-group, 4 dims); the chunk weights exp(m_c - M), L and O are folded in chunk order.
-// Few threads and no shared memory: a merge CTA fits beside the next GEMM's CTA, which can
-// then start streaming its weights while the merge runs.
+// Fixed-order merge of chunk partials (attn_merge.cuh): one CTA per (row, KV group), one
+// thread per (head-in-group, 4 dims). Few threads and no shared memory: a merge CTA fits
+// beside the next GEMM's CTA, which can then start streaming its weights while the merge
+// runs. The tcgen05 path merges inside its partial kernel with the same fold.
 constexpr int MERGE_THREADS = 128;
 
-// MB chunks per batch: 12 (<= 96 registers, fits beside a GEMM CTA) when every row has at
-// most 12 chunks (decode steps), else 24 (long contexts: fewer round trips).
-template <int HD, int MB>
-__global__ void __launch_bounds__(MERGE_THREADS, MB <= 12 ? 5 : 1)
+template <int HD>
+__global__ void __launch_bounds__(MERGE_THREADS)
     attn_merge_kernel(const float* __restrict__ part_o, const float2* __restrict__ part_ml,
                       const int* __restrict__ row_pos, const int* __restrict__ row_kind,
                       int num_heads, int group, int max_chunks, int chunk_tokens,
@@ -370,71 +369,11 @@ __global__ void __launch_bounds__(MERGE_THREADS, MB <= 12 ? 5 : 1)
   const int cta_id = blockIdx.y * gridDim.x + blockIdx.x;
   if (trace != nullptr && threadIdx.x == 0 && cta_id < 4096) trace[(size_t)cta_id * 16 + 6] = globaltimer();
   pdl_launch();
-  // the row table is uploaded before the forward: read it while the partials run
-  const int r = blockIdx.x, g = blockIdx.y;
-  const int kind = row_kind[r], nch = row_pos[r] / chunk_tokens + 1;
   pdl_wait();
   if (trace != nullptr && threadIdx.x == 0 && cta_id < 4096) trace[(size_t)cta_id * 16 + 7] = globaltimer();
-  if (kind < 0) return;
-  // The (m, l) loads of one head are the same address across its threads (broadcast).
-  constexpr int V = HD / 4;
-  for (int idx = threadIdx.x; idx < group * V; idx += blockDim.x) {
-    const int hg = idx / V, d = (idx % V) * 4;
-    const int head = g * group + hg;
-    const size_t base = ((size_t)r * num_heads + head) * max_chunks;
-    float M = -INFINITY, L = 0.f;
-    float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
-    auto fold = [&](const float2& ml, const float4& po) {
-      const float w = exp2f(ml.x - M);  // partial maxima are in the log2 domain
-      L = fmaf(ml.y, w, L);
-      O.x = fmaf(po.x, w, O.x);
-      O.y = fmaf(po.y, w, O.y);
-      O.z = fmaf(po.z, w, O.z);
-      O.w = fmaf(po.w, w, O.w);
-    };
-    // batches of MB chunks, one round trip each; the running maximum rescales what was
-    // folded so far when a later batch raises it (rows with <= MB chunks: one batch)
-    for (int c0 = 0; c0 < nch; c0 += MB) {
-      float2 ml[MB];
-      float4 po[MB];
-#pragma unroll
-      for (int k = 0; k < MB; ++k) {
-        ml[k] = (c0 + k < nch) ? part_ml[base + c0 + k] : make_float2(-INFINITY, 0.f);
-        po[k] = (c0 + k < nch) ? *reinterpret_cast<const float4*>(part_o + (base + c0 + k) * HD + d)
-                               : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-      float Mn = M;
-#pragma unroll
-      for (int k = 0; k < MB; ++k) Mn = fmaxf(Mn, ml[k].x);
-      if (c0 > 0 && Mn != M) {
-        const float sc = exp2f(M - Mn);
-        L *= sc;
-        O.x *= sc;
-        O.y *= sc;
-        O.z *= sc;
-        O.w *= sc;
-      }
-      M = Mn;
-#pragma unroll
-      for (int k = 0; k < MB; ++k)
-        if (c0 + k < nch) fold(ml[k], po[k]);
-    }
-    __nv_bfloat162 lo = __floats2bfloat162_rn(__fdiv_rn(O.x, L), __fdiv_rn(O.y, L));
-    __nv_bfloat162 hi = __floats2bfloat162_rn(__fdiv_rn(O.z, L), __fdiv_rn(O.w, L));
-    uint2 pk;
-    pk.x = *reinterpret_cast<uint32_t*>(&lo);
-    pk.y = *reinterpret_cast<uint32_t*>(&hi);
-    *reinterpret_cast<uint2*>(out + (size_t)r * out_ld + head * HD + d) = pk;
-  }
+  merge_unit<HD>(part_o, part_ml, row_pos, row_kind, blockIdx.x, blockIdx.y, num_heads, group,
+                 max_chunks, chunk_tokens, out, out_ld, threadIdx.x, blockDim.x);
   if (trace != nullptr && threadIdx.x == 0 && cta_id < 4096) trace[(size_t)cta_id * 16 + 5] = globaltimer();
-}
-
-// MB = 12 (<= 96 registers: a merge CTA shares an SM with the next kernel's CTA) when every
-// row has at most 12 chunks -- decode steps at moderate context; 24 (one round trip fewer)
-// for long contexts
-template <int HD>
-static auto merge_kernel(int max_chunks) {
-  return max_chunks > 12 ? attn_merge_kernel<HD, 24> : attn_merge_kernel<HD, 12>;
 }
 
 static bool use_tc(int head_dim) {
@@ -446,16 +385,7 @@ int attn_entries_per_item(int head_dim) { return use_tc(head_dim) ? 128 : 64; }
 
 template <int HD>
 static cudaError_t attn_launch_hd(const AttnLaunch& a, cudaStream_t s) {
-  if (use_tc(HD)) {
-    cudaError_t e = attn_tc_partial_launch(a, a.chunk_tokens / 16, s);
-    if (e != cudaSuccess) return e;
-    const int mthreads = std::min(MERGE_THREADS, ((a.group * HD / 4 + 31) / 32) * 32);
-    return launch_pdl(merge_kernel<HD>(a.max_chunks),
-                      dim3(a.n_rows, a.num_kv_heads), dim3(mthreads), 0, s,
-                      a.part_o, a.part_ml, a.row_pos, a.row_kind, a.num_heads, a.group,
-                      a.max_chunks, a.chunk_tokens, a.out, a.out_ld,
-                      a.trace ? a.trace + 4096 * 16 : nullptr);
-  }
+  if (use_tc(HD)) return attn_tc_partial_launch(a, a.chunk_tokens / 16, s);  // merge fused
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(attn_partial_kernel<HD>,
@@ -471,7 +401,7 @@ static cudaError_t attn_launch_hd(const AttnLaunch& a, cudaStream_t s) {
                              a.scale, a.part_o, a.part_ml, a.n_items_dev, a.pf_base, a.pf_bytes, a.trace);
   if (e != cudaSuccess) return e;
   const int mthreads = std::min(MERGE_THREADS, ((a.group * HD / 4 + 31) / 32) * 32);
-  return launch_pdl(merge_kernel<HD>(a.max_chunks),
+  return launch_pdl(attn_merge_kernel<HD>,
                     dim3(a.n_rows, a.num_kv_heads), dim3(mthreads), 0, s,
                     a.part_o, a.part_ml, a.row_pos, a.row_kind, a.num_heads, a.group,
                     a.max_chunks, a.chunk_tokens, a.out, a.out_ld,

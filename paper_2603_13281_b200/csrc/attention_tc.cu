@@ -3,21 +3,28 @@
 // heads of `block_forward` decode (src/model.py:495-501): scores = (q . k) * 1/sqrt(hd) with
 // the causal mask, softmax, weights @ V -- per (row, head), batch-invariant.
 //
-// One CTA = one work item x one KV head. A work item is a chunk of pages at fixed absolute
-// positions shared by every sequence whose block table maps the same physical pages; its up to
-// 128 query entries (row, head-in-group) -- the encoder and decoder heads of every model
-// sharing the prefix -- are the M = 128 rows of the tcgen05 MMAs. The chunk is streamed in
-// sub-chunks of SUBP = 8 pages (128 keys) through a 2-stage TMA ring:
+// Persistent: one CTA per SM walks a host-scheduled (LPT) list of units = work item x KV
+// head. A work item is a chunk of pages at fixed absolute positions shared by every sequence
+// whose block table maps the same physical pages; its up to 128 query entries (row,
+// head-in-group) -- the encoder and decoder heads of every model sharing the prefix -- are the
+// M = 128 rows of the tcgen05 MMAs. The chunk is streamed in sub-chunks of SUBP = 8 pages
+// (128 keys) through a 2-stage TMA ring:
 //   S_j[128 x 128] = Q . K_j^T            (K-major Q and K; fp32, double-buffered in TMEM)
 //   softmax        : 8 warps, two per TMEM lane quarter (each half of the key columns), exp2
 //                    domain with the causal mask; running max m, sum l per entry; P_j bf16 into
 //                    the SW128 K-major layout; O rescaled in TMEM when the max moves
 //   O[128 x 128]  += P_j . V_j              (V consumed MN-major straight from the pages)
-// so S_{j+1}, the loads of sub-chunk j+2 and the softmax of j overlap. The unnormalised
-// partial (O, m, l) per (row, head, chunk) goes to the fixed-order merge kernel. Each K/V page
-// is staged in shared memory once per KV head for all entries: HBM bytes scale with context,
-// not with the number of models. Sub-chunk boundaries sit at fixed offsets from the chunk's
-// absolute start, so a row's partial never depends on which other rows share the item.
+// so S_{j+1}, the loads of sub-chunk j+2 and the softmax of j overlap -- within a unit and
+// across consecutive units of a CTA. The unnormalised partial (O, m, l) per (row, head, chunk)
+// is written out; after a grid barrier (all CTAs are resident) the CTAs fold the partials of
+// every (row, KV group) in chunk order (attn_merge.cuh) -- no second launch. Each K/V page is
+// staged in shared memory once per KV head for all entries: HBM bytes scale with context, not
+// with the number of models. Sub-chunk boundaries sit at fixed offsets from the chunk's
+// absolute start, so a row's partial never depends on which other rows share the item or on
+// which CTA runs it.
+#include <cstdlib>
+
+#include "attn_merge.cuh"
 #include "kernels.h"
 #include "ptx.cuh"
 
@@ -36,8 +43,9 @@ struct TcLayout {
   static constexpr uint32_t STAGE_BYTES = 4 * HALF;        // 64 KB
   static constexpr uint32_t BAR_OFF = STAGE0 + 2 * STAGE_BYTES;
   static constexpr uint32_t RED_OFF = BAR_OFF + 256;       // float [2 halves][128]
-  // 230,656 B: within the opt-in maximum of 232,448 less the 1 KB the driver reserves
-  static constexpr size_t SMEM = RED_OFF + 256 * 4;
+  static constexpr uint32_t FLAG_OFF = RED_OFF + 256 * 4;  // int [16] merge bookkeeping
+  // 230,720 B: within the opt-in maximum of 232,448 less the 1 KB the driver reserves
+  static constexpr size_t SMEM = FLAG_OFF + 16 * 4;
   static constexpr uint32_t TMEM_COLS = 512;               // S0 [0,128) S1 [128,256) O [256,384)
 };
 
@@ -69,55 +77,72 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
       : "memory");
 }
 
-static_assert(128 * 132 * 4 <= 2 * TcLayout::STAGE_BYTES, "O staging must fit in the K/V stages");
 static_assert(TcLayout::SMEM <= 232448 - 1024, "exceeds the per-block shared memory limit");
 
+__device__ __forceinline__ void cp_async16_s(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+}
+
+// Persistent: CTA c runs the (item, KV head) units sched_units[sched_off[c] .. sched_off[c+1])
+// (a host LPT schedule over min(#SMs, units) CTAs, one per SM). Every role walks the same unit
+// list, so each knows the item sequence without communication; mbarrier phases follow a
+// global sub-chunk counter J (stages, S buffers, P buffers) or the CTA's item count (Q, O).
+// Across units the K/V producers run ahead into the next unit's pages, the Q warp stages the
+// next unit's queries as soon as the last S MMA of the current one has read Q, and the next
+// unit's first S MMA overlaps the current unit's softmax tail and epilogue.
 __global__ void __launch_bounds__(TC_THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                    const __nv_bfloat16* __restrict__ q, int q_ld, int num_kv_heads, int group,
                    const AttnItem* __restrict__ items, const int* __restrict__ item_pages,
                    const int2* __restrict__ item_rows, const int* __restrict__ row_pos,
                    int num_heads, int max_chunks, float scale, float* __restrict__ part_o,
-                   float2* __restrict__ part_ml, const int* __restrict__ n_items_dev,
-                   unsigned long long* __restrict__ trace) {
+                   float2* __restrict__ part_ml, const int* __restrict__ sched_off,
+                   const int* __restrict__ sched_units, unsigned long long* __restrict__ trace,
+                   const int* __restrict__ row_kind, int n_rows, int chunk_tokens,
+                   __nv_bfloat16* __restrict__ out, int out_ld, int* __restrict__ coop, int diag) {
   using L = TcLayout;
   extern __shared__ __align__(1024) uint8_t tc_smem[];
   uint8_t* smem = tc_smem;  // no static shared memory: the dynamic window starts 1024-aligned
   uint8_t* sQ = smem + L::Q_OFF;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
-  uint64_t* q_full = bars + 0;
+  uint64_t* q_full = bars + 0;    // Q of the CTA's n-th unit staged (phase n)
   uint64_t* kv_full = bars + 1;   // [2] K landed
   uint64_t* kv_empty = bars + 3;  // [2] K consumed by S
-  uint64_t* v_full = bars + 12;   // [2] V landed
-  uint64_t* v_empty = bars + 14;  // [2] V consumed by P.V
   uint64_t* s_full = bars + 5;    // [2]
-  // P(j) written (+ O rescaled): one barrier per P buffer, so the MMA warp's parity wait can
-  // never alias -- softmax(j + 2) needs P.V(j), i.e. the MMA warp past its wait for P(j)
-  uint64_t* p_full_b[2] = {bars + 7, bars + 17};
+  uint64_t* p_full_b[2] = {bars + 7, bars + 17};  // P(J) written (+ O rescaled), per buffer
   uint64_t* o_done = bars + 8;    // one phase per P.V (the lazy rescale waits on it)
-  uint64_t* o_final = bars + 16;  // the last P.V only: the epilogue's single-phase wait
   uint64_t* p_free = bars + 9;    // [2]: P buffer b consumed by its P.V
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
+  uint64_t* v_full = bars + 12;   // [2] V landed
+  uint64_t* v_empty = bars + 14;  // [2] V consumed by P.V
+  uint64_t* o_final = bars + 16;  // the unit's last P.V landed (phase n)
+  uint64_t* q_free = bars + 18;   // the unit's last S MMA has read Q (phase n)
   float* red = reinterpret_cast<float*>(smem + L::RED_OFF);
+  int* flag_s = reinterpret_cast<int*>(smem + L::FLAG_OFF);  // [0] generation
 
-  const int cta_id = blockIdx.y * gridDim.x + blockIdx.x;
+  const int cta = blockIdx.x;
   auto stamp = [&](int k) {
-    if (trace != nullptr && cta_id < 4096) trace[(size_t)cta_id * 16 + k] = globaltimer();
+    if (trace != nullptr && cta < 4096) trace[(size_t)cta * 16 + k] = globaltimer();
   };
-  // per-sub-chunk timeline of CTA 0 (diagnostic): [j][0 K issued, 1 S done, 2 P written, 3 PV issued]
+  // per-sub-chunk timeline of CTA 0 (diagnostic): [J][0 K issued, 1 S done, 2 P written, 3 PV issued]
   auto sstamp = [&](int j, int k) {
-    if (trace != nullptr && cta_id == 0 && j < 256) trace[(size_t)2 * 4096 * 16 + j * 8 + k] = globaltimer();
+    if (trace != nullptr && cta == 0 && j < 256) trace[(size_t)2 * 4096 * 16 + j * 8 + k] = globaltimer();
   };
   if (threadIdx.x == 0) stamp(6);
   if ((smem_u32(tc_smem) & 1023) != 0) __trap();  // SW128 tiles need a 1024-byte base
   pdl_launch();
-  // grid (KV head, item): consecutive CTAs are the KV heads of one item, so with items in
-  // longest-first order every head of the long items is dispatched in the first wave
-  const int item_id = blockIdx.y;
-  if (item_id >= *n_items_dev) return;
   const int warp = warp_id(), lane = lane_id();
+  const int cp = chunk_tokens >> 4;
+  // CTA c's first unit is unit c (schedule_units assigns the G longest units to CTAs 0..G-1):
+  // its item, page ids and (Q warp) row table are requested right away, together with the
+  // schedule, all uploaded before the forward -- one round trip, overlapping the set-up
+  const int k_begin = sched_off[cta], k_end = sched_off[cta + 1];
+  const AttnItem it0 = items[cta / num_kv_heads];
+  int pid0 = 0;
+  if ((warp == 0 || warp == 2) && lane < cp) pid0 = __ldg(item_pages + (cta / num_kv_heads) * cp + lane);
+
   if (threadIdx.x == 0) {
-    mbar_init(q_full, 288);
+    mbar_init(q_full, 32);
     for (int b = 0; b < 2; ++b) {
       mbar_init(&kv_full[b], 1);
       mbar_init(&kv_empty[b], 1);
@@ -129,174 +154,209 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     mbar_init(p_full_b[1], 256);
     mbar_init(o_done, 1);
     mbar_init(o_final, 1);
+    mbar_init(q_free, 1);
     mbar_init(&p_free[0], 1);
     mbar_init(&p_free[1], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<L::TMEM_COLS>(tmem_slot);
+  // P starts zero (padding entries' rows are never written; they only feed padding O rows)
+  if (warp >= 4)
+    for (int i = threadIdx.x - 128; i < 2 * (int)L::P_BYTES / 16; i += 256)
+      *reinterpret_cast<uint4*>(smem + L::P_OFF + i * 16) = make_uint4(0, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const uint32_t tmem_o = tmem_base + 256;
-  const AttnItem it = items[item_id];  // uploaded before the forward
-  const int g = blockIdx.x;
-  const int np = it.n_pages;
-  const int nsub = (np + SUBP - 1) / SUBP;
 
   if (warp == 0 || warp == 2) {
     // ---------------- producers: K (warp 0) and V (warp 2) rings, decoupled: a K stage is
-    // free once S has read it, a V stage only after P.V -- K runs ahead of the softmax ------
+    // free once S has read it, a V stage only after P.V -- K runs ahead of the softmax. The
+    // whole warp walks the pages: lane i holds the page id of position i of the current
+    // 32-page window; lane 0 issues the TMAs ------------------------------------------------
     const bool is_k = warp == 0;
-    if (elect_one()) {
-      const CUtensorMap* tm = is_k ? &tm_k : &tm_v;
-      uint64_t* full = is_k ? kv_full : v_full;
-      uint64_t* empty = is_k ? kv_empty : v_empty;
-      tma_prefetch_desc(tm);
-      const int pre = it.n_pre;  // pages no kernel of this forward writes
-      bool waited = false;
-      for (int j = 0; j < nsub; ++j) {
-        const int b = j & 1;
-        if (j >= 2) mbar_wait(&empty[b], ((j >> 1) - 1) & 1);
+    const CUtensorMap* tm = is_k ? &tm_k : &tm_v;
+    uint64_t* full = is_k ? kv_full : v_full;
+    uint64_t* empty = is_k ? kv_empty : v_empty;
+    if (lane == 0) tma_prefetch_desc(tm);
+    bool waited = false;
+    int J = 0;
+    AttnItem it = it0;
+    int pid_cur = pid0;
+    for (int k = k_begin; k < k_end; ++k) {
+      const int unit = k == k_begin ? cta : sched_units[k];
+      const int item = unit / num_kv_heads, g = unit % num_kv_heads;
+      const int np = it.n_pages, nsub = (np + SUBP - 1) / SUBP;
+      AttnItem it_n = it;
+      int pid_n0 = 0, pid_nxt = 0;
+      for (int j = 0; j < nsub; ++j, ++J) {
+        const int b = J & 1;
+        if (J >= 2) mbar_wait(&empty[b], ((J >> 1) - 1) & 1);
         const int p0 = j * SUBP, pn = min(SUBP, np - p0);
+        if (p0 > 0 && (p0 & 31) == 0) {
+          pid_cur = pid_nxt;
+          pid_nxt = (p0 + 32 + lane < np) ? __ldg(item_pages + item * cp + p0 + 32 + lane) : 0;
+        }
         uint8_t* st = smem + L::STAGE0 + b * L::STAGE_BYTES + (is_k ? 0 : 2 * L::HALF);
-        mbar_expect_tx(&full[b], (uint32_t)pn * 2 * 2048);
+        if (lane == 0) mbar_expect_tx(&full[b], (uint32_t)pn * 2 * 2048);
         for (int pi = 0; pi < pn; ++pi) {
-          if (!waited && p0 + pi >= pre) {
+          if (!waited && p0 + pi >= it.n_pre) {
             pdl_wait();
-            if (is_k) stamp(7);
+            if (is_k && lane == 0) stamp(7);
             waited = true;
           }
-          const int plane = item_pages[it.page_off + p0 + pi] * num_kv_heads + g;
+          const int plane = __shfl_sync(0xffffffffu, pid_cur, (p0 + pi) & 31) * num_kv_heads + g;
+          if (lane == 0) {
 #pragma unroll
-          for (int h = 0; h < 2; ++h) tma_load_3d(st + h * L::HALF + pi * 2048, tm, &full[b], h * 64, 0, plane);
+            for (int h = 0; h < 2; ++h) tma_load_3d(st + h * L::HALF + pi * 2048, tm, &full[b], h * 64, 0, plane);
+          }
         }
-        if (is_k) sstamp(j, 0);
+        if (is_k && lane == 0) sstamp(J, 0);
+        if (j == 0) {
+          pid_nxt = (32 + lane < np) ? __ldg(item_pages + item * cp + 32 + lane) : 0;
+          if (k + 1 < k_end) {
+            const int nitem = sched_units[k + 1] / num_kv_heads;
+            it_n = items[nitem];
+            pid_n0 = lane < cp ? __ldg(item_pages + nitem * cp + lane) : 0;
+          }
+        }
       }
-      if (!waited) pdl_wait();
+      it = it_n;
+      pid_cur = pid_n0;
     }
+    if (!waited) pdl_wait();
     __syncwarp();
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
-    mbar_wait(q_full, 0);
-    tc_fence_after();
-    auto issue_s = [&](int j) {
-      const int b = j & 1;
-      mbar_wait(&kv_full[b], (j >> 1) & 1);
-      tc_fence_after();
-      if (elect_one()) {
-        const int keys = min(SUBP, np - j * SUBP) * 16;
-        const uint32_t idesc_s = idesc_bf16_f32(TC_ROWS, (uint32_t)keys);
-        const uint32_t kb = smem_u32(smem + L::STAGE0 + b * L::STAGE_BYTES);
+    int J = 0, n = 0;
+    for (int k = k_begin; k < k_end; ++k, ++n) {
+      const int np = k == k_begin ? it0.n_pages : items[sched_units[k] / num_kv_heads].n_pages;
+      const int nsub = (np + SUBP - 1) / SUBP;
+      auto issue_s = [&](int Jx, int jx) {
+        const int b = Jx & 1;
+        mbar_wait(&kv_full[b], (Jx >> 1) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const int keys = min(SUBP, np - jx * SUBP) * 16;
+          const uint32_t idesc_s = idesc_bf16_f32(TC_ROWS, (uint32_t)keys);
+          const uint32_t kb = smem_u32(smem + L::STAGE0 + b * L::STAGE_BYTES);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t a = smem_u32(sQ) + (kk >> 2) * (TC_ROWS * 128) + (kk & 3) * 32;
-          const uint32_t bb = kb + (kk >> 2) * L::HALF + (kk & 3) * 32;
-          tc_mma_bf16(tmem_base + b * 128, sdesc_kmajor_sw128(a), sdesc_kmajor_sw128(bb), idesc_s,
-                      kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t a = smem_u32(sQ) + (kk >> 2) * (TC_ROWS * 128) + (kk & 3) * 32;
+            const uint32_t bb = kb + (kk >> 2) * L::HALF + (kk & 3) * 32;
+            tc_mma_bf16(tmem_base + b * 128, sdesc_kmajor_sw128(a), sdesc_kmajor_sw128(bb), idesc_s,
+                        kk > 0 ? 1u : 0u);
+          }
+          tc_commit(&s_full[b]);
+          tc_commit(&kv_empty[b]);
+          if (jx == nsub - 1) tc_commit(q_free);  // Q may be restaged for the next unit
         }
-        tc_commit(&s_full[b]);
-        tc_commit(&kv_empty[b]);
-      }
-      __syncwarp();
-    };
-    issue_s(0);
-    for (int j = 0; j < nsub; ++j) {
-      if (j + 1 < nsub) issue_s(j + 1);
-      mbar_wait(p_full_b[j & 1], (j >> 1) & 1);  // softmax j wrote P and rescaled O
-      mbar_wait(&v_full[j & 1], (j >> 1) & 1);
+        __syncwarp();
+      };
+      mbar_wait(q_full, n & 1);
       tc_fence_after();
-      if (elect_one()) {
-        const int pn = min(SUBP, np - j * SUBP);
-        const uint32_t idesc_o = idesc_bf16_f32(TC_ROWS, 128) | (1u << 16);  // B (V) MN-major
-        const uint32_t vb = smem_u32(smem + L::STAGE0 + (j & 1) * L::STAGE_BYTES) + 2 * L::HALF;
-        const uint32_t pb = smem_u32(smem + L::P_OFF + (j & 1) * L::P_BYTES);
-        for (int kk = 0; kk < pn; ++kk) {  // 16 keys (one page) per instruction
-          const uint32_t a = pb + (kk >> 2) * (TC_ROWS * 128) + (kk & 3) * 32;
-          tc_mma_bf16(tmem_o, sdesc_kmajor_sw128(a), sdesc_mnmajor_sw128(vb + kk * 2048, L::HALF, 1024),
-                      idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+      issue_s(J, 0);
+      for (int j = 0; j < nsub; ++j, ++J) {
+        if (j + 1 < nsub) issue_s(J + 1, j + 1);
+        mbar_wait(p_full_b[J & 1], (J >> 1) & 1);  // softmax J wrote P and rescaled O
+        mbar_wait(&v_full[J & 1], (J >> 1) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const int pn = min(SUBP, np - j * SUBP);
+          const uint32_t idesc_o = idesc_bf16_f32(TC_ROWS, 128) | (1u << 16);  // B (V) MN-major
+          const uint32_t vb = smem_u32(smem + L::STAGE0 + (J & 1) * L::STAGE_BYTES) + 2 * L::HALF;
+          const uint32_t pb = smem_u32(smem + L::P_OFF + (J & 1) * L::P_BYTES);
+          for (int kk = 0; kk < pn; ++kk) {  // 16 keys (one page) per instruction
+            const uint32_t a = pb + (kk >> 2) * (TC_ROWS * 128) + (kk & 3) * 32;
+            tc_mma_bf16(tmem_o, sdesc_kmajor_sw128(a), sdesc_mnmajor_sw128(vb + kk * 2048, L::HALF, 1024),
+                        idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+          }
+          sstamp(J, 3);
+          tc_commit(o_done);
+          if (j == nsub - 1) tc_commit(o_final);
+          tc_commit(&p_free[J & 1]);
+          tc_commit(&v_empty[J & 1]);
         }
-        sstamp(j, 3);
-        tc_commit(o_done);
-        if (j == nsub - 1) tc_commit(o_final);
-        tc_commit(&p_free[j & 1]);
-        tc_commit(&v_empty[j & 1]);
+        __syncwarp();
       }
-      __syncwarp();
+    }
+  } else if (warp == 3) {
+    // ---------------- Q staging: one warp, cp.async straight into the swizzled tile ----------
+    int n = 0;
+    for (int k = k_begin; k < k_end; ++k, ++n) {
+      const int unit = k == k_begin ? cta : sched_units[k];
+      const AttnItem it = k == k_begin ? it0 : items[unit / num_kv_heads];
+      const int g = unit % num_kv_heads;
+      // the row table (uploaded before the forward) before the wait: one round trip
+      int2 rws[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+        rws[m] = (lane + 32 * m < it.n_rows) ? item_rows[it.row_off + lane + 32 * m] : make_int2(0, 0);
+      if (n == 0) {
+        pdl_wait();  // q comes from the q/k/v GEMM
+        if (lane == 0) {
+          stamp(3);
+          flag_s[0] = ld_acquire(coop);  // generation of the merge counters (after the wait)
+        }
+      } else {
+        mbar_wait(q_free, (n - 1) & 1);  // the previous unit's S MMAs have read Q
+      }
+      // entry e sits in M row / TMEM lane r(e) = (e % 4) * 32 + e / 4: the entries of a partly
+      // filled item spread over all four lane quarters. Lane l stages entries l + 32 m (all 16
+      // chunks each); the row table is read before the copies are issued (one round trip)
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int e = lane + 32 * m;
+        if (e < it.n_rows) {
+          const int r = (e & 3) * 32 + (e >> 2);
+          const __nv_bfloat16* src = q + (size_t)rws[m].x * q_ld + (g * group + rws[m].y) * 128;
+#pragma unroll
+          for (int c = 0; c < 16; ++c)
+            cp_async16_s(smem_u32(sQ + (c >> 3) * (TC_ROWS * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4)),
+                         src + c * 8);
+        }
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      mbar_arrive(q_full);
     }
   } else {
-    // ---------------- Q gather (warps 3-11) ----------------
-    const int t = threadIdx.x - 96;  // 0..287
-    // entry e sits in M row / TMEM lane r(e) = (e % 4) * 32 + e / 4: the entries of a partly
-    // filled item spread over all four lane quarters
-    // all of a thread's loads are issued before its first store: one round trip, not eight
-    constexpr int QPT = (TC_ROWS * 16 + 287) / 288;  // 16-byte chunks per thread
-    int qoff[QPT];  // the item's row table is uploaded before the forward: read it before the wait
-#pragma unroll
-    for (int k = 0; k < QPT; ++k) {
-      const int idx = t + k * 288;
-      const int e = idx >> 4, c = idx & 15;
-      qoff[k] = -1;
-      if (idx < TC_ROWS * 16 && e < it.n_rows) {
-        const int2 rr = item_rows[it.row_off + e];
-        qoff[k] = rr.x * q_ld + (g * group + rr.y) * 128 + c * 8;
-      }
-    }
-    // P rows of padding entries stay zero for the whole item (the softmax skips them); this
-    // does not depend on the previous kernel, so it runs before the wait
-    for (int idx = t; idx < TC_ROWS * 2 * 2 * 8; idx += 288) {
-      const int r = idx & 127, chunk = idx >> 7;  // chunk: buffer (2) x K-block (2) x 16 B (8)
-      const int e = (r & 31) * 4 + (r >> 5);
-      if (e >= it.n_rows)
-        *reinterpret_cast<uint4*>(smem + L::P_OFF + (chunk >> 3) * (TC_ROWS * 128) + r * 128 + (chunk & 7) * 16) =
-            make_uint4(0, 0, 0, 0);
-    }
-    pdl_wait();  // q comes from the q/k/v GEMM
-    if (threadIdx.x == 96) stamp(3);
-    uint4 qv[QPT];
-#pragma unroll
-    for (int k = 0; k < QPT; ++k)
-      qv[k] = qoff[k] >= 0 ? __ldg(reinterpret_cast<const uint4*>(q + qoff[k])) : make_uint4(0, 0, 0, 0);
-#pragma unroll
-    for (int k = 0; k < QPT; ++k) {
-      const int idx = t + k * 288;
-      if (idx < TC_ROWS * 16) {
-        const int e = idx >> 4, c = idx & 15;
-        const int r = (e & 3) * 32 + (e >> 2);
-        *reinterpret_cast<uint4*>(sQ + (c >> 3) * (TC_ROWS * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4)) = qv[k];
-      }
-    }
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-    mbar_arrive(q_full);
-    if (lane == 0 && warp == 3) stamp(1);
-
-    if (warp >= 4) {
-      // ---------------- softmax: warps w and w + 4 (same SM sub-partition, same TMEM lane
-      // quarter w % 4) split each row's 128 key columns; the row max and sum are exchanged
-      // through shared memory under a 64-thread barrier per quarter ------------------------
-      const int sw = warp - 4;                       // 0..7
-      const int quarter = sw & 3, half = sw >> 2;    // key columns [64 half, 64 half + 64)
-      const int r = quarter * 32 + lane;             // TMEM lane = M row
-      const int e = (r & 31) * 4 + (r >> 5);         // the query entry held in that row
-      const uint32_t lane_base = (uint32_t)(32 * quarter) << 16;
+    // ---------------- softmax: warps w and w + 4 (same SM sub-partition, same TMEM lane
+    // quarter w % 4) split each row's 128 key columns; the row max and sum are exchanged
+    // through shared memory under a 64-thread barrier per quarter ------------------------
+    const int sw = warp - 4;                       // 0..7
+    const int quarter = sw & 3, half = sw >> 2;    // key columns [64 half, 64 half + 64)
+    const int r = quarter * 32 + lane;             // TMEM lane = M row
+    const int e = (r & 31) * 4 + (r >> 5);         // the query entry held in that row
+    const uint32_t lane_base = (uint32_t)(32 * quarter) << 16;
+    const float sl2 = scale * 1.4426950408889634f;
+    int J = 0, n = 0;
+    for (int k = k_begin; k < k_end; ++k, ++n) {
+      const int unit = k == k_begin ? cta : sched_units[k];
+      const AttnItem it = k == k_begin ? it0 : items[unit / num_kv_heads];
+      const int g = unit % num_kv_heads;
+      const int np = it.n_pages, nsub = (np + SUBP - 1) / SUBP;
       const bool valid = e < it.n_rows;
-      int2 rr = make_int2(0, 0);
       int pos = -1;
+      size_t slot = 0;
       if (valid) {
-        rr = item_rows[it.row_off + e];
+        const int2 rr = item_rows[it.row_off + e];
         pos = row_pos[rr.x];
+        slot = ((size_t)rr.x * num_heads + g * group + rr.y) * max_chunks + it.chunk_idx;
       }
-      const float sl2 = scale * 1.4426950408889634f;
       float m_run = -INFINITY, l_part = 0.f;
-      for (int j = 0; j < nsub; ++j) {
-        const int b = j & 1;
+      for (int j = 0; j < nsub; ++j, ++J) {
+        const int b = J & 1;
         const int keys = min(SUBP, np - j * SUBP) * 16;
         const int kbase = it.chunk_start + j * SUBP * 16 + half * 64;
         const int hkeys = min(64, keys - half * 64);  // this half's columns (may be <= 0)
-        mbar_wait(&s_full[b], (j >> 1) & 1);
+        mbar_wait(&s_full[b], (J >> 1) & 1);
         tc_fence_after();
-        if (r == 0 && half == 0) sstamp(j, 1);
-        if (r == 0 && half == 0 && j == 0) stamp(2);
+        if (r == 0 && half == 0) sstamp(J, 1);
+        if (r == 0 && half == 0 && J == 0) stamp(2);
         uint32_t v[4][16];  // raw q.k of this half's (<= 64) keys
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4)
@@ -304,14 +364,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         tmem_wait_ld();
 #pragma unroll
         for (int q4 = 0; q4 < 4; ++q4) tmem_reg_fence(v[q4]);
-        if (r == 0 && half == 0) sstamp(j, 4);
         // visible keys of this half: [kbase, kbase + nvis); max of raw scores x sl2 (> 0)
         // equals the max of the scaled scores (rounding is monotonic)
         const int nvis = valid ? max(0, min(hkeys, pos + 1 - kbase)) : 0;
         if (nvis > 0 && nvis < 64) {
           // rare (the row's causal edge or a short last sub-chunk): invisible keys become
-          // -inf once, so the max and exp loops below carry no per-key predicates (the
-          // volatile asm keeps this a branch instead of 64 if-converted selects)
+          // -inf once, so the max and exp loops below carry no per-key predicates
           asm volatile("" ::: "memory");
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4)
@@ -336,11 +394,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         // is exact enough in bf16 / fp32), so O is rescaled only when the max jumps
         const float m_new = (m_cand > m_run + 8.f) ? m_cand : m_run;
         const float corr = (m_run == -INFINITY) ? 1.f : ex2_approx(m_run - m_new);
-        if (r == 0 && half == 0) sstamp(j, 5);
-        // P buffer b was last read by P.V(j - 2)
-        if (j >= 2) mbar_wait(&p_free[b], ((j >> 1) - 1) & 1);
-        if (r == 0 && half == 0) sstamp(j, 6);
-        const long long clk0 = clock64();
+        // P buffer b was last read by P.V(J - 2)
+        if (J >= 2) mbar_wait(&p_free[b], ((J >> 1) - 1) & 1);
         uint8_t* rowp0 = smem + L::P_OFF + b * L::P_BYTES + half * (TC_ROWS * 128) + r * 128;
         float ls[4] = {0.f, 0.f, 0.f, 0.f};  // four short row-sum chains instead of two long ones
         if (nvis > 0) {  // padding rows, rows past their position: P stays zero
@@ -351,10 +406,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               uint32_t pk[8];
 #pragma unroll
               for (int jj = 0; jj < 16; jj += 2) {
-                const int c = q4 * 16 + jj;
-                // every exponential on the SFU: measured faster than moving a quarter or a
-                // half of them to an FMA-pipe polynomial (the FMA/ALU issue slots are the
-                // scarcer resource in this loop: 1430 vs 1520 / 1800 cycles per sub-chunk)
+                // every exponential on the SFU (measured faster than an FMA-pipe share);
                 // masked keys hold -inf: exp2(-inf) = +0
                 const float p0 = ex2_approx(fmaf(__uint_as_float(v[q4][jj]), sl2, nm));
                 const float p1 = ex2_approx(fmaf(__uint_as_float(v[q4][jj + 1]), sl2, nm));
@@ -375,11 +427,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         l_part = l_part * corr + ((ls[0] + ls[1]) + (ls[2] + ls[3]));
         m_run = m_new;
-        if (trace != nullptr && cta_id == 0 && r == 0 && half == 0 && j < 256)
-          trace[(size_t)2 * 4096 * 16 + j * 8 + 7] = (unsigned long long)(clock64() - clk0);
         if (j > 0 && __any_sync(0xffffffffu, valid && corr != 1.f)) {
-          // the max moved: rescale this half's 64 O columns once P.V(j - 1) has landed
-          mbar_wait(o_done, (j - 1) & 1);
+          // the max moved: rescale this half's 64 O columns once P.V(J - 1) has landed
+          mbar_wait(o_done, (J - 1) & 1);
           tc_fence_after();
           uint32_t o[4][16];
 #pragma unroll
@@ -397,53 +447,75 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         tc_fence_before();
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         mbar_arrive(p_full_b[b]);
-        if (r == 0 && half == 0) sstamp(j, 2);
+        if (r == 0 && half == 0) sstamp(J, 2);
       }
       if (r == 0 && half == 0) stamp(4);
-      // ---------------- epilogue: unnormalised partial O and (m, l) ----------------
-      float* rl = red;  // free: both partners passed the last iteration's second barrier
-      rl[half * 128 + r] = l_part;
-      // not o_done: the last softmax iteration only knows P.V(nsub - 3) finished, so o_done
-      // may still be two phases behind and a parity wait would alias an older phase
-      mbar_wait(o_final, 0);
+      // ---------------- epilogue: unnormalised partial O and (m, l), straight from TMEM
+      // (each thread 256 contiguous bytes of its entry's row) ----------------
+      red[half * 128 + r] = l_part;
+      mbar_wait(o_final, n & 1);  // the unit's last P.V landed (single phase per unit)
       tc_fence_after();
-      if (r == 0 && half == 0) stamp(0);
       named_bar_sync(1 + quarter, 64);
-      const float l = rl[r] + rl[128 + r];
-      const size_t slot = valid ? ((size_t)rr.x * num_heads + g * group + rr.y) * max_chunks + it.chunk_idx : 0;
-      // O leaves through shared memory (the K/V stages are idle once the last P.V landed):
-      // rows padded to 528 B so a quarter-warp's 16-byte stores hit distinct banks, then each
-      // warp writes one entry's 512 contiguous bytes per instruction
-      float* stg = reinterpret_cast<float*>(smem + L::STAGE0);
-      constexpr int STG_LD = 132;  // floats per staged row: 128 + 4 padding
+      const float l = red[r] + red[128 + r];
+      named_bar_sync(1 + quarter, 64);  // red is rewritten by the next unit's first exchange
       uint32_t o[4][16];
 #pragma unroll
       for (int q4 = 0; q4 < 4; ++q4) tmem_ld16_nowait(tmem_o + lane_base + half * 64 + q4 * 16, o[q4]);
       tmem_wait_ld();
+      if (valid) {
+        float4* dst = reinterpret_cast<float4*>(part_o + slot * 128 + half * 64);
 #pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4) {
-        tmem_reg_fence(o[q4]);
+        for (int q4 = 0; q4 < 4; ++q4) {
+          tmem_reg_fence(o[q4]);
 #pragma unroll
-        for (int jj = 0; jj < 16; jj += 4)
-          *reinterpret_cast<float4*>(stg + r * STG_LD + half * 64 + q4 * 16 + jj) =
-              make_float4(__uint_as_float(o[q4][jj]), __uint_as_float(o[q4][jj + 1]),
-                          __uint_as_float(o[q4][jj + 2]), __uint_as_float(o[q4][jj + 3]));
+          for (int jj = 0; jj < 16; jj += 4)
+            dst[q4 * 4 + jj / 4] = make_float4(__uint_as_float(o[q4][jj]), __uint_as_float(o[q4][jj + 1]),
+                                               __uint_as_float(o[q4][jj + 2]), __uint_as_float(o[q4][jj + 3]));
+        }
+        if (half == 0) part_ml[slot] = make_float2(m_run, l);
       }
-      if (valid && half == 0) part_ml[slot] = make_float2(m_run, l);
-      named_bar_sync(5, 256);
-      for (int idx = threadIdx.x - 128; idx < it.n_rows * 32; idx += 256) {
-        const int e = idx >> 5, f = idx & 31;
-        const int2 re = item_rows[it.row_off + e];
-        const size_t sl = ((size_t)re.x * num_heads + g * group + re.y) * max_chunks + it.chunk_idx;
-        const int rw = (e & 3) * 32 + (e >> 2);
-        reinterpret_cast<float4*>(part_o + sl * 128)[f] = *reinterpret_cast<const float4*>(stg + rw * STG_LD + f * 4);
-      }
+      // O may now be overwritten: the next unit's first P.V waits for this group's P arrive
+      tc_fence_before();
       if (r == 0 && half == 0) stamp(5);
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<L::TMEM_COLS>(tmem_base);
+  if (diag & 2) return;  // ICR_ATTN_DIAG (timing diagnostics only): no barrier, no merge
+
+  // ---------------- grid barrier + merge (attn_merge.cuh) ----------------
+  // All CTAs are resident (one per SM, grid <= #SMs; dependents launch only after every CTA
+  // has started), so they can wait for each other. Counters: coop[0] generation; per
+  // generation parity {arrived, go} (coop[32 + 64 p], coop[64 + 64 p]). The last to arrive re-arms the other set for the next
+  // launch, bumps the generation and releases everyone; the (row, KV group) merge units are
+  // then split statically, three per CTA round (one per 128-thread group).
+  if (threadIdx.x == 0) {
+    stamp(9);
+    const int gen = flag_s[0];
+    int* arrived = coop + 32 + (gen & 1) * 64;  // counter and flag on separate 128-byte lines
+    int* go = arrived + 32;
+    const int f = atom_add_acq_rel(arrived, 1);
+    if (f == (int)gridDim.x - 1) {
+      int* other = coop + 32 + ((gen + 1) & 1) * 64;
+      other[0] = 0;
+      other[32] = 0;
+      coop[0] = gen + 1;
+      red_add_release(go, 1);
+    } else {
+      while (ld_acquire(go) == 0) __nanosleep(20);
+    }
+    stamp(10);
+  }
+  __syncthreads();
+  if (!(diag & 1)) {
+    const int grp = threadIdx.x >> 7, lt = threadIdx.x & 127;
+    const int units = n_rows * num_kv_heads;
+    for (int u = grp * (int)gridDim.x + cta; u < units; u += 3 * (int)gridDim.x)
+      merge_unit<128>(part_o, part_ml, row_pos, row_kind, u / num_kv_heads, u % num_kv_heads,
+                      num_heads, group, max_chunks, chunk_tokens, out, out_ld, lt, 128);
+  }
+  if (threadIdx.x == 0) stamp(11);
 }
 
 cudaError_t attn_tc_partial_launch(const AttnLaunch& a, int /*chunk_pages*/, cudaStream_t s) {
@@ -454,10 +526,14 @@ cudaError_t attn_tc_partial_launch(const AttnLaunch& a, int /*chunk_pages*/, cud
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  return launch_pdl(attn_tc_kernel, dim3(a.num_kv_heads, a.n_items_cap), dim3(TC_THREADS), L::SMEM, s,
+  static const int diag = getenv("ICR_ATTN_DIAG") ? atoi(getenv("ICR_ATTN_DIAG")) : 0;
+  const int units = a.n_items_cap * a.num_kv_heads;
+  const int grid = units < a.num_sms ? units : a.num_sms;
+  return launch_pdl(attn_tc_kernel, dim3(grid), dim3(TC_THREADS), L::SMEM, s,
                     a.tm_k, a.tm_v, a.q, a.q_ld, a.num_kv_heads, a.group, a.items, a.item_pages,
                     a.item_rows, a.row_pos, a.num_heads, a.max_chunks, a.scale, a.part_o, a.part_ml,
-                    a.n_items_dev, a.trace);
+                    a.sched_off, a.sched_units, a.trace, a.row_kind, a.n_rows, a.chunk_tokens, a.out,
+                    a.out_ld, a.coop, diag);
 }
 
 }  // namespace icr

@@ -59,6 +59,9 @@ struct AttnLaunch {
   const __nv_bfloat16* v_pages;
   int num_kv_heads, num_heads, group, head_dim;
   const AttnItem* items;
+  const int* sched_off;    // tcgen05 path: persistent CTA c runs units [sched_off[c], sched_off[c+1])
+  const int* sched_units;  //   unit = item * num_kv_heads + KV head
+  int num_sms;             //   grid = min(num_sms, n_items_cap * num_kv_heads)
   const int* item_pages;
   const int2* item_rows;
   const int* n_items_dev;
@@ -71,6 +74,7 @@ struct AttnLaunch {
   float* part_o;
   float2* part_ml;
   int* merge_cnt;  // unused (kept for ABI of the test entry)
+  int* coop;       // tcgen05 path: grid-barrier counters [256], zero-initialised, per stream
   CUtensorMap tm_k, tm_v;  // page-arena maps: dims {hd, 16, pages*H_kv}, box {64, 16, 1}, 128B swizzle
   const uint8_t* pf_base;  // L2 prefetch of the next projection's weights (null = none)
   long long pf_bytes;

@@ -142,13 +142,49 @@ struct AttnPlan {
   std::vector<AttnItem> items;
   std::vector<int> pages;
   std::vector<int2> rows;
+  // persistent tcgen05 kernel: CTA c runs units sched_units[sched_off[c] .. sched_off[c+1]),
+  // unit = item * num_kv_heads + KV head
+  std::vector<int> sched_off, sched_units;
 };
+
+// Static longest-processing-time schedule of the (item, KV head) units over G = min(#SMs,
+// units) persistent CTAs: cost = pages + a fixed start-up cost of one 8-page sub-chunk; each
+// unit (longest first) goes to the least-loaded CTA (lowest index on ties) -- so units 0..G-1
+// go to CTAs 0..G-1 in order, which the kernel relies on to fetch its first unit without
+// reading the schedule. Deterministic, and no unit's arithmetic depends on where it runs.
+static void schedule_units(AttnPlan& plan, int num_kv_heads, int num_sms) {
+  const int n_units = (int)plan.items.size() * num_kv_heads;
+  const int G = std::max(1, std::min(num_sms, n_units));
+  std::vector<std::vector<int>> per(G);
+  std::vector<std::pair<long long, int>> heap;  // (load, cta), min-heap
+  for (int c = 0; c < G; ++c) heap.push_back({0, c});
+  auto cmp = [](const std::pair<long long, int>& a, const std::pair<long long, int>& b) { return a > b; };
+  std::make_heap(heap.begin(), heap.end(), cmp);
+  for (int i = 0; i < (int)plan.items.size(); ++i) {  // items are already longest-first
+    const long long cost = plan.items[i].n_pages + 8;
+    for (int h = 0; h < num_kv_heads; ++h) {
+      std::pop_heap(heap.begin(), heap.end(), cmp);
+      auto lc = heap.back();
+      per[lc.second].push_back(i * num_kv_heads + h);
+      lc.first += cost;
+      heap.back() = lc;
+      std::push_heap(heap.begin(), heap.end(), cmp);
+    }
+  }
+  plan.sched_off.assign(1, 0);
+  plan.sched_units.clear();
+  for (int c = 0; c < G; ++c) {
+    plan.sched_units.insert(plan.sched_units.end(), per[c].begin(), per[c].end());
+    plan.sched_off.push_back((int)plan.sched_units.size());
+  }
+}
 
 // Group (sequence, chunk) pairs that map to identical physical pages, so each shared page
 // is read once per KV head for every query row attached to it.
 static icr_status build_attn_plan(int n_rows, const int* kind, const int* seq, const int* pos,
                                   const int* bt, int n_seqs, int bt_stride, int num_pages,
-                                  int group, int chunk_pages, AttnPlan& plan, int head_dim) {
+                                  int group, int chunk_pages, AttnPlan& plan, int head_dim,
+                                  int num_kv_heads, int num_sms) {
   const int CT = chunk_pages * 16;
   const size_t EPI = (size_t)attn_entries_per_item(head_dim);
   plan.items.clear();
@@ -227,7 +263,9 @@ static icr_status build_attn_plan(int n_rows, const int* kind, const int* seq, c
       AttnItem it;
       it.chunk_start = c0;
       it.n_pages = npages;
-      it.page_off = (int)plan.pages.size();
+      // fixed stride: item i's pages start at i * chunk_pages, so a CTA can request its page
+      // ids in parallel with (not after) its item record
+      it.page_off = (int)plan.items.size() * chunk_pages;
       it.row_off = (int)plan.rows.size();
       it.n_rows = (int)(e1 - e0);
       it.chunk_idx = gr.c;
@@ -235,10 +273,12 @@ static icr_status build_attn_plan(int n_rows, const int* kind, const int* seq, c
       it.n_pre = fresh == INT32_MAX ? npages
                                     : std::min(npages, std::max(0, (fresh - c0) >> 4));
       plan.items.push_back(it);
-      plan.pages.insert(plan.pages.end(), gr.pages.begin(), gr.pages.begin() + npages);
+      plan.pages.resize((size_t)it.page_off + chunk_pages, 0);
+      std::copy(gr.pages.begin(), gr.pages.begin() + npages, plan.pages.begin() + it.page_off);
       plan.rows.insert(plan.rows.end(), entries.begin() + e0, entries.begin() + e1);
     }
   }
+  schedule_units(plan, num_kv_heads, num_sms);
   return ICR_OK;
 }
 
@@ -251,7 +291,7 @@ struct Meta {
   size_t items_cap = 0, rows_cap = 0, pages_cap = 0;
   size_t o_tokens = 0, o_kind = 0, o_seq = 0, o_pos = 0, o_adapter = 0, o_lm_rows = 0,
          o_seg_off = 0, o_seg_rows = 0, o_n_items = 0, o_feedback = 0, o_bt = 0, o_items = 0,
-         o_lm_store = 0,
+         o_lm_store = 0, o_sched_off = 0, o_sched_units = 0,
          o_item_rows = 0, o_item_pages = 0, total = 0, used = 0;
 };
 
@@ -300,6 +340,7 @@ struct icr_model {
   float* part_o = nullptr;
   float2* part_ml = nullptr;
   int* merge_cnt = nullptr;
+  int* attn_coop = nullptr;  // in-kernel attention merge counters
   float2* rope = nullptr;
   float* ws = nullptr;
   int* counters = nullptr;
@@ -369,6 +410,8 @@ static Meta layout_meta(const icr_model* m, int n_rows) {
   mt.o_bt = take((size_t)c.max_seqs * c.max_pages_per_seq);
   mt.o_items = take(mt.items_cap * (sizeof(AttnItem) / sizeof(int)));
   mt.o_item_rows = take(mt.rows_cap * 2);
+  mt.o_sched_off = take(m->num_sms + 1);
+  mt.o_sched_units = take(mt.items_cap * c.num_kv_heads);
   mt.o_item_pages = take(mt.pages_cap);
   mt.total = off;
   return mt;
@@ -397,7 +440,8 @@ static icr_status pack_meta(icr_model* m, const icr_batch* b, const int* pos, co
   const icr_model_config& c = m->cfg;
   const int n = b->n_rows, rp = mt.rp;
   if (plan.items.size() > mt.items_cap || plan.rows.size() > mt.rows_cap ||
-      plan.pages.size() > mt.pages_cap)
+      plan.pages.size() > mt.pages_cap || plan.sched_off.size() > (size_t)m->num_sms + 1 ||
+      plan.sched_units.size() > mt.items_cap * c.num_kv_heads)
     return fail(ICR_CAPACITY, "attention plan exceeds metadata capacity");
   mt.n_items = (int)plan.items.size();
   int n_lm = 0, n_dec = 0;
@@ -440,6 +484,8 @@ static icr_status pack_meta(icr_model* m, const icr_batch* b, const int* pos, co
   memcpy(t + mt.o_bt, b->block_table, sizeof(int) * (size_t)b->n_seqs * c.max_pages_per_seq);
   memcpy(t + mt.o_items, plan.items.data(), plan.items.size() * sizeof(AttnItem));
   memcpy(t + mt.o_item_rows, plan.rows.data(), plan.rows.size() * sizeof(int2));
+  memcpy(t + mt.o_sched_off, plan.sched_off.data(), plan.sched_off.size() * sizeof(int));
+  memcpy(t + mt.o_sched_units, plan.sched_units.data(), plan.sched_units.size() * sizeof(int));
   memcpy(t + mt.o_item_pages, plan.pages.data(), plan.pages.size() * sizeof(int));
   mt.used = mt.o_item_pages + plan.pages.size();
   return ICR_OK;
@@ -547,6 +593,9 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
   al.group = m->group;
   al.head_dim = c.head_dim;
   al.items = reinterpret_cast<const AttnItem*>(md + mt.o_items);
+  al.sched_off = md + mt.o_sched_off;
+  al.sched_units = md + mt.o_sched_units;
+  al.num_sms = m->num_sms;
   al.item_pages = md + mt.o_item_pages;
   al.item_rows = reinterpret_cast<const int2*>(md + mt.o_item_rows);
   al.n_items_dev = md + mt.o_n_items;
@@ -560,6 +609,7 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
   al.part_o = m->part_o;
   al.part_ml = m->part_ml;
   al.merge_cnt = m->merge_cnt;
+  al.coop = m->attn_coop;
   al.out = m->att;
   al.out_ld = m->q_dim;
 
@@ -833,6 +883,7 @@ icr_status icr_model_create(const icr_model_config* cfg, const icr_layer_weights
   ALLOC(m->part_o, rp * c.num_heads * m->max_chunks * c.head_dim * sizeof(float));
   ALLOC(m->part_ml, rp * c.num_heads * m->max_chunks * sizeof(float2));
   ALLOC(m->merge_cnt, rp * c.num_kv_heads * sizeof(int));
+  ALLOC(m->attn_coop, 256 * sizeof(int));
   ALLOC(m->rope, (size_t)c.max_positions * (c.head_dim / 2) * sizeof(float2));
   ALLOC(m->ws, gemm_ws_floats(m->num_sms) * sizeof(float));
   {
@@ -907,7 +958,7 @@ icr_status icr_model_destroy(icr_model* m) {
   cudaDeviceSynchronize();
   for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
   void* bufs[] = {m->x, m->xb, m->ssq, m->ssq_lm, m->qb, m->att, m->f, m->hlm, m->ubd,
-                  m->tile_best, m->out_tok, m->hid, m->hid_ssq, m->slot_idx, m->part_o, m->part_ml, m->merge_cnt, m->rope, m->ws,
+                  m->tile_best, m->out_tok, m->hid, m->hid_ssq, m->slot_idx, m->part_o, m->part_ml, m->merge_cnt, m->attn_coop, m->rope, m->ws,
                   m->counters, m->sync, m->sh_part, m->sh_cnt, m->meta_dev};
   for (void* p : bufs)
     if (p) cudaFree(p);
@@ -947,7 +998,8 @@ icr_status icr_forward(icr_model* m, const icr_batch* b, int32_t* out_tokens_hos
   AttnPlan plan;
   st = build_attn_plan(b->n_rows, b->row_kind, b->row_seq, b->row_pos, b->block_table, b->n_seqs,
                        m->cfg.max_pages_per_seq, m->cfg.num_pages, plan_group(m),
-                       m->cfg.chunk_pages, plan, m->cfg.head_dim);
+                       m->cfg.chunk_pages, plan, m->cfg.head_dim,
+                       m->cfg.num_kv_heads, m->num_sms);
   if (st) return st;
   Meta mt = layout_meta(m, b->n_rows);
   if ((st = ensure_meta(m, mt.total))) return st;
@@ -994,7 +1046,8 @@ icr_status icr_decode_loop(icr_model* m, const icr_batch* first, const int32_t* 
     AttnPlan plan;
     if ((st = build_attn_plan(n, first->row_kind, first->row_seq, pos.data(), first->block_table,
                               first->n_seqs, m->cfg.max_pages_per_seq, m->cfg.num_pages,
-                              plan_group(m), m->cfg.chunk_pages, plan, m->cfg.head_dim)))
+                              plan_group(m), m->cfg.chunk_pages, plan, m->cfg.head_dim,
+                       m->cfg.num_kv_heads, m->num_sms)))
       break;
     const int slot = i & 1;
     cudaEventSynchronize(m->staging_ev[slot]);
@@ -1382,6 +1435,8 @@ __global__ void l2_flush_read_kernel(const uint4* __restrict__ p, size_t n, unsi
   if (acc == 0x12345678u) *sink = acc;
 }
 
+__global__ void stamp_kernel(unsigned long long* dst) { *dst = globaltimer(); }
+
 // Attention micro-benchmark (C4 sweep): plans once, then launches partial + merge `iters`
 // times (L2 flushed between launches by the caller-provided flush buffer when non-null);
 // returns the average device ms per launch pair and the number of work items.
@@ -1398,7 +1453,8 @@ icr_status icr_bench_attention(const void* q_dev, const void* k_pages, const voi
   AttnPlan plan;
   icr_status st = build_attn_plan(n_rows, kind.data(), row_seq_host, row_pos_host, block_table_host,
                                   n_seqs, max_pages_per_seq, 1 << 30, num_heads / num_kv_heads,
-                                  chunk_pages, plan, head_dim);
+                                  chunk_pages, plan, head_dim, num_kv_heads,
+                                  query_sms());
   if (st) return st;
   if (n_items_out) *n_items_out = (int)plan.items.size();
   int maxpos = 0;
@@ -1417,6 +1473,14 @@ icr_status icr_bench_attention(const void* q_dev, const void* k_pages, const voi
   CUDA_TRY(cudaMalloc(&d_rows, std::max<size_t>(plan.rows.size(), 1) * sizeof(int2)));
   CUDA_TRY(cudaMalloc(&d_po, (size_t)n_rows * num_heads * max_chunks * head_dim * sizeof(float)));
   CUDA_TRY(cudaMalloc(&d_pml, (size_t)n_rows * num_heads * max_chunks * sizeof(float2)));
+  int* d_coop = nullptr;
+  CUDA_TRY(cudaMalloc(&d_coop, 256 * sizeof(int)));
+  CUDA_TRY(cudaMemset(d_coop, 0, 256 * sizeof(int)));
+  int* d_sched = nullptr;
+  CUDA_TRY(cudaMalloc(&d_sched, (plan.sched_off.size() + plan.sched_units.size()) * sizeof(int)));
+  CUDA_TRY(cudaMemcpy(d_sched, plan.sched_off.data(), plan.sched_off.size() * sizeof(int), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(d_sched + plan.sched_off.size(), plan.sched_units.data(),
+                      plan.sched_units.size() * sizeof(int), cudaMemcpyHostToDevice));
   int nitems = (int)plan.items.size();
   CUDA_TRY(cudaMemcpy(d_pos, row_pos_host, n_rows * sizeof(int), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(d_kind, kind.data(), n_rows * sizeof(int), cudaMemcpyHostToDevice));
@@ -1446,6 +1510,10 @@ icr_status icr_bench_attention(const void* q_dev, const void* k_pages, const voi
   a.scale = (float)(1.0 / std::sqrt((double)head_dim));
   a.part_o = d_po;
   a.part_ml = d_pml;
+  a.coop = d_coop;
+  a.sched_off = d_sched;
+  a.sched_units = d_sched + plan.sched_off.size();
+  a.num_sms = query_sms();
   a.out = (__nv_bfloat16*)out_dev;
   a.out_ld = num_heads * head_dim;
   {
@@ -1488,6 +1556,10 @@ icr_status icr_bench_attention(const void* q_dev, const void* k_pages, const voi
     total = ms;
     cudaFree(d_alt);
   }
+  // the flush runs with the attention kernel's shared-memory carveout, so the timed launch
+  // does not pay an L1/shared reconfiguration of every SM (inside a decode step the kernel
+  // before the attention is a GEMM with the same carveout)
+  cudaFuncSetAttribute(l2_flush_read_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   for (int it = 0; it < iters && e == cudaSuccess && alt_page_offset == 0; ++it) {
     if (flush_dev) {
       l2_flush_read_kernel<<<1184, 256, 0, s>>>((const uint4*)flush_dev, (size_t)flush_bytes / 16,
@@ -1500,10 +1572,17 @@ icr_status icr_bench_attention(const void* q_dev, const void* k_pages, const voi
       cudaMemcpyAsync(d_items, plan.items.data(), plan.items.size() * sizeof(AttnItem), cudaMemcpyHostToDevice, s);
       cudaMemcpyAsync(d_rows, plan.rows.data(), plan.rows.size() * sizeof(int2), cudaMemcpyHostToDevice, s);
       cudaMemcpyAsync(d_n, &nitems, sizeof(int), cudaMemcpyHostToDevice, s);
+      cudaMemcpyAsync(d_sched, plan.sched_off.data(), plan.sched_off.size() * sizeof(int), cudaMemcpyHostToDevice, s);
+      cudaMemcpyAsync(d_sched + plan.sched_off.size(), plan.sched_units.data(),
+                      plan.sched_units.size() * sizeof(int), cudaMemcpyHostToDevice, s);
     }
     cudaEventRecord(e0, s);
-    if (tr && it == iters - 1) a.trace = tr;
+    if (tr && it == iters - 1) {
+      a.trace = tr;
+      stamp_kernel<<<1, 1, 0, s>>>(tr + (size_t)3 * 4096 * 16 - 8);
+    }
     e = attn_launch(a, s);
+    if (tr && it == iters - 1) stamp_kernel<<<1, 1, 0, s>>>(tr + (size_t)3 * 4096 * 16 - 7);
     a.trace = nullptr;
     cudaEventRecord(e1, s);
     cudaEventSynchronize(e1);
@@ -1521,15 +1600,20 @@ icr_status icr_bench_attention(const void* q_dev, const void* k_pages, const voi
     for (size_t i = 0; i < (size_t)2 * 4096 * 16; ++i)
       if (i % 16 < 8 && h[i] && h[i] < t0) t0 = h[i];
     if (FILE* f = fopen(trace_path, "w")) {
-      fprintf(f, "kind,idx,s0,s1,s2,s3,s4,s5,s6,s7\n");
+      fprintf(f, "kind,idx,s0,s1,s2,s3,s4,s5,s6,s7,s8,s9,s10,s11\n");
       for (int k = 0; k < 2; ++k)
         for (int c2 = 0; c2 < 4096; ++c2) {
           const unsigned long long* r = &h[((size_t)k * 4096 + c2) * 16];
           if (!r[6]) continue;
           fprintf(f, "%s,%d", k ? "merge" : "partial", c2);
-          for (int q = 0; q < 8; ++q) fprintf(f, ",%.3f", r[q] ? (r[q] - t0) / 1000.0 : -1.0);
+          for (int q = 0; q < 12; ++q) fprintf(f, ",%.3f", (r[q] && q != 8) ? (r[q] - t0) / 1000.0 : -1.0);
           fprintf(f, "\n");
         }
+      {
+        const unsigned long long* r = &h[(size_t)3 * 4096 * 16 - 8];
+        fprintf(f, "launch,0,%.3f,%.3f\n", r[0] ? ((long long)r[0] - (long long)t0) / 1000.0 : -1.0,
+                r[1] ? ((long long)r[1] - (long long)t0) / 1000.0 : -1.0);
+      }
       for (int j = 0; j < 256; ++j) {
         const unsigned long long* r = &h[(size_t)2 * 4096 * 16 + j * 8];
         if (!r[0] && !r[1]) continue;
@@ -1542,7 +1626,7 @@ icr_status icr_bench_attention(const void* q_dev, const void* k_pages, const voi
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  void* bufs[] = {d_pos, d_kind, d_pages, d_n, d_items, d_rows, d_po, d_pml};
+  void* bufs[] = {d_pos, d_kind, d_pages, d_n, d_items, d_rows, d_po, d_pml, d_coop, d_sched};
   for (void* p : bufs) cudaFree(p);
   if (e != cudaSuccess) return fail(ICR_CUDA, "attention bench: %s", cudaGetErrorString(e));
   return ICR_OK;
@@ -1603,7 +1687,8 @@ icr_status icr_paged_attention(const void* q_dev, const void* k_pages, const voi
   AttnPlan plan;
   icr_status st = build_attn_plan(n_rows, kind.data(), row_seq_host, row_pos_host, block_table_host,
                                   n_seqs, max_pages_per_seq, 1 << 30, num_heads / num_kv_heads,
-                                  chunk_pages, plan, head_dim);
+                                  chunk_pages, plan, head_dim, num_kv_heads,
+                                  query_sms());
   if (st) return st;
   if (n_items_out) *n_items_out = (int)plan.items.size();
   int maxpos = 0;
@@ -1615,6 +1700,7 @@ icr_status icr_paged_attention(const void* q_dev, const void* k_pages, const voi
   float* d_po;
   float2* d_pml;
   int* d_cnt;
+  int* d_sched;
   const size_t np = std::max<size_t>(plan.pages.size(), 1), nr = std::max<size_t>(plan.rows.size(), 1),
                ni = std::max<size_t>(plan.items.size(), 1);
   CUDA_TRY(cudaMalloc(&d_pos, n_rows * sizeof(int)));
@@ -1625,8 +1711,14 @@ icr_status icr_paged_attention(const void* q_dev, const void* k_pages, const voi
   CUDA_TRY(cudaMalloc(&d_rows, nr * sizeof(int2)));
   CUDA_TRY(cudaMalloc(&d_po, (size_t)n_rows * num_heads * max_chunks * head_dim * sizeof(float)));
   CUDA_TRY(cudaMalloc(&d_pml, (size_t)n_rows * num_heads * max_chunks * sizeof(float2)));
-  CUDA_TRY(cudaMalloc(&d_cnt, (size_t)n_rows * num_kv_heads * sizeof(int)));
-  CUDA_TRY(cudaMemsetAsync(d_cnt, 0, (size_t)n_rows * num_kv_heads * sizeof(int), s));
+  const size_t cnt_n = std::max<size_t>((size_t)n_rows * num_kv_heads, 256);
+  CUDA_TRY(cudaMalloc(&d_cnt, cnt_n * sizeof(int)));
+  CUDA_TRY(cudaMemsetAsync(d_cnt, 0, cnt_n * sizeof(int), s));
+  CUDA_TRY(cudaMalloc(&d_sched, (plan.sched_off.size() + plan.sched_units.size()) * sizeof(int)));
+  CUDA_TRY(cudaMemcpyAsync(d_sched, plan.sched_off.data(), plan.sched_off.size() * sizeof(int),
+                           cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(d_sched + plan.sched_off.size(), plan.sched_units.data(),
+                           plan.sched_units.size() * sizeof(int), cudaMemcpyHostToDevice, s));
   int nitems = (int)plan.items.size();
   CUDA_TRY(cudaMemcpyAsync(d_pos, row_pos_host, n_rows * sizeof(int), cudaMemcpyHostToDevice, s));
   CUDA_TRY(cudaMemcpyAsync(d_kind, kind.data(), n_rows * sizeof(int), cudaMemcpyHostToDevice, s));
@@ -1657,6 +1749,10 @@ icr_status icr_paged_attention(const void* q_dev, const void* k_pages, const voi
   a.part_o = d_po;
   a.part_ml = d_pml;
   a.merge_cnt = d_cnt;
+  a.coop = d_cnt;
+  a.sched_off = d_sched;
+  a.sched_units = d_sched + plan.sched_off.size();
+  a.num_sms = query_sms();
   {
     int maxpage = 0;
     for (size_t i = 0; i < plan.pages.size(); ++i) maxpage = std::max(maxpage, plan.pages[i]);
@@ -1668,7 +1764,7 @@ icr_status icr_paged_attention(const void* q_dev, const void* k_pages, const voi
   a.out_ld = num_heads * head_dim;
   cudaError_t e = attn_launch(a, s);
   cudaError_t e2 = cudaStreamSynchronize(s);
-  void* bufs[] = {d_pos, d_kind, d_pages, d_n, d_items, d_rows, d_po, d_pml, d_cnt};
+  void* bufs[] = {d_pos, d_kind, d_pages, d_n, d_items, d_rows, d_po, d_pml, d_cnt, d_sched};
   for (void* p : bufs) cudaFree(p);
   if (e != cudaSuccess) return fail(ICR_CUDA, "attention: %s", cudaGetErrorString(e));
   if (e2 != cudaSuccess) return fail(ICR_CUDA, "attention sync: %s", cudaGetErrorString(e2));
@@ -1690,7 +1786,8 @@ icr_status icr_layer_forward(icr_model* m, const icr_batch* b, int layer, const 
   AttnPlan plan;
   st = build_attn_plan(b->n_rows, b->row_kind, b->row_seq, b->row_pos, b->block_table, b->n_seqs,
                        m->cfg.max_pages_per_seq, m->cfg.num_pages, plan_group(m),
-                       m->cfg.chunk_pages, plan, m->cfg.head_dim);
+                       m->cfg.chunk_pages, plan, m->cfg.head_dim,
+                       m->cfg.num_kv_heads, m->num_sms);
   if (st) return st;
   Meta mt = layout_meta(m, b->n_rows);
   if ((st = ensure_meta(m, mt.total))) return st;
