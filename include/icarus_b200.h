@@ -170,13 +170,16 @@ icr_status icr_bench_gemm(const void* w, const void* x, int M, int K, int rows, 
  * partial + merge kernels (a read of flush_dev between launches evicts L2 when non-NULL).
  * alt_page_offset > 0: pipelined mode -- `iters` launches back to back (PDL, no flush), odd
  * launches reading the same plan with every page id + alt_page_offset (a second copy of the
- * K/V, so no launch finds its pages in L2); avg_ms = total / iters. */
+ * K/V, so no launch finds its pages in L2); avg_ms = total / iters. span_us (may be NULL):
+ * cold mode's average device span of the kernels themselves -- first partial CTA start to
+ * last partial / merge CTA end by %globaltimer, i.e. without the event/launch overhead. */
 icr_status icr_bench_attention(const void* q_dev, const void* k_pages, const void* v_pages,
                                int num_heads, int num_kv_heads, int head_dim, int chunk_pages,
                                int n_rows, const int32_t* row_seq_host, const int32_t* row_pos_host,
                                const int32_t* block_table_host, int n_seqs, int max_pages_per_seq,
                                void* out_dev, void* flush_dev, long long flush_bytes, int iters,
-                               int alt_page_offset, float* avg_ms, int32_t* n_items_out, void* stream);
+                               int alt_page_offset, float* avg_ms, int32_t* n_items_out,
+                               float* span_us, void* stream);
 
 /* --- building blocks, exported for parity tests -------------------------------- */
 

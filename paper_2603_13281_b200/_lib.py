@@ -89,7 +89,8 @@ def load():
         "icr_gemm_bf16": [p, p, p, i, i, i, p],
         "icr_bench_attention": [p, p, p, i, i, i, i, i, C.POINTER(C.c_int32),
                                 C.POINTER(C.c_int32), C.POINTER(C.c_int32), i, i, p, p,
-                                C.c_longlong, i, i, C.POINTER(C.c_float), C.POINTER(C.c_int32), p],
+                                C.c_longlong, i, i, C.POINTER(C.c_float), C.POINTER(C.c_int32),
+                                C.POINTER(C.c_float), p],
         "icr_layer_forward": [p, C.POINTER(BatchC), i, p, p, p],
         "icr_seq_logits": [p, C.POINTER(C.c_int32), i, p, p],
         "icr_linear_bf16": [p, p, p, i, i, i, p, p, i, C.POINTER(C.c_int32), p],

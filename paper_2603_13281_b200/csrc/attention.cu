@@ -149,8 +149,8 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
         mbar_expect_tx(&full[st], 2 * PB);
 #pragma unroll
         for (int h = 0; h < HD / 64; ++h) {
-          tma_load_3d(kd + h * 2048, &tm_k, &full[st], h * 64, 0, plane);
-          tma_load_3d(kd + PB + h * 2048, &tm_v, &full[st], h * 64, 0, plane);
+          tma_load_4d(kd + h * 2048, &tm_k, &full[st], 0, 0, h, plane);
+          tma_load_4d(kd + PB + h * 2048, &tm_v, &full[st], 0, 0, h, plane);
         }
       }
       if (it.n_pages <= pre) pdl_wait();
@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
 // Fixed-order merge of chunk partials (attn_merge.cuh): one CTA per (row, KV group), one
 // thread per (head-in-group, 4 dims). Few threads and no shared memory: a merge CTA fits
 // beside the next GEMM's CTA, which can then start streaming its weights while the merge
-// runs. The tcgen05 path merges inside its partial kernel with the same fold.
+// runs. Both partial kernels (mma.sync and tcgen05) feed it.
 constexpr int MERGE_THREADS = 128;
 
 template <int HD>
@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(MERGE_THREADS)
                       const int* __restrict__ row_pos, const int* __restrict__ row_kind,
                       int num_heads, int group, int max_chunks, int chunk_tokens,
                       __nv_bfloat16* __restrict__ out, int out_ld,
-                      unsigned long long* __restrict__ trace) {
+                      unsigned long long* __restrict__ trace, unsigned long long* __restrict__ span) {
   const int cta_id = blockIdx.y * gridDim.x + blockIdx.x;
   if (trace != nullptr && threadIdx.x == 0 && cta_id < 4096) trace[(size_t)cta_id * 16 + 6] = globaltimer();
   pdl_launch();
@@ -374,6 +374,10 @@ __global__ void __launch_bounds__(MERGE_THREADS)
   merge_unit<HD>(part_o, part_ml, row_pos, row_kind, blockIdx.x, blockIdx.y, num_heads, group,
                  max_chunks, chunk_tokens, out, out_ld, threadIdx.x, blockDim.x);
   if (trace != nullptr && threadIdx.x == 0 && cta_id < 4096) trace[(size_t)cta_id * 16 + 5] = globaltimer();
+  if (span != nullptr) {
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMax(span + 1, globaltimer());
+  }
 }
 
 static bool use_tc(int head_dim) {
@@ -385,7 +389,15 @@ int attn_entries_per_item(int head_dim) { return use_tc(head_dim) ? 128 : 64; }
 
 template <int HD>
 static cudaError_t attn_launch_hd(const AttnLaunch& a, cudaStream_t s) {
-  if (use_tc(HD)) return attn_tc_partial_launch(a, a.chunk_tokens / 16, s);  // merge fused
+  if (use_tc(HD)) {
+    cudaError_t e = attn_tc_partial_launch(a, a.chunk_tokens / 16, s);
+    if (e != cudaSuccess) return e;
+    const int mthreads = std::min(MERGE_THREADS, ((a.group * HD / 4 + 31) / 32) * 32);
+    return launch_pdl(attn_merge_kernel<HD>, dim3(a.n_rows, a.num_kv_heads), dim3(mthreads), 0, s,
+                      a.part_o, a.part_ml, a.row_pos, a.row_kind, a.num_heads, a.group,
+                      a.max_chunks, a.chunk_tokens, a.out, a.out_ld,
+                      a.trace ? a.trace + 4096 * 16 : nullptr, a.span);
+  }
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(attn_partial_kernel<HD>,
@@ -405,7 +417,7 @@ static cudaError_t attn_launch_hd(const AttnLaunch& a, cudaStream_t s) {
                     dim3(a.n_rows, a.num_kv_heads), dim3(mthreads), 0, s,
                     a.part_o, a.part_ml, a.row_pos, a.row_kind, a.num_heads, a.group,
                     a.max_chunks, a.chunk_tokens, a.out, a.out_ld,
-                    a.trace ? a.trace + 4096 * 16 : nullptr);
+                    a.trace ? a.trace + 4096 * 16 : nullptr, a.span);
 }
 
 cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t s) {

@@ -8,23 +8,21 @@
 // whose block table maps the same physical pages; its up to 128 query entries (row,
 // head-in-group) -- the encoder and decoder heads of every model sharing the prefix -- are the
 // M = 128 rows of the tcgen05 MMAs. The chunk is streamed in sub-chunks of SUBP = 8 pages
-// (128 keys) through a 2-stage TMA ring:
+// (128 keys) through a 3-stage TMA ring:
 //   S_j[128 x 128] = Q . K_j^T            (K-major Q and K; fp32, double-buffered in TMEM)
 //   softmax        : 8 warps, two per TMEM lane quarter (each half of the key columns), exp2
-//                    domain with the causal mask; running max m, sum l per entry; P_j bf16 into
-//                    the SW128 K-major layout; O rescaled in TMEM when the max moves
-//   O[128 x 128]  += P_j . V_j              (V consumed MN-major straight from the pages)
+//                    domain with the causal mask; running max m, sum l per entry; P_j bf16
+//                    back into TMEM; O rescaled in TMEM when the max moves
+//   O[128 x 128]  += P_j . V_j              (P from TMEM, V MN-major straight from the pages)
 // so S_{j+1}, the loads of sub-chunk j+2 and the softmax of j overlap -- within a unit and
 // across consecutive units of a CTA. The unnormalised partial (O, m, l) per (row, head, chunk)
-// is written out; after a grid barrier (all CTAs are resident) the CTAs fold the partials of
-// every (row, KV group) in chunk order (attn_merge.cuh) -- no second launch. Each K/V page is
+// is written out and folded in chunk order by the merge kernel (attention.cu, attn_merge.cuh),
+// launched behind this one with PDL: its small CTAs share SMs with the next projection GEMM,
+// which streams its weights while the merge runs. Each K/V page is
 // staged in shared memory once per KV head for all entries: HBM bytes scale with context, not
 // with the number of models. Sub-chunk boundaries sit at fixed offsets from the chunk's
 // absolute start, so a row's partial never depends on which other rows share the item or on
 // which CTA runs it.
-#include <cstdlib>
-
-#include "attn_merge.cuh"
 #include "kernels.h"
 #include "ptx.cuh"
 
@@ -36,17 +34,19 @@ constexpr int SUBP = 8;          // pages per sub-chunk (N = 128 keys per S MMA)
 
 struct TcLayout {
   static constexpr uint32_t Q_OFF = 0;                     // 2 K-blocks x [128 rows x 128 B]
-  static constexpr uint32_t P_OFF = 32768;                 // [2 buffers][2 K-blocks][128 x 128 B]
-  static constexpr uint32_t P_BYTES = 32768;
   static constexpr uint32_t HALF = SUBP * 16 * 128;        // 16 KB: one 64-dim half, 128 keys
-  static constexpr uint32_t STAGE0 = P_OFF + 2 * P_BYTES;  // stage s: K halves, then V halves
+  static constexpr uint32_t STAGE0 = 32768;                // stage s: K halves, then V halves
   static constexpr uint32_t STAGE_BYTES = 4 * HALF;        // 64 KB
-  static constexpr uint32_t BAR_OFF = STAGE0 + 2 * STAGE_BYTES;
+  static constexpr int NSTAGE = 3;                         // K/V sub-chunks in flight
+  static constexpr uint32_t BAR_OFF = STAGE0 + NSTAGE * STAGE_BYTES;
   static constexpr uint32_t RED_OFF = BAR_OFF + 256;       // float [2 halves][128]
-  static constexpr uint32_t FLAG_OFF = RED_OFF + 256 * 4;  // int [16] merge bookkeeping
-  // 230,720 B: within the opt-in maximum of 232,448 less the 1 KB the driver reserves
-  static constexpr size_t SMEM = FLAG_OFF + 16 * 4;
-  static constexpr uint32_t TMEM_COLS = 512;               // S0 [0,128) S1 [128,256) O [256,384)
+  // 230,656 B: within the opt-in maximum of 232,448 less the 1 KB the driver reserves
+  static constexpr size_t SMEM = RED_OFF + 256 * 4;
+  // TMEM columns: S0 [0,128) S1 [128,256) O [256,384) P0 [384,448) P1 [448,512) -- P (bf16
+  // pairs packed in 32-bit columns) is the A operand of P.V straight from TMEM, so shared
+  // memory holds Q and three K/V stages
+  static constexpr uint32_t TMEM_COLS = 512;
+  static constexpr uint32_t P_COL = 384;
 };
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -98,27 +98,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                    int num_heads, int max_chunks, float scale, float* __restrict__ part_o,
                    float2* __restrict__ part_ml, const int* __restrict__ sched_off,
                    const int* __restrict__ sched_units, unsigned long long* __restrict__ trace,
-                   const int* __restrict__ row_kind, int n_rows, int chunk_tokens,
-                   __nv_bfloat16* __restrict__ out, int out_ld, int* __restrict__ coop, int diag) {
+                   int chunk_tokens, unsigned long long* __restrict__ span) {
   using L = TcLayout;
   extern __shared__ __align__(1024) uint8_t tc_smem[];
   uint8_t* smem = tc_smem;  // no static shared memory: the dynamic window starts 1024-aligned
   uint8_t* sQ = smem + L::Q_OFF;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
   uint64_t* q_full = bars + 0;    // Q of the CTA's n-th unit staged (phase n)
-  uint64_t* kv_full = bars + 1;   // [2] K landed
-  uint64_t* kv_empty = bars + 3;  // [2] K consumed by S
+  uint64_t* kv_full = bars + 20;  // [3] K landed
+  uint64_t* kv_empty = bars + 23; // [3] K consumed by S
   uint64_t* s_full = bars + 5;    // [2]
   uint64_t* p_full_b[2] = {bars + 7, bars + 17};  // P(J) written (+ O rescaled), per buffer
   uint64_t* o_done = bars + 8;    // one phase per P.V (the lazy rescale waits on it)
-  uint64_t* p_free = bars + 9;    // [2]: P buffer b consumed by its P.V
+  uint64_t* p_free = bars + 9;    // [2]: TMEM P buffer b consumed by its P.V
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
-  uint64_t* v_full = bars + 12;   // [2] V landed
-  uint64_t* v_empty = bars + 14;  // [2] V consumed by P.V
+  uint64_t* v_full = bars + 26;   // [3] V landed
+  uint64_t* v_empty = bars + 29;  // [3] V consumed by P.V
   uint64_t* o_final = bars + 16;  // the unit's last P.V landed (phase n)
   uint64_t* q_free = bars + 18;   // the unit's last S MMA has read Q (phase n)
   float* red = reinterpret_cast<float*>(smem + L::RED_OFF);
-  int* flag_s = reinterpret_cast<int*>(smem + L::FLAG_OFF);  // [0] generation
 
   const int cta = blockIdx.x;
   auto stamp = [&](int k) {
@@ -128,7 +126,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   auto sstamp = [&](int j, int k) {
     if (trace != nullptr && cta == 0 && j < 256) trace[(size_t)2 * 4096 * 16 + j * 8 + k] = globaltimer();
   };
-  if (threadIdx.x == 0) stamp(6);
+  if (threadIdx.x == 0) {
+    stamp(6);
+    if (span != nullptr) atomicMin(span, globaltimer());
+  }
   if ((smem_u32(tc_smem) & 1023) != 0) __trap();  // SW128 tiles need a 1024-byte base
   pdl_launch();
   const int warp = warp_id(), lane = lane_id();
@@ -143,13 +144,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 32);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < L::NSTAGE; ++b) {
       mbar_init(&kv_full[b], 1);
       mbar_init(&kv_empty[b], 1);
       mbar_init(&v_full[b], 1);
       mbar_init(&v_empty[b], 1);
-      mbar_init(&s_full[b], 1);
     }
+    for (int b = 0; b < 2; ++b) mbar_init(&s_full[b], 1);
     mbar_init(p_full_b[0], 256);
     mbar_init(p_full_b[1], 256);
     mbar_init(o_done, 1);
@@ -160,11 +161,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<L::TMEM_COLS>(tmem_slot);
-  // P starts zero (padding entries' rows are never written; they only feed padding O rows)
-  if (warp >= 4)
-    for (int i = threadIdx.x - 128; i < 2 * (int)L::P_BYTES / 16; i += 256)
-      *reinterpret_cast<uint4*>(smem + L::P_OFF + i * 16) = make_uint4(0, 0, 0, 0);
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -190,10 +186,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int item = unit / num_kv_heads, g = unit % num_kv_heads;
       const int np = it.n_pages, nsub = (np + SUBP - 1) / SUBP;
       AttnItem it_n = it;
-      int pid_n0 = 0, pid_nxt = 0;
+      int pid_n0 = 0, pid_nxt = 0, nunit = 0;
       for (int j = 0; j < nsub; ++j, ++J) {
-        const int b = J & 1;
-        if (J >= 2) mbar_wait(&empty[b], ((J >> 1) - 1) & 1);
+        const int b = J % L::NSTAGE, ph = (J / L::NSTAGE) & 1;
+        if (J >= L::NSTAGE) mbar_wait(&empty[b], ph ^ 1);
         const int p0 = j * SUBP, pn = min(SUBP, np - p0);
         if (p0 > 0 && (p0 & 31) == 0) {
           pid_cur = pid_nxt;
@@ -210,17 +206,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           const int plane = __shfl_sync(0xffffffffu, pid_cur, (p0 + pi) & 31) * num_kv_heads + g;
           if (lane == 0) {
 #pragma unroll
-            for (int h = 0; h < 2; ++h) tma_load_3d(st + h * L::HALF + pi * 2048, tm, &full[b], h * 64, 0, plane);
+            for (int h = 0; h < 2; ++h) tma_load_4d(st + h * L::HALF + pi * 2048, tm, &full[b], 0, 0, h, plane);
           }
         }
         if (is_k && lane == 0) sstamp(J, 0);
+        // prefetches, each issued right after a sub-chunk's loads so that an in-order stall on
+        // a dependent address never delays a TMA: this unit's second page window, the next
+        // unit's id, then (last sub-chunk, the ring full) its record and first page window
         if (j == 0) {
           pid_nxt = (32 + lane < np) ? __ldg(item_pages + item * cp + 32 + lane) : 0;
-          if (k + 1 < k_end) {
-            const int nitem = sched_units[k + 1] / num_kv_heads;
-            it_n = items[nitem];
-            pid_n0 = lane < cp ? __ldg(item_pages + nitem * cp + lane) : 0;
-          }
+          if (k + 1 < k_end) nunit = sched_units[k + 1];
+        }
+        if (j == nsub - 1 && k + 1 < k_end) {
+          const int nitem = nunit / num_kv_heads;
+          it_n = items[nitem];
+          pid_n0 = lane < cp ? __ldg(item_pages + nitem * cp + lane) : 0;
         }
       }
       it = it_n;
@@ -235,13 +235,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int np = k == k_begin ? it0.n_pages : items[sched_units[k] / num_kv_heads].n_pages;
       const int nsub = (np + SUBP - 1) / SUBP;
       auto issue_s = [&](int Jx, int jx) {
-        const int b = Jx & 1;
-        mbar_wait(&kv_full[b], (Jx >> 1) & 1);
+        const int st = Jx % L::NSTAGE, b = Jx & 1;
+        mbar_wait(&kv_full[st], (Jx / L::NSTAGE) & 1);
         tc_fence_after();
         if (elect_one()) {
           const int keys = min(SUBP, np - jx * SUBP) * 16;
           const uint32_t idesc_s = idesc_bf16_f32(TC_ROWS, (uint32_t)keys);
-          const uint32_t kb = smem_u32(smem + L::STAGE0 + b * L::STAGE_BYTES);
+          const uint32_t kb = smem_u32(smem + L::STAGE0 + st * L::STAGE_BYTES);
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             const uint32_t a = smem_u32(sQ) + (kk >> 2) * (TC_ROWS * 128) + (kk & 3) * 32;
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                         kk > 0 ? 1u : 0u);
           }
           tc_commit(&s_full[b]);
-          tc_commit(&kv_empty[b]);
+          tc_commit(&kv_empty[st]);
           if (jx == nsub - 1) tc_commit(q_free);  // Q may be restaged for the next unit
         }
         __syncwarp();
@@ -260,24 +260,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       issue_s(J, 0);
       for (int j = 0; j < nsub; ++j, ++J) {
         if (j + 1 < nsub) issue_s(J + 1, j + 1);
+        const int st = J % L::NSTAGE;
         mbar_wait(p_full_b[J & 1], (J >> 1) & 1);  // softmax J wrote P and rescaled O
-        mbar_wait(&v_full[J & 1], (J >> 1) & 1);
+        mbar_wait(&v_full[st], (J / L::NSTAGE) & 1);
         tc_fence_after();
         if (elect_one()) {
           const int pn = min(SUBP, np - j * SUBP);
           const uint32_t idesc_o = idesc_bf16_f32(TC_ROWS, 128) | (1u << 16);  // B (V) MN-major
-          const uint32_t vb = smem_u32(smem + L::STAGE0 + (J & 1) * L::STAGE_BYTES) + 2 * L::HALF;
-          const uint32_t pb = smem_u32(smem + L::P_OFF + (J & 1) * L::P_BYTES);
-          for (int kk = 0; kk < pn; ++kk) {  // 16 keys (one page) per instruction
-            const uint32_t a = pb + (kk >> 2) * (TC_ROWS * 128) + (kk & 3) * 32;
-            tc_mma_bf16(tmem_o, sdesc_kmajor_sw128(a), sdesc_mnmajor_sw128(vb + kk * 2048, L::HALF, 1024),
-                        idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
-          }
+          const uint32_t vb = smem_u32(smem + L::STAGE0 + st * L::STAGE_BYTES) + 2 * L::HALF;
+          const uint32_t pt = tmem_base + L::P_COL + (J & 1) * 64;
+          for (int kk = 0; kk < pn; ++kk)  // 16 keys (one page, 8 P columns) per instruction
+            tc_mma_bf16_ts(tmem_o, pt + kk * 8, sdesc_mnmajor_sw128(vb + kk * 2048, L::HALF, 1024),
+                           idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
           sstamp(J, 3);
           tc_commit(o_done);
           if (j == nsub - 1) tc_commit(o_final);
           tc_commit(&p_free[J & 1]);
-          tc_commit(&v_empty[J & 1]);
+          tc_commit(&v_empty[st]);
         }
         __syncwarp();
       }
@@ -296,10 +295,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         rws[m] = (lane + 32 * m < it.n_rows) ? item_rows[it.row_off + lane + 32 * m] : make_int2(0, 0);
       if (n == 0) {
         pdl_wait();  // q comes from the q/k/v GEMM
-        if (lane == 0) {
-          stamp(3);
-          flag_s[0] = ld_acquire(coop);  // generation of the merge counters (after the wait)
-        }
+        if (lane == 0) stamp(3);
       } else {
         mbar_wait(q_free, (n - 1) & 1);  // the previous unit's S MMAs have read Q
       }
@@ -396,34 +392,33 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const float corr = (m_run == -INFINITY) ? 1.f : ex2_approx(m_run - m_new);
         // P buffer b was last read by P.V(J - 2)
         if (J >= 2) mbar_wait(&p_free[b], ((J >> 1) - 1) & 1);
-        uint8_t* rowp0 = smem + L::P_OFF + b * L::P_BYTES + half * (TC_ROWS * 128) + r * 128;
+        tc_fence_after();
+        // this half's 64 keys -> 32 packed bf16x2 columns of TMEM P buffer b
+        const uint32_t pcol = tmem_base + lane_base + L::P_COL + b * 64 + half * 32;
         float ls[4] = {0.f, 0.f, 0.f, 0.f};  // four short row-sum chains instead of two long ones
-        if (nvis > 0) {  // padding rows, rows past their position: P stays zero
+        uint32_t pk[2][16];
+        if (nvis > 0) {  // padding rows, rows past their position: P is zero
           const float nm = -m_new;
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) {
-            if (q4 * 16 < hkeys) {
-              uint32_t pk[8];
 #pragma unroll
-              for (int jj = 0; jj < 16; jj += 2) {
-                // every exponential on the SFU (measured faster than an FMA-pipe share);
-                // masked keys hold -inf: exp2(-inf) = +0
-                const float p0 = ex2_approx(fmaf(__uint_as_float(v[q4][jj]), sl2, nm));
-                const float p1 = ex2_approx(fmaf(__uint_as_float(v[q4][jj + 1]), sl2, nm));
-                ls[(jj >> 1) & 3] += p0 + p1;
-                __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
-                pk[jj >> 1] = *reinterpret_cast<uint32_t*>(&h2);
-              }
-              const int ch = q4 * 2;  // 8-key chunk index within this half's 64-key block
-              *reinterpret_cast<uint4*>(rowp0 + ((ch ^ (r & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-              *reinterpret_cast<uint4*>(rowp0 + (((ch + 1) ^ (r & 7)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+            for (int jj = 0; jj < 16; jj += 2) {
+              // every exponential on the SFU (measured faster than an FMA-pipe share); masked
+              // keys and columns past a short sub-chunk hold -inf: exp2(-inf) = +0
+              const float p0 = ex2_approx(fmaf(__uint_as_float(v[q4][jj]), sl2, nm));
+              const float p1 = ex2_approx(fmaf(__uint_as_float(v[q4][jj + 1]), sl2, nm));
+              ls[(jj >> 1) & 3] += p0 + p1;
+              __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+              pk[q4 >> 1][(q4 & 1) * 8 + (jj >> 1)] = *reinterpret_cast<uint32_t*>(&h2);
             }
           }
-        } else if (valid && hkeys > 0) {
-          // a valid row with no visible key in this half of the sub-chunk: zero its P
+        } else {
 #pragma unroll
-          for (int c = 0; c < 8; ++c)
-            *reinterpret_cast<uint4*>(rowp0 + ((c ^ (r & 7)) << 4)) = make_uint4(0, 0, 0, 0);
+          for (int c = 0; c < 16; ++c) { pk[0][c] = 0u; pk[1][c] = 0u; }
+        }
+        if (hkeys > 0) {  // (columns past the sub-chunk's pages are never read by P.V)
+          tmem_st16(pcol, pk[0]);
+          tmem_st16(pcol + 16, pk[1]);
         }
         l_part = l_part * corr + ((ls[0] + ls[1]) + (ls[2] + ls[3]));
         m_run = m_new;
@@ -442,10 +437,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             for (int jj = 0; jj < 16; ++jj) o[q4][jj] = __float_as_uint(__uint_as_float(o[q4][jj]) * corr);
             tmem_st16(tmem_o + lane_base + half * 64 + q4 * 16, o[q4]);
           }
-          asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
         }
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");  // P (and rescaled O) in TMEM
         tc_fence_before();
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         mbar_arrive(p_full_b[b]);
         if (r == 0 && half == 0) sstamp(J, 2);
       }
@@ -482,40 +476,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<L::TMEM_COLS>(tmem_base);
-  if (diag & 2) return;  // ICR_ATTN_DIAG (timing diagnostics only): no barrier, no merge
-
-  // ---------------- grid barrier + merge (attn_merge.cuh) ----------------
-  // All CTAs are resident (one per SM, grid <= #SMs; dependents launch only after every CTA
-  // has started), so they can wait for each other. Counters: coop[0] generation; per
-  // generation parity {arrived, go} (coop[32 + 64 p], coop[64 + 64 p]). The last to arrive re-arms the other set for the next
-  // launch, bumps the generation and releases everyone; the (row, KV group) merge units are
-  // then split statically, three per CTA round (one per 128-thread group).
   if (threadIdx.x == 0) {
     stamp(9);
-    const int gen = flag_s[0];
-    int* arrived = coop + 32 + (gen & 1) * 64;  // counter and flag on separate 128-byte lines
-    int* go = arrived + 32;
-    const int f = atom_add_acq_rel(arrived, 1);
-    if (f == (int)gridDim.x - 1) {
-      int* other = coop + 32 + ((gen + 1) & 1) * 64;
-      other[0] = 0;
-      other[32] = 0;
-      coop[0] = gen + 1;
-      red_add_release(go, 1);
-    } else {
-      while (ld_acquire(go) == 0) __nanosleep(20);
-    }
-    stamp(10);
+    if (span != nullptr) atomicMax(span + 1, globaltimer());
   }
-  __syncthreads();
-  if (!(diag & 1)) {
-    const int grp = threadIdx.x >> 7, lt = threadIdx.x & 127;
-    const int units = n_rows * num_kv_heads;
-    for (int u = grp * (int)gridDim.x + cta; u < units; u += 3 * (int)gridDim.x)
-      merge_unit<128>(part_o, part_ml, row_pos, row_kind, u / num_kv_heads, u % num_kv_heads,
-                      num_heads, group, max_chunks, chunk_tokens, out, out_ld, lt, 128);
-  }
-  if (threadIdx.x == 0) stamp(11);
 }
 
 cudaError_t attn_tc_partial_launch(const AttnLaunch& a, int /*chunk_pages*/, cudaStream_t s) {
@@ -526,14 +490,12 @@ cudaError_t attn_tc_partial_launch(const AttnLaunch& a, int /*chunk_pages*/, cud
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  static const int diag = getenv("ICR_ATTN_DIAG") ? atoi(getenv("ICR_ATTN_DIAG")) : 0;
   const int units = a.n_items_cap * a.num_kv_heads;
   const int grid = units < a.num_sms ? units : a.num_sms;
   return launch_pdl(attn_tc_kernel, dim3(grid), dim3(TC_THREADS), L::SMEM, s,
                     a.tm_k, a.tm_v, a.q, a.q_ld, a.num_kv_heads, a.group, a.items, a.item_pages,
                     a.item_rows, a.row_pos, a.num_heads, a.max_chunks, a.scale, a.part_o, a.part_ml,
-                    a.sched_off, a.sched_units, a.trace, a.row_kind, a.n_rows, a.chunk_tokens, a.out,
-                    a.out_ld, a.coop, diag);
+                    a.sched_off, a.sched_units, a.trace, a.chunk_tokens, a.span);
 }
 
 }  // namespace icr

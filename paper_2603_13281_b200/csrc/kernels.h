@@ -74,13 +74,13 @@ struct AttnLaunch {
   float* part_o;
   float2* part_ml;
   int* merge_cnt;  // unused (kept for ABI of the test entry)
-  int* coop;       // tcgen05 path: grid-barrier counters [256], zero-initialised, per stream
   CUtensorMap tm_k, tm_v;  // page-arena maps: dims {hd, 16, pages*H_kv}, box {64, 16, 1}, 128B swizzle
   const uint8_t* pf_base;  // L2 prefetch of the next projection's weights (null = none)
   long long pf_bytes;
   __nv_bfloat16* out;
   int out_ld;
   unsigned long long* trace;  // diagnostic per-CTA stamps [2 launches][4096][8] (null = off)
+  unsigned long long* span;   // bench: {min CTA start, max CTA end} %globaltimer (null = off)
 };
 cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t s);
 // tcgen05 partial kernel (attention_tc.cu), head_dim 128, chunks of <= 16 pages.

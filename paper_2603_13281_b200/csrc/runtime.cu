@@ -101,16 +101,18 @@ static icr_status make_map_blocked(CUtensorMap* m, const void* ptr, uint64_t row
   return ICR_OK;
 }
 
-// KV page arena of one layer [planes = pages*H_kv][16][hd] bf16: box {64, 16, 1} = one
-// 128-byte-swizzled half page of one KV head (attention TMA ring).
+// KV page arena of one layer [planes = pages*H_kv][16][hd] bf16, viewed as
+// {64 dims, 16 keys, hd/64 halves, planes} (strides 2*hd B per key, 128 B per half): box
+// {64, 16, 1, 1} = one 64-dim half of a page of one KV head, landing as [key][128 B] with the
+// 128-byte swizzle -- the K-major SW128 layout the MMAs / ldmatrix read.
 static icr_status make_page_map(CUtensorMap* m, const void* ptr, uint64_t planes, uint64_t hd) {
   icr_status st = get_encode();
   if (st) return st;
-  cuuint64_t dims[3] = {hd, 16, planes};
-  cuuint64_t strides[2] = {hd * 2, 16 * hd * 2};
-  cuuint32_t box[3] = {64, 16, 1};
-  cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims,
+  cuuint64_t dims[4] = {64, 16, hd / 64, planes};
+  cuuint64_t strides[3] = {hd * 2, 128, 16 * hd * 2};
+  cuuint32_t box[4] = {64, 16, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims,
                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -340,7 +342,6 @@ struct icr_model {
   float* part_o = nullptr;
   float2* part_ml = nullptr;
   int* merge_cnt = nullptr;
-  int* attn_coop = nullptr;  // in-kernel attention merge counters
   float2* rope = nullptr;
   float* ws = nullptr;
   int* counters = nullptr;
@@ -609,7 +610,6 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
   al.part_o = m->part_o;
   al.part_ml = m->part_ml;
   al.merge_cnt = m->merge_cnt;
-  al.coop = m->attn_coop;
   al.out = m->att;
   al.out_ld = m->q_dim;
 
@@ -883,7 +883,6 @@ icr_status icr_model_create(const icr_model_config* cfg, const icr_layer_weights
   ALLOC(m->part_o, rp * c.num_heads * m->max_chunks * c.head_dim * sizeof(float));
   ALLOC(m->part_ml, rp * c.num_heads * m->max_chunks * sizeof(float2));
   ALLOC(m->merge_cnt, rp * c.num_kv_heads * sizeof(int));
-  ALLOC(m->attn_coop, 256 * sizeof(int));
   ALLOC(m->rope, (size_t)c.max_positions * (c.head_dim / 2) * sizeof(float2));
   ALLOC(m->ws, gemm_ws_floats(m->num_sms) * sizeof(float));
   {
@@ -958,7 +957,7 @@ icr_status icr_model_destroy(icr_model* m) {
   cudaDeviceSynchronize();
   for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
   void* bufs[] = {m->x, m->xb, m->ssq, m->ssq_lm, m->qb, m->att, m->f, m->hlm, m->ubd,
-                  m->tile_best, m->out_tok, m->hid, m->hid_ssq, m->slot_idx, m->part_o, m->part_ml, m->merge_cnt, m->attn_coop, m->rope, m->ws,
+                  m->tile_best, m->out_tok, m->hid, m->hid_ssq, m->slot_idx, m->part_o, m->part_ml, m->merge_cnt, m->rope, m->ws,
                   m->counters, m->sync, m->sh_part, m->sh_cnt, m->meta_dev};
   for (void* p : bufs)
     if (p) cudaFree(p);
@@ -1445,7 +1444,8 @@ icr_status icr_bench_attention(const void* q_dev, const void* k_pages, const voi
                                int n_rows, const int32_t* row_seq_host, const int32_t* row_pos_host,
                                const int32_t* block_table_host, int n_seqs, int max_pages_per_seq,
                                void* out_dev, void* flush_dev, long long flush_bytes, int iters,
-                               int alt_page_offset, float* avg_ms, int32_t* n_items_out, void* stream) {
+                               int alt_page_offset, float* avg_ms, int32_t* n_items_out,
+                               float* span_us, void* stream) {
   if (head_dim != 64 && head_dim != 128) return fail(ICR_CONFIG, "head_dim must be 64 or 128");
   if (alt_page_offset < 0) return fail(ICR_CONFIG, "alt_page_offset must be >= 0");
   cudaStream_t s = (cudaStream_t)stream;
@@ -1473,9 +1473,6 @@ icr_status icr_bench_attention(const void* q_dev, const void* k_pages, const voi
   CUDA_TRY(cudaMalloc(&d_rows, std::max<size_t>(plan.rows.size(), 1) * sizeof(int2)));
   CUDA_TRY(cudaMalloc(&d_po, (size_t)n_rows * num_heads * max_chunks * head_dim * sizeof(float)));
   CUDA_TRY(cudaMalloc(&d_pml, (size_t)n_rows * num_heads * max_chunks * sizeof(float2)));
-  int* d_coop = nullptr;
-  CUDA_TRY(cudaMalloc(&d_coop, 256 * sizeof(int)));
-  CUDA_TRY(cudaMemset(d_coop, 0, 256 * sizeof(int)));
   int* d_sched = nullptr;
   CUDA_TRY(cudaMalloc(&d_sched, (plan.sched_off.size() + plan.sched_units.size()) * sizeof(int)));
   CUDA_TRY(cudaMemcpy(d_sched, plan.sched_off.data(), plan.sched_off.size() * sizeof(int), cudaMemcpyHostToDevice));
@@ -1510,7 +1507,6 @@ icr_status icr_bench_attention(const void* q_dev, const void* k_pages, const voi
   a.scale = (float)(1.0 / std::sqrt((double)head_dim));
   a.part_o = d_po;
   a.part_ml = d_pml;
-  a.coop = d_coop;
   a.sched_off = d_sched;
   a.sched_units = d_sched + plan.sched_off.size();
   a.num_sms = query_sms();
@@ -1527,6 +1523,9 @@ icr_status icr_bench_attention(const void* q_dev, const void* k_pages, const voi
   CUDA_TRY(cudaEventCreate(&e0));
   CUDA_TRY(cudaEventCreate(&e1));
   float total = 0.f;
+  unsigned long long* d_span = nullptr;
+  CUDA_TRY(cudaMalloc(&d_span, 2 * sizeof(unsigned long long)));
+  double span_total = 0.0;
   unsigned long long* tr = nullptr;  // ICR_ATTN_TRACE=path: per-CTA + CTA-0 sub-chunk stamps
   const char* trace_path = getenv("ICR_ATTN_TRACE");
   if (trace_path) {
@@ -1576,6 +1575,10 @@ icr_status icr_bench_attention(const void* q_dev, const void* k_pages, const voi
       cudaMemcpyAsync(d_sched + plan.sched_off.size(), plan.sched_units.data(),
                       plan.sched_units.size() * sizeof(int), cudaMemcpyHostToDevice, s);
     }
+    // kernel span: first partial CTA start -> last partial / merge CTA end (%globaltimer)
+    const unsigned long long span_init[2] = {~0ull, 0ull};
+    cudaMemcpyAsync(d_span, span_init, sizeof(span_init), cudaMemcpyHostToDevice, s);
+    a.span = d_span;
     cudaEventRecord(e0, s);
     if (tr && it == iters - 1) {
       a.trace = tr;
@@ -1584,13 +1587,18 @@ icr_status icr_bench_attention(const void* q_dev, const void* k_pages, const voi
     e = attn_launch(a, s);
     if (tr && it == iters - 1) stamp_kernel<<<1, 1, 0, s>>>(tr + (size_t)3 * 4096 * 16 - 7);
     a.trace = nullptr;
+    a.span = nullptr;
     cudaEventRecord(e1, s);
     cudaEventSynchronize(e1);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e0, e1);
     total += ms;
+    unsigned long long hsp[2];
+    cudaMemcpy(hsp, d_span, sizeof(hsp), cudaMemcpyDeviceToHost);
+    span_total += (hsp[1] > hsp[0]) ? (double)(hsp[1] - hsp[0]) / 1000.0 : 0.0;
   }
   *avg_ms = total / iters;
+  if (span_us) *span_us = alt_page_offset == 0 ? (float)(span_total / iters) : 0.f;
   cudaStreamSynchronize(s);
   if (tr) {
     std::vector<unsigned long long> h((size_t)3 * 4096 * 16);
@@ -1626,7 +1634,7 @@ icr_status icr_bench_attention(const void* q_dev, const void* k_pages, const voi
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  void* bufs[] = {d_pos, d_kind, d_pages, d_n, d_items, d_rows, d_po, d_pml, d_coop, d_sched};
+  void* bufs[] = {d_pos, d_kind, d_pages, d_n, d_items, d_rows, d_po, d_pml, d_sched, d_span};
   for (void* p : bufs) cudaFree(p);
   if (e != cudaSuccess) return fail(ICR_CUDA, "attention bench: %s", cudaGetErrorString(e));
   return ICR_OK;
@@ -1711,7 +1719,7 @@ icr_status icr_paged_attention(const void* q_dev, const void* k_pages, const voi
   CUDA_TRY(cudaMalloc(&d_rows, nr * sizeof(int2)));
   CUDA_TRY(cudaMalloc(&d_po, (size_t)n_rows * num_heads * max_chunks * head_dim * sizeof(float)));
   CUDA_TRY(cudaMalloc(&d_pml, (size_t)n_rows * num_heads * max_chunks * sizeof(float2)));
-  const size_t cnt_n = std::max<size_t>((size_t)n_rows * num_kv_heads, 256);
+  const size_t cnt_n = (size_t)n_rows * num_kv_heads;
   CUDA_TRY(cudaMalloc(&d_cnt, cnt_n * sizeof(int)));
   CUDA_TRY(cudaMemsetAsync(d_cnt, 0, cnt_n * sizeof(int), s));
   CUDA_TRY(cudaMalloc(&d_sched, (plan.sched_off.size() + plan.sched_units.size()) * sizeof(int)));
@@ -1749,7 +1757,6 @@ icr_status icr_paged_attention(const void* q_dev, const void* k_pages, const voi
   a.part_o = d_po;
   a.part_ml = d_pml;
   a.merge_cnt = d_cnt;
-  a.coop = d_cnt;
   a.sched_off = d_sched;
   a.sched_units = d_sched + plan.sched_off.size();
   a.num_sms = query_sms();

@@ -46,21 +46,26 @@ def run(ctx, n_adapters, chunk_pages, iters=5, pipelined=False):
     if pipelined:
         iters = max(iters, 20)
     ms = C.c_float()
+    span = C.c_float()
     nitems = np.zeros(1, np.int32)
     _lib.check(lib.icr_bench_attention(
         q.data_ptr(), kp.data_ptr(), vp.data_ptr(), H, Hkv, hd, chunk_pages, 2 * n_adapters,
         _lib.i32_ptr(rows_seq), _lib.i32_ptr(rows_pos), _lib.i32_ptr(bt), n_adapters, mpps,
         out.data_ptr(), flush.data_ptr() if flush is not None else None,
         flush.numel() if flush is not None else 0, iters, n_pages if pipelined else 0,
-        C.byref(ms), _lib.i32_ptr(nitems),
+        C.byref(ms), _lib.i32_ptr(nitems), C.byref(span),
         _lib.stream_handle()))
     kv_bytes = (ctx + 1) * Hkv * hd * 2 * 2 + (n_adapters - 1) * Hkv * hd * 2 * 2
     gbs = kv_bytes / (ms.value / 1e3) / 1e9
     del kp, vp, flush
     torch.cuda.empty_cache()
-    return {"context": ctx, "adapters": n_adapters, "ms": ms.value, "unique_kv_bytes": kv_bytes,
-            "gbs": gbs, "items": int(nitems[0]), "chunk_pages": chunk_pages,
-            "mode": "pipelined" if pipelined else "cold"}
+    out = {"context": ctx, "adapters": n_adapters, "ms": ms.value, "unique_kv_bytes": kv_bytes,
+           "gbs": gbs, "items": int(nitems[0]), "chunk_pages": chunk_pages,
+           "mode": "pipelined" if pipelined else "cold"}
+    if not pipelined and span.value > 0:
+        out["kernel_span_us"] = span.value
+        out["kernel_span_gbs"] = kv_bytes / (span.value / 1e6) / 1e9
+    return out
 
 
 def main():
