@@ -369,10 +369,12 @@ __global__ void __launch_bounds__(MERGE_THREADS)
   const int cta_id = blockIdx.y * gridDim.x + blockIdx.x;
   if (trace != nullptr && threadIdx.x == 0 && cta_id < 4096) trace[(size_t)cta_id * 16 + 6] = globaltimer();
   pdl_launch();
+  // the row table is uploaded before the forward: read it while the partials run
+  const int kind = row_kind[blockIdx.x], nch = row_pos[blockIdx.x] / chunk_tokens + 1;
   pdl_wait();
   if (trace != nullptr && threadIdx.x == 0 && cta_id < 4096) trace[(size_t)cta_id * 16 + 7] = globaltimer();
-  merge_unit<HD>(part_o, part_ml, row_pos, row_kind, blockIdx.x, blockIdx.y, num_heads, group,
-                 max_chunks, chunk_tokens, out, out_ld, threadIdx.x, blockDim.x);
+  merge_unit<HD>(part_o, part_ml, kind, nch, blockIdx.x, blockIdx.y, num_heads, group, max_chunks,
+                 out, out_ld, threadIdx.x, blockDim.x);
   if (trace != nullptr && threadIdx.x == 0 && cta_id < 4096) trace[(size_t)cta_id * 16 + 5] = globaltimer();
   if (span != nullptr) {
     __syncthreads();

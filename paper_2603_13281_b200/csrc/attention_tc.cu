@@ -92,6 +92,7 @@ __device__ __forceinline__ void cp_async16_s(uint32_t dst, const void* src) {
 // unit's first S MMA overlaps the current unit's softmax tail and epilogue.
 __global__ void __launch_bounds__(TC_THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                   const __grid_constant__ CUtensorMap tm_k8, const __grid_constant__ CUtensorMap tm_v8,
                    const __nv_bfloat16* __restrict__ q, int q_ld, int num_kv_heads, int group,
                    const AttnItem* __restrict__ items, const int* __restrict__ item_pages,
                    const int2* __restrict__ item_rows, const int* __restrict__ row_pos,
@@ -133,6 +134,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if ((smem_u32(tc_smem) & 1023) != 0) __trap();  // SW128 tiles need a 1024-byte base
   pdl_launch();
   const int warp = warp_id(), lane = lane_id();
+  if ((warp == 0 || warp == 2) && lane == 0) {  // descriptor fetches off the critical path
+    tma_prefetch_desc(warp == 0 ? &tm_k8 : &tm_v8);
+    tma_prefetch_desc(warp == 0 ? &tm_k : &tm_v);
+  }
   const int cp = chunk_tokens >> 4;
   // CTA c's first unit is unit c (schedule_units assigns the G longest units to CTAs 0..G-1):
   // its item, page ids and (Q warp) row table are requested right away, together with the
@@ -174,9 +179,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // 32-page window; lane 0 issues the TMAs ------------------------------------------------
     const bool is_k = warp == 0;
     const CUtensorMap* tm = is_k ? &tm_k : &tm_v;
+    const CUtensorMap* tm8 = is_k ? &tm_k8 : &tm_v8;
     uint64_t* full = is_k ? kv_full : v_full;
     uint64_t* empty = is_k ? kv_empty : v_empty;
-    if (lane == 0) tma_prefetch_desc(tm);
     bool waited = false;
     int J = 0;
     AttnItem it = it0;
@@ -197,16 +202,32 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
         uint8_t* st = smem + L::STAGE0 + b * L::STAGE_BYTES + (is_k ? 0 : 2 * L::HALF);
         if (lane == 0) mbar_expect_tx(&full[b], (uint32_t)pn * 2 * 2048);
-        for (int pi = 0; pi < pn; ++pi) {
-          if (!waited && p0 + pi >= it.n_pre) {
+        // a full sub-chunk of consecutive page ids (sequentially allocated prompts) is ONE
+        // 32 KB TMA; otherwise one TMA per 64-dim half page
+        const int w0 = p0 & 31;
+        const int first = __shfl_sync(0xffffffffu, pid_cur, w0);
+        const bool run = pn == SUBP &&
+            __ballot_sync(0xffffffffu, lane >= w0 && lane < w0 + SUBP && pid_cur == first + (lane - w0)) ==
+                (0xffu << w0);
+        if (run) {
+          if (!waited && p0 + SUBP > it.n_pre) {
             pdl_wait();
             if (is_k && lane == 0) stamp(7);
             waited = true;
           }
-          const int plane = __shfl_sync(0xffffffffu, pid_cur, (p0 + pi) & 31) * num_kv_heads + g;
-          if (lane == 0) {
+          if (lane == 0) tma_load_5d(st, tm8, &full[b], 0, 0, first, 0, g);
+        } else {
+          for (int pi = 0; pi < pn; ++pi) {
+            if (!waited && p0 + pi >= it.n_pre) {
+              pdl_wait();
+              if (is_k && lane == 0) stamp(7);
+              waited = true;
+            }
+            const int plane = __shfl_sync(0xffffffffu, pid_cur, (p0 + pi) & 31) * num_kv_heads + g;
+            if (lane == 0) {
 #pragma unroll
-            for (int h = 0; h < 2; ++h) tma_load_4d(st + h * L::HALF + pi * 2048, tm, &full[b], 0, 0, h, plane);
+              for (int h = 0; h < 2; ++h) tma_load_4d(st + h * L::HALF + pi * 2048, tm, &full[b], 0, 0, h, plane);
+            }
           }
         }
         if (is_k && lane == 0) sstamp(J, 0);
@@ -493,7 +514,7 @@ cudaError_t attn_tc_partial_launch(const AttnLaunch& a, int /*chunk_pages*/, cud
   const int units = a.n_items_cap * a.num_kv_heads;
   const int grid = units < a.num_sms ? units : a.num_sms;
   return launch_pdl(attn_tc_kernel, dim3(grid), dim3(TC_THREADS), L::SMEM, s,
-                    a.tm_k, a.tm_v, a.q, a.q_ld, a.num_kv_heads, a.group, a.items, a.item_pages,
+                    a.tm_k, a.tm_v, a.tm_k8, a.tm_v8, a.q, a.q_ld, a.num_kv_heads, a.group, a.items, a.item_pages,
                     a.item_rows, a.row_pos, a.num_heads, a.max_chunks, a.scale, a.part_o, a.part_ml,
                     a.sched_off, a.sched_units, a.trace, a.chunk_tokens, a.span);
 }

@@ -88,16 +88,14 @@ __device__ __forceinline__ void merge_slice4(const float* __restrict__ part_o,
 
 // The merge of one (row r, KV group g) unit by `nthr` threads (thread lt): every head of the
 // group, HD / 4 threads per head. Padding rows (kind < 0) have no output.
+// (kind, nch = chunks of the row) come from the row table, which the caller may read early.
 template <int HD>
 __device__ __forceinline__ void merge_unit(const float* __restrict__ part_o,
-                                           const float2* __restrict__ part_ml,
-                                           const int* __restrict__ row_pos,
-                                           const int* __restrict__ row_kind, int r, int g,
-                                           int num_heads, int group, int max_chunks,
-                                           int chunk_tokens, __nv_bfloat16* __restrict__ out,
-                                           int out_ld, int lt, int nthr) {
-  if (row_kind[r] < 0) return;
-  const int nch = row_pos[r] / chunk_tokens + 1;
+                                           const float2* __restrict__ part_ml, int kind, int nch,
+                                           int r, int g, int num_heads, int group, int max_chunks,
+                                           __nv_bfloat16* __restrict__ out, int out_ld, int lt,
+                                           int nthr) {
+  if (kind < 0) return;
   constexpr int V = HD / 4;
   for (int idx = lt; idx < group * V; idx += nthr) {
     const int hg = idx / V, d = (idx % V) * 4;

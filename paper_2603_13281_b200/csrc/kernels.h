@@ -74,7 +74,9 @@ struct AttnLaunch {
   float* part_o;
   float2* part_ml;
   int* merge_cnt;  // unused (kept for ABI of the test entry)
-  CUtensorMap tm_k, tm_v;  // page-arena maps: dims {hd, 16, pages*H_kv}, box {64, 16, 1}, 128B swizzle
+  CUtensorMap tm_k, tm_v;  // page-arena maps: one 64-dim half page of one KV head per box
+  CUtensorMap tm_k8, tm_v8;  // the same arena as runs: 8 consecutive page ids of one KV head,
+                             // both halves, in one box (32 KB, [half][page][key][128 B])
   const uint8_t* pf_base;  // L2 prefetch of the next projection's weights (null = none)
   long long pf_bytes;
   __nv_bfloat16* out;

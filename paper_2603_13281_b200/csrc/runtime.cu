@@ -122,6 +122,28 @@ static icr_status make_page_map(CUtensorMap* m, const void* ptr, uint64_t planes
   return ICR_OK;
 }
 
+// The same arena as runs of SUBP = 8 consecutive page ids of one KV head: dims {64 dims,
+// 16 keys, pages (stride H_kv * 16 * hd * 2), hd/64 halves (stride 128 B), H_kv heads
+// (stride 16 * hd * 2)}, box {64, 16, 8, hd/64, 1} = 32 KB landing as [half][page][key][128 B]
+// -- exactly the tcgen05 attention's K / V stage layout. One TMA per sub-chunk instead of 16.
+static icr_status make_page_run_map(CUtensorMap* m, const void* ptr, uint64_t pages, uint64_t hkv,
+                                    uint64_t hd) {
+  icr_status st = get_encode();
+  if (st) return st;
+  cuuint64_t dims[5] = {64, 16, pages, hd / 64, hkv};
+  cuuint64_t strides[4] = {hd * 2, hkv * 16 * hd * 2, 128, 16 * hd * 2};
+  cuuint32_t box[5] = {64, 16, 8, (cuuint32_t)(hd / 64), 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(ptr), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(ICR_CUDA, "cuTensorMapEncodeTiled (page runs) failed (%d) pages=%llu", (int)r,
+                (unsigned long long)pages);
+  return ICR_OK;
+}
+
 static int nt_index(int nt) {
   switch (nt) {
     case 16: return 0;
@@ -302,6 +324,7 @@ struct LayerMaps {
   CUtensorMap qkv, o, gu, down;          // base weights (tile-major)
   CUtensorMap lb_q, lb_o, lb_gu, lb_down;  // LoRA B_cat (tile-major), when lora_rank > 0
   CUtensorMap kpg, vpg;                    // this layer's K / V page arenas (attention TMA)
+  CUtensorMap kpg8, vpg8;                  // the same as 8-page runs
 };
 
 struct GraphKey {
@@ -661,6 +684,8 @@ static icr_status enqueue_forward(icr_model* m, const Meta& mt, float* logits_de
     al.v_pages = (const __nv_bfloat16*)w.v_pages;
     al.tm_k = lm.kpg;
     al.tm_v = lm.vpg;
+    al.tm_k8 = lm.kpg8;
+    al.tm_v8 = lm.vpg8;
     al.pf_base = pf_on ? (const uint8_t*)w.w_o : nullptr;
     al.pf_bytes = (long long)d * m->q_dim * 2;
     {  // attention over 2H heads (src/model.py:497-501)
@@ -929,6 +954,8 @@ icr_status icr_model_create(const icr_model_config* cfg, const icr_layer_weights
     if ((st = make_map_blocked(&m->maps[l].down, w.w_down, c.hidden_dim, c.ffn_dim))) return bail(st);
     if ((st = make_page_map(&m->maps[l].kpg, w.k_pages, (uint64_t)c.num_pages * c.num_kv_heads, c.head_dim))) return bail(st);
     if ((st = make_page_map(&m->maps[l].vpg, w.v_pages, (uint64_t)c.num_pages * c.num_kv_heads, c.head_dim))) return bail(st);
+    if ((st = make_page_run_map(&m->maps[l].kpg8, w.k_pages, c.num_pages, c.num_kv_heads, c.head_dim))) return bail(st);
+    if ((st = make_page_run_map(&m->maps[l].vpg8, w.v_pages, c.num_pages, c.num_kv_heads, c.head_dim))) return bail(st);
     if (c.lora_rank > 0) {
       if ((st = make_map_blocked(&m->maps[l].lb_q, w.b_q, q_dim + 2 * kv_dim, m->lc1 * 64))) return bail(st);
       if ((st = make_map_blocked(&m->maps[l].lb_o, w.b_o, c.hidden_dim, m->lc1 * 64))) return bail(st);
@@ -1518,6 +1545,8 @@ icr_status icr_bench_attention(const void* q_dev, const void* k_pages, const voi
     const uint64_t planes = (uint64_t)(maxpage + 1 + alt_page_offset) * num_kv_heads;
     if ((st = make_page_map(&a.tm_k, k_pages, planes, head_dim))) return st;
     if ((st = make_page_map(&a.tm_v, v_pages, planes, head_dim))) return st;
+    if ((st = make_page_run_map(&a.tm_k8, k_pages, maxpage + 1 + alt_page_offset, num_kv_heads, head_dim))) return st;
+    if ((st = make_page_run_map(&a.tm_v8, v_pages, maxpage + 1 + alt_page_offset, num_kv_heads, head_dim))) return st;
   }
   cudaEvent_t e0, e1;
   CUDA_TRY(cudaEventCreate(&e0));
@@ -1766,6 +1795,8 @@ icr_status icr_paged_attention(const void* q_dev, const void* k_pages, const voi
     const uint64_t planes = (uint64_t)(maxpage + 1) * num_kv_heads;
     if ((st = make_page_map(&a.tm_k, k_pages, planes, head_dim))) return st;
     if ((st = make_page_map(&a.tm_v, v_pages, planes, head_dim))) return st;
+    if ((st = make_page_run_map(&a.tm_k8, k_pages, maxpage + 1, num_kv_heads, head_dim))) return st;
+    if ((st = make_page_run_map(&a.tm_v8, v_pages, maxpage + 1, num_kv_heads, head_dim))) return st;
   }
   a.out = (__nv_bfloat16*)out_dev;
   a.out_ld = num_heads * head_dim;

@@ -49,8 +49,10 @@ def main():
     print("  first 4 / last 4 CTAs by entry (entry, end):",
           [(round(part[i, 6], 2), round(part[i, 5], 2)) for i in list(order[:4]) + list(order[-4:])])
     if len(merge):
-        print(f"merge CTAs {len(merge)}: entry min {merge[:, 6].min():.2f} "
-              f"end max {merge[:, 5].max():.2f}")
+        w = merge[:, 7][merge[:, 7] >= 0]
+        print(f"merge CTAs {len(merge)}: entry min {merge[:, 6].min():.2f}, past the PDL wait "
+              f"min {w.min():.2f} med {np.median(w):.2f}, end med {np.median(merge[:, 5]):.2f} "
+              f"max {merge[:, 5].max():.2f}")
     if sub:
         print("CTA-0 sub-chunks: j, K issued, S done, P written, PV issued, S->regs, max, pfree, softmax cycles")
         for l in sub[:20]:
