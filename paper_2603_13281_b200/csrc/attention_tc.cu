@@ -417,29 +417,31 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         // this half's 64 keys -> 32 packed bf16x2 columns of TMEM P buffer b
         const uint32_t pcol = tmem_base + lane_base + L::P_COL + b * 64 + half * 32;
         float ls[4] = {0.f, 0.f, 0.f, 0.f};  // four short row-sum chains instead of two long ones
-        uint32_t pk[2][16];
-        if (nvis > 0) {  // padding rows, rows past their position: P is zero
-          const float nm = -m_new;
+        const float nm = -m_new;
 #pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) {
+        for (int hb = 0; hb < 2; ++hb) {  // 32 keys -> 16 packed columns, stored at once
+          uint32_t pk[16];
+          if (nvis > 0) {  // padding rows, rows past their position: P is zero
 #pragma unroll
-            for (int jj = 0; jj < 16; jj += 2) {
-              // every exponential on the SFU (measured faster than an FMA-pipe share); masked
-              // keys and columns past a short sub-chunk hold -inf: exp2(-inf) = +0
-              const float p0 = ex2_approx(fmaf(__uint_as_float(v[q4][jj]), sl2, nm));
-              const float p1 = ex2_approx(fmaf(__uint_as_float(v[q4][jj + 1]), sl2, nm));
-              ls[(jj >> 1) & 3] += p0 + p1;
-              __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
-              pk[q4 >> 1][(q4 & 1) * 8 + (jj >> 1)] = *reinterpret_cast<uint32_t*>(&h2);
+            for (int q = 0; q < 2; ++q) {
+              const int q4 = hb * 2 + q;
+#pragma unroll
+              for (int jj = 0; jj < 16; jj += 2) {
+                // every exponential on the SFU (measured faster than an FMA-pipe share); masked
+                // keys and columns past a short sub-chunk hold -inf: exp2(-inf) = +0
+                const float p0 = ex2_approx(fmaf(__uint_as_float(v[q4][jj]), sl2, nm));
+                const float p1 = ex2_approx(fmaf(__uint_as_float(v[q4][jj + 1]), sl2, nm));
+                ls[(jj >> 1) & 3] += p0 + p1;
+                __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+                pk[q * 8 + (jj >> 1)] = *reinterpret_cast<uint32_t*>(&h2);
+              }
             }
-          }
-        } else {
+          } else {
 #pragma unroll
-          for (int c = 0; c < 16; ++c) { pk[0][c] = 0u; pk[1][c] = 0u; }
-        }
-        if (hkeys > 0) {  // (columns past the sub-chunk's pages are never read by P.V)
-          tmem_st16(pcol, pk[0]);
-          tmem_st16(pcol + 16, pk[1]);
+            for (int c = 0; c < 16; ++c) pk[c] = 0u;
+          }
+          // (columns past the sub-chunk's pages are never read by P.V)
+          if (hkeys > 0) tmem_st16(pcol + hb * 16, pk);
         }
         l_part = l_part * corr + ((ls[0] + ls[1]) + (ls[2] + ls[3]));
         m_run = m_new;
