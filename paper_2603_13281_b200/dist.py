@@ -65,6 +65,17 @@ def max_over_ranks(value: float, device=None) -> float:
     return float(t.item())
 
 
+def sum_over_ranks(value: float, device=None) -> float:
+    """Sum of a scalar over all ranks (whole-job totals: tokens, steps)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
 def p95_nearest_rank(latencies: Sequence[float]) -> float:
     """Nearest-rank P95 exactly as the reference computes it (src/simulate.py:226-231)."""
     if not latencies:
