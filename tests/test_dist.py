@@ -30,7 +30,8 @@ def _worker(rank, world, port, q):
         p95 = D.global_p95(lat)
         prompts = [[7] * 32] * 6 + [[9] * 32] * 2
         mine = D.shard(list(range(8)), world, rank, prompts)
-        q.put((rank, t, p95, mine))
+        total = D.sum_over_ranks(float(len(mine)))        # whole-job token / step totals (C5)
+        q.put((rank, t, p95, mine, total))
     finally:
         dist.destroy_process_group()
 
@@ -47,10 +48,11 @@ def test_two_rank_timing_and_p95_over_gloo():
         p.join(timeout=60)
         assert p.exitcode == 0
     all_lat = [float(r * 100 + i) for r in range(2) for i in range(20)]
-    for rank, t, p95, mine in res:
+    for rank, t, p95, mine, total in res:
         assert t == 2.5                                   # max over ranks
+        assert total == 8.0                               # sum over ranks
         assert p95 == D.p95_nearest_rank(all_lat) == 117.0  # rank ceil(0.95*40)=38
-    shards = [set(m) for _, _, _, m in res]
+    shards = [set(m) for _, _, _, m, _ in res]
     assert shards[0].isdisjoint(shards[1]) and shards[0] | shards[1] == set(range(8))
     assert len(shards[0]) == len(shards[1]) == 4       # weak scaling: equal per-GPU work
 
@@ -80,3 +82,33 @@ def test_prefix_key_uses_first_block_chain_hash():
     toks = list(range(40))
     assert D.prefix_key(toks) == chain_hash(0, tuple(range(16)))
     assert D.prefix_key(toks[:10]) == 0
+
+
+def test_bench_gpus_flag_relaunches_one_rank_per_gpu(monkeypatch):
+    """`bench.py --gpus N` without a torchrun environment re-launches itself under
+    torch.distributed.run with N processes on 127.0.0.1 (--gpus was ignored)."""
+    import subprocess
+    import sys
+
+    import bench
+    seen = {}
+
+    def fake_call(cmd):
+        seen["cmd"] = cmd
+        return 0
+
+    monkeypatch.setattr(subprocess, "call", fake_call)
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "8"])
+    with pytest.raises(SystemExit) as ex:
+        bench.main()
+    assert ex.value.code == 0
+    cmd = seen["cmd"]
+    assert cmd[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"]
+    assert "--nproc-per-node=4" in cmd and "127.0.0.1" in cmd
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "8"]
+    # under torchrun a disagreeing --gpus is an error, not a silent single rank
+    monkeypatch.setenv("WORLD_SIZE", "2")
+    with pytest.raises(SystemExit) as ex2:
+        bench.main()
+    assert "disagrees" in str(ex2.value.code)
