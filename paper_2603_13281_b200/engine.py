@@ -247,6 +247,9 @@ def _prefill_setup(sessions, prompts, pool, namespace, readers, rt):
     ledger; returns the suffix rows (session index, token, position, emit) and the first
     tokens of fully pooled prompts."""
     readers = list(readers) if readers is not None else [None] * len(sessions)
+    # one namespace for all, or one per session (the reference's baseline mode serves each
+    # agent from its own namespace, src/simulate.py:313)
+    spaces = list(namespace) if isinstance(namespace, (list, tuple)) else [namespace] * len(sessions)
     firsts: list = [None] * len(sessions)
     rows = []
     for i, (session, prompt) in enumerate(zip(sessions, prompts)):
@@ -259,7 +262,7 @@ def _prefill_setup(sessions, prompts, pool, namespace, readers, rt):
             raise CapacityError(f"prompt length {len(toks)} exceeds max context {session.max_context}")
         matched, chain = 0, []
         if pool is not None:
-            matched, chain = pool.lookup(namespace, toks, reader=readers[i])
+            matched, chain = pool.lookup(spaces[i], toks, reader=readers[i])
             if chain:
                 if any(b.arena is not rt.arena for b in chain):
                     pool.release(chain)

@@ -140,9 +140,12 @@ class _Live:
 
 
 def serve(base, adapters: Sequence, pool, prefix: Sequence[int], reqs: Sequence[Request],
-          cfg: WorkflowConfig, max_context: int, runtime=None) -> ServeReport:
+          cfg: WorkflowConfig, max_context: int, runtime=None, ledger=None) -> ServeReport:
     """Continuous-batching multi-agent serving; returns a ServeReport. All requests are present
-    at t = 0 (closed batch); the shared prefix must already be committed in `pool`."""
+    at t = 0 (closed batch); the shared prefix must already be committed in `pool`. `ledger`
+    (optional) is shared by every session, as the reference's run() shares one
+    (src/simulate.py:277, 318-319). In a "baseline"-mode pool every agent reads and commits
+    in its own namespace (src/simulate.py:313)."""
     rep = ServeReport()
     stats0 = pool.stats()
     live: list[_Live] = []
@@ -151,21 +154,25 @@ def serve(base, adapters: Sequence, pool, prefix: Sequence[int], reqs: Sequence[
     next_turn = {r.rid: 0 for r in reqs}
     t0 = time.perf_counter()
 
+    def space(agent: int):
+        return f"agent{agent}" if pool.mode == "baseline" else None
+
     def open_turns(reqs_: list) -> list:
         """Open the next turn of each request (sessions not yet prefilled)."""
         out = []
         for req in reqs_:
             turn = req.turns[next_turn[req.rid]]
             ctx = contexts[req.rid] + list(turn.new_tokens)
-            s = E.new_session(base, adapters[turn.agent], max_context, runtime=runtime)
+            s = E.new_session(base, adapters[turn.agent], max_context, runtime=runtime,
+                              ledger=ledger)
             out.append(_Live(req, next_turn[req.rid], ctx, s, []))
         return out
 
     def finish_turn(lv: _Live) -> None:
         s, turn = lv.session, lv.req.turns[lv.turn]
         covered = lv.context + lv.out[:-1]   # the last emitted token has no KV yet
-        pool.commit(None, covered, s.cache, next_token_fn=lambda p: E.base_next_token_at(s, p),
-                    creator=f"agent{turn.agent}")
+        pool.commit(space(turn.agent), covered, s.cache,
+                    next_token_fn=lambda p: E.base_next_token_at(s, p), creator=f"agent{turn.agent}")
         if s.borrowed_chain:
             pool.release(s.borrowed_chain)
             s.borrowed_chain = []
@@ -193,7 +200,8 @@ def serve(base, adapters: Sequence, pool, prefix: Sequence[int], reqs: Sequence[
             # forward (engine.step_batch): the base weights stream once for both
             nxt, firsts = E.step_batch([lv.session for lv in active], [lv.out[-1] for lv in active],
                                        [lv.session for lv in new], [lv.context for lv in new],
-                                       pool=pool, namespace=None,
+                                       pool=pool,
+                                       namespace=[space(lv.req.turns[lv.turn].agent) for lv in new],
                                        readers=[f"agent{lv.req.turns[lv.turn].agent}" for lv in new])
             if active:
                 rep.decode_steps += 1
