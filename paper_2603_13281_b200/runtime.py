@@ -49,6 +49,7 @@ class PageArena:
         self.refs = np.zeros(num_pages, dtype=np.int32)
         self.gen = np.zeros(num_pages, dtype=np.int64)  # bumped per allocation: page identity
         self._free = list(range(num_pages - 1, -1, -1))
+        self._reclaimers: list = []  # weak refs to prefix pools holding pages of this arena
 
     @classmethod
     def host_only(cls, config: ModelConfig, pages: int) -> "PageArena":
@@ -65,7 +66,20 @@ class PageArena:
     def free_pages(self) -> int:
         return len(self._free)
 
+    def register_reclaimer(self, pool) -> None:
+        """A prefix pool that holds page references here: when the arena runs dry, its
+        unpinned blocks are evicted (LRU) before allocation fails -- the device pages, not
+        only the pool's byte budget, bound what the pool may keep."""
+        import weakref
+        if not any(r() is pool for r in self._reclaimers):
+            self._reclaimers.append(weakref.ref(pool))
+
     def alloc(self) -> int:
+        if not self._free:
+            for ref in list(self._reclaimers):
+                pool = ref()
+                if pool is not None and not self._free:
+                    pool.reclaim_pages(self, 1)
         if not self._free:
             raise CapacityError(f"KV page arena exhausted ({self.num_pages} pages)")
         pid = self._free.pop()
@@ -290,6 +304,9 @@ class AdapterSlots:
         self._refs: list = [None] * slots
 
     def slot_of(self, adapter: AdapterSet) -> int:
+        """The adapter's resident slot (uploaded on first use). Served adapters are treated as
+        immutable: after changing an adapter's weights in place, call `release(adapter)` so
+        the next use uploads the new values."""
         key = id(adapter)
         if key in self._owner:
             return self._owner[key]
@@ -313,12 +330,18 @@ class AdapterSlots:
         bt = self.b[key][layer]                           # [Mt, Kt, 128, 64]
         view = bt.permute(0, 2, 1, 3)                     # [Mt, 128, Kt, 64] logical (m, k)
         col = target * self.n * r + s * r
-        kt, kin = col // 64, col % 64
         Mt = bt.shape[0]
         full = torch.zeros(Mt * 128, r, dtype=torch.bfloat16, device=self.device)
         vv = value.to(self.device, torch.bfloat16)
         full[rows, :vv.shape[1]] = vv
-        view[:, :, kt, kin:kin + r] = full.view(Mt, 128, r)
+        full = full.view(Mt, 128, r)
+        # the slot's r columns may straddle a 64-column block (rank 24, slot >= 2)
+        j = 0
+        while j < r:
+            kt, kin = (col + j) // 64, (col + j) % 64
+            w = min(r - j, 64 - kin)
+            view[:, :, kt, kin:kin + w] = full[:, :, j:j + w]
+            j += w
 
     def _upload(self, s: int, ad: AdapterSet) -> None:
         torch = _torch()

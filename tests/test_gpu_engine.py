@@ -532,3 +532,30 @@ def test_over_256_row_adapted_batch_equals_single_session_steps(c1_setup):
             assert s.last_logits.tobytes() == want[i][1][step], f"session {i} step {step}"
     for s in batch:
         s.close()
+
+
+def test_rank24_adapters_in_straddling_slots_match_oracle(cuda):
+    """lora_rank 24 puts slot 2's columns across a 64-column block of the B_cat operand
+    (the upload crashed); three rank-24 adapters decoding side by side match the
+    oracle within the bf16 band."""
+    E, P, M = _mods()
+    from paper_2603_13281_b200.runtime import Runtime
+    shape = O.Shape(**C1)
+    w = O.bf16_weights(O.init_base(shape, 0))
+    base = base_from_oracle(C1, w)
+    raw = [O.bf16_adapter(a) for a in O.make_agents(shape, 3, seed=5, rank=24, alpha=48.0)]
+    ads = [adapter_from_oracle(base.config, a, f"r24_{i}") for i, a in enumerate(raw)]
+    rt = Runtime(base, max_seqs=6, max_context=128, max_rows=64, adapter_slots=3, lora_rank=24)
+    prompt = [int(t) for t in np.random.default_rng(8).integers(1, 1024, 24)]
+    sess = [E.new_session(base, a, 96, runtime=rt, capture_logits=True) for a in ads]
+    assert [s.adapter_slot for s in sess] == [0, 1, 2]
+    refs = [O.Session(shape, w, a) for a in raw]
+    toks = [E.prefill(s, prompt) for s in sess]
+    assert toks == [r.prefill(prompt) for r in refs]
+    for step in range(4):
+        E.decode_step_batch(sess, toks)
+        toks = [r.decode_fused(t) for r, t in zip(refs, toks)]
+        for i, (s, r) in enumerate(zip(sess, refs)):
+            _check_logits(s.last_logits, r.last_logits, f"rank24 slot {i} step {step}")
+    for s in sess:
+        s.close()
