@@ -185,6 +185,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     bool waited = false;
     int J = 0;
     AttnItem it = it0;
+    // K/V stream through L2 once per launch: evict first, so the partials written by the
+    // units that finish early (read back by the merge) are not pushed out by the stream
+    const uint64_t pol = policy_evict_first();
     int pid_cur = pid0;
     for (int k = k_begin; k < k_end; ++k) {
       const int unit = k == k_begin ? cta : sched_units[k];
@@ -215,7 +218,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             if (is_k && lane == 0) stamp(7);
             waited = true;
           }
-          if (lane == 0) tma_load_5d(st, tm8, &full[b], 0, 0, first, 0, g);
+          if (lane == 0) tma_load_5d_hint(st, tm8, &full[b], 0, 0, first, 0, g, pol);
         } else {
           for (int pi = 0; pi < pn; ++pi) {
             if (!waited && p0 + pi >= it.n_pre) {
@@ -226,7 +229,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const int plane = __shfl_sync(0xffffffffu, pid_cur, (p0 + pi) & 31) * num_kv_heads + g;
             if (lane == 0) {
 #pragma unroll
-              for (int h = 0; h < 2; ++h) tma_load_4d(st + h * L::HALF + pi * 2048, tm, &full[b], 0, 0, h, plane);
+              for (int h = 0; h < 2; ++h)
+                tma_load_4d_hint(st + h * L::HALF + pi * 2048, tm, &full[b], 0, 0, h, plane, pol);
             }
           }
         }
