@@ -40,8 +40,9 @@ struct TcLayout {
   static constexpr int NSTAGE = 3;                         // K/V sub-chunks in flight
   static constexpr uint32_t BAR_OFF = STAGE0 + NSTAGE * STAGE_BYTES;
   static constexpr uint32_t RED_OFF = BAR_OFF + 256;       // float [2 halves][128]
-  // 230,656 B: within the opt-in maximum of 232,448 less the 1 KB the driver reserves
-  static constexpr size_t SMEM = RED_OFF + 256 * 4;
+  static constexpr uint32_t MROW_OFF = RED_OFF + 256 * 4;  // float [128]: row max of the unit
+  // 231,168 B: within the opt-in maximum of 232,448 less the 1 KB the driver reserves
+  static constexpr size_t SMEM = MROW_OFF + 128 * 4;
   // TMEM columns: S0 [0,128) S1 [128,256) O [256,384) P0 [384,448) P1 [448,512) -- P (bf16
   // pairs packed in 32-bit columns) is the A operand of P.V straight from TMEM, so shared
   // memory holds Q and three K/V stages
@@ -90,6 +91,7 @@ __device__ __forceinline__ void cp_async16_s(uint32_t dst, const void* src) {
 // Across units the K/V producers run ahead into the next unit's pages, the Q warp stages the
 // next unit's queries as soon as the last S MMA of the current one has read Q, and the next
 // unit's first S MMA overlaps the current unit's softmax tail and epilogue.
+template <bool kNarrow>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                    const __grid_constant__ CUtensorMap tm_k8, const __grid_constant__ CUtensorMap tm_v8,
@@ -109,7 +111,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t* kv_full = bars + 20;  // [3] K landed
   uint64_t* kv_empty = bars + 23; // [3] K consumed by S
   uint64_t* s_full = bars + 5;    // [2]
-  uint64_t* p_full_b[2] = {bars + 7, bars + 17};  // P(J) written (+ O rescaled), per buffer
+  // P(J) written (+ O rescaled): bars[7] for P buffer 0, bars[17] for buffer 1
   uint64_t* o_done = bars + 8;    // one phase per P.V (the lazy rescale waits on it)
   uint64_t* p_free = bars + 9;    // [2]: TMEM P buffer b consumed by its P.V
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
@@ -118,6 +120,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t* o_final = bars + 16;  // the unit's last P.V landed (phase n)
   uint64_t* q_free = bars + 18;   // the unit's last S MMA has read Q (phase n)
   float* red = reinterpret_cast<float*>(smem + L::RED_OFF);
+  float* mrow = reinterpret_cast<float*>(smem + L::MROW_OFF);
 
   const int cta = blockIdx.x;
   auto stamp = [&](int k) {
@@ -156,8 +159,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_init(&v_empty[b], 1);
     }
     for (int b = 0; b < 2; ++b) mbar_init(&s_full[b], 1);
-    mbar_init(p_full_b[0], 256);
-    mbar_init(p_full_b[1], 256);
+    mbar_init(bars + 7, 256);
+    mbar_init(bars + 17, 256);
     mbar_init(o_done, 1);
     mbar_init(o_final, 1);
     mbar_init(q_free, 1);
@@ -286,7 +289,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int j = 0; j < nsub; ++j, ++J) {
         if (j + 1 < nsub) issue_s(J + 1, j + 1);
         const int st = J % L::NSTAGE;
-        mbar_wait(p_full_b[J & 1], (J >> 1) & 1);  // softmax J wrote P and rescaled O
+        mbar_wait((bars + ((J & 1) ? 17 : 7)), (J >> 1) & 1);  // softmax J wrote P and rescaled O
         mbar_wait(&v_full[st], (J / L::NSTAGE) & 1);
         tc_fence_after();
         if (elect_one()) {
@@ -369,115 +372,248 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         slot = ((size_t)rr.x * num_heads + g * group + rr.y) * max_chunks + it.chunk_idx;
       }
       float m_run = -INFINITY, l_part = 0.f;
-      for (int j = 0; j < nsub; ++j, ++J) {
-        const int b = J & 1;
-        const int keys = min(SUBP, np - j * SUBP) * 16;
-        const int kbase = it.chunk_start + j * SUBP * 16 + half * 64;
-        const int hkeys = min(64, keys - half * 64);  // this half's columns (may be <= 0)
-        mbar_wait(&s_full[b], (J >> 1) & 1);
-        tc_fence_after();
-        if (r == 0 && half == 0) sstamp(J, 1);
-        if (r == 0 && half == 0 && J == 0) stamp(2);
-        uint32_t v[4][16];  // raw q.k of this half's (<= 64) keys
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4)
-          if (q4 * 16 < hkeys) tmem_ld16_nowait(tmem_base + b * 128 + lane_base + half * 64 + q4 * 16, v[q4]);
-        tmem_wait_ld();
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) tmem_reg_fence(v[q4]);
-        // visible keys of this half: [kbase, kbase + nvis); max of raw scores x sl2 (> 0)
-        // equals the max of the scaled scores (rounding is monotonic)
-        const int nvis = valid ? max(0, min(hkeys, pos + 1 - kbase)) : 0;
-        if (nvis > 0 && nvis < 64) {
-          // rare (the row's causal edge or a short last sub-chunk): invisible keys become
-          // -inf once, so the max and exp loops below carry no per-key predicates
-          asm volatile("" ::: "memory");
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4)
-#pragma unroll
-            for (int jj = 0; jj < 16; ++jj)
-              if (q4 * 16 + jj >= nvis) v[q4][jj] = 0xff800000u;  // -inf
-        }
-        float mx = -INFINITY;
-        if (nvis > 0) {
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4)
-#pragma unroll
-            for (int jj = 0; jj < 16; ++jj) mx = fmaxf(mx, __uint_as_float(v[q4][jj]));
-        }
-        // exchange with the partner thread (same row, other half); the second barrier lets
-        // the buffer be rewritten next iteration
-        red[half * 128 + r] = mx;
-        named_bar_sync(1 + quarter, 64);
-        const float m_cand = fmaxf(m_run, __fmul_rn(fmaxf(red[r], red[128 + r]), sl2));
-        named_bar_sync(1 + quarter, 64);
-        // lazy max: keep the reference while the new scores stay within 2^8 of it (P <= 256
-        // is exact enough in bf16 / fp32), so O is rescaled only when the max jumps
-        const float m_new = (m_cand > m_run + 8.f) ? m_cand : m_run;
-        const float corr = (m_run == -INFINITY) ? 1.f : ex2_approx(m_run - m_new);
-        // P buffer b was last read by P.V(J - 2)
-        if (J >= 2) mbar_wait(&p_free[b], ((J >> 1) - 1) & 1);
-        tc_fence_after();
-        // this half's 64 keys -> 32 packed bf16x2 columns of TMEM P buffer b
-        const uint32_t pcol = tmem_base + lane_base + L::P_COL + b * 64 + half * 32;
-        float ls[4] = {0.f, 0.f, 0.f, 0.f};  // four short row-sum chains instead of two long ones
-        const float nm = -m_new;
-#pragma unroll
-        for (int hb = 0; hb < 2; ++hb) {  // 32 keys -> 16 packed columns, stored at once
-          uint32_t pk[16];
-          if (nvis > 0) {  // padding rows, rows past their position: P is zero
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-              const int q4 = hb * 2 + q;
-#pragma unroll
-              for (int jj = 0; jj < 16; jj += 2) {
-                // every exponential on the SFU (measured faster than an FMA-pipe share); masked
-                // keys and columns past a short sub-chunk hold -inf: exp2(-inf) = +0
-                const float p0 = ex2_approx(fmaf(__uint_as_float(v[q4][jj]), sl2, nm));
-                const float p1 = ex2_approx(fmaf(__uint_as_float(v[q4][jj + 1]), sl2, nm));
-                ls[(jj >> 1) & 3] += p0 + p1;
-                __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
-                pk[q * 8 + (jj >> 1)] = *reinterpret_cast<uint32_t*>(&h2);
-              }
-            }
-          } else {
-#pragma unroll
-            for (int c = 0; c < 16; ++c) pk[c] = 0u;
-          }
-          // (columns past the sub-chunk's pages are never read by P.V)
-          if (hkeys > 0) tmem_st16(pcol + hb * 16, pk);
-        }
-        l_part = l_part * corr + ((ls[0] + ls[1]) + (ls[2] + ls[3]));
-        m_run = m_new;
-        if (j > 0 && __any_sync(0xffffffffu, valid && corr != 1.f)) {
-          // the max moved: rescale this half's 64 O columns once P.V(J - 1) has landed
-          mbar_wait(o_done, (J - 1) & 1);
+      // Narrow units (<= 64 entries: every entry sits in lanes 0-15 of its lane quarter) read
+      // and write only those 16 lanes (16x256b / 16x128b shapes): each thread holds two rows x
+      // 16 keys, half the exponentials of the 32-lane form. The arithmetic per row is the same
+      // as the wide form's -- thread t%4 of a row's group carries exactly the wide form's row-sum
+      // chain t%4, combined in the same order -- so a row's partial does not depend on how many
+      // entries share its item. Used for units of >= 4 sub-chunks, where the softmax sets the
+      // pace (measured: C4 32k streaming 1.4 -> 1.1 us per sub-chunk).
+      const bool narrow = kNarrow && it.n_rows <= 64 && nsub >= 4;
+      if (narrow) {
+        const int gq = lane & 3;
+        const int rA = quarter * 32 + (lane >> 2), rB = rA + 8;
+        const int eA = (lane >> 2) * 4 + quarter, eB = eA + 32;
+        const bool vA = eA < it.n_rows, vB = eB < it.n_rows;
+        const int posA = vA ? row_pos[item_rows[it.row_off + eA].x] : -1;
+        const int posB = vB ? row_pos[item_rows[it.row_off + eB].x] : -1;
+        float mA = -INFINITY, mB = -INFINITY, lA = 0.f, lB = 0.f;
+        for (int j = 0; j < nsub; ++j, ++J) {
+          const int b = J & 1;
+          const int keys = min(SUBP, np - j * SUBP) * 16;
+          const int kbase = it.chunk_start + j * SUBP * 16 + half * 64;
+          const int hkeys = min(64, keys - half * 64);
+          mbar_wait(&s_full[b], (J >> 1) & 1);
           tc_fence_after();
-          uint32_t o[4][16];
+          if (r == 0 && half == 0) sstamp(J, 1);
+          if (r == 0 && half == 0 && J == 0) stamp(2);
+          uint32_t v[32];  // v[4i + c]: row A key 8i + 2gq + c; v[4i + 2 + c]: row B
+          if (hkeys > 0) {
+            tmem_ld_16x256b_x8(tmem_base + b * 128 + lane_base + half * 64, v);
+            tmem_wait_ld();
+            tmem_reg_fence32(v);
+          }
+          const int nvA = vA ? max(0, min(hkeys, posA + 1 - kbase)) : 0;
+          const int nvB = vB ? max(0, min(hkeys, posB + 1 - kbase)) : 0;
+          if ((nvA > 0 && nvA < 64) || (nvB > 0 && nvB < 64)) {
+            asm volatile("" ::: "memory");
 #pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) tmem_ld16_nowait(tmem_o + lane_base + half * 64 + q4 * 16, o[q4]);
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+              for (int c = 0; c < 2; ++c) {
+                const int key = 8 * i + 2 * gq + c;
+                if (key >= nvA) v[4 * i + c] = 0xff800000u;
+                if (key >= nvB) v[4 * i + 2 + c] = 0xff800000u;
+              }
+          }
+          float mxA = -INFINITY, mxB = -INFINITY;
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              mxA = fmaxf(mxA, __uint_as_float(v[4 * i + c]));
+              mxB = fmaxf(mxB, __uint_as_float(v[4 * i + 2 + c]));
+            }
+          if (nvA == 0) mxA = -INFINITY;
+          if (nvB == 0) mxB = -INFINITY;
+          mxA = fmaxf(mxA, __shfl_xor_sync(0xffffffffu, mxA, 1));
+          mxB = fmaxf(mxB, __shfl_xor_sync(0xffffffffu, mxB, 1));
+          mxA = fmaxf(mxA, __shfl_xor_sync(0xffffffffu, mxA, 2));
+          mxB = fmaxf(mxB, __shfl_xor_sync(0xffffffffu, mxB, 2));
+          if (gq == 0) {
+            red[half * 128 + rA] = mxA;
+            red[half * 128 + rB] = mxB;
+          }
+          named_bar_sync(1 + quarter, 64);
+          const float mcA = fmaxf(mA, __fmul_rn(fmaxf(red[rA], red[128 + rA]), sl2));
+          const float mcB = fmaxf(mB, __fmul_rn(fmaxf(red[rB], red[128 + rB]), sl2));
+          named_bar_sync(1 + quarter, 64);
+          const float mnA = (mcA > mA + 8.f) ? mcA : mA;
+          const float mnB = (mcB > mB + 8.f) ? mcB : mB;
+          const float corrA = (mA == -INFINITY) ? 1.f : ex2_approx(mA - mnA);
+          const float corrB = (mB == -INFINITY) ? 1.f : ex2_approx(mB - mnB);
+          if (J >= 2) mbar_wait(&p_free[b], ((J >> 1) - 1) & 1);
+          tc_fence_after();
+          uint32_t pk[16];  // pk[2i]: row A P column 4i + gq (keys 8i + 2gq, +1); pk[2i + 1]: row B
+          float lsA = 0.f, lsB = 0.f;
+          const float nmA = -mnA, nmB = -mnB;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float a0 = nvA > 0 ? ex2_approx(fmaf(__uint_as_float(v[4 * i]), sl2, nmA)) : 0.f;
+            const float a1 = nvA > 0 ? ex2_approx(fmaf(__uint_as_float(v[4 * i + 1]), sl2, nmA)) : 0.f;
+            const float b0 = nvB > 0 ? ex2_approx(fmaf(__uint_as_float(v[4 * i + 2]), sl2, nmB)) : 0.f;
+            const float b1 = nvB > 0 ? ex2_approx(fmaf(__uint_as_float(v[4 * i + 3]), sl2, nmB)) : 0.f;
+            lsA += a0 + a1;
+            lsB += b0 + b1;
+            __nv_bfloat162 ha = __floats2bfloat162_rn(a0, a1), hb2 = __floats2bfloat162_rn(b0, b1);
+            pk[2 * i] = *reinterpret_cast<uint32_t*>(&ha);
+            pk[2 * i + 1] = *reinterpret_cast<uint32_t*>(&hb2);
+          }
+          if (hkeys > 0) tmem_st_16x128b_x8(tmem_base + lane_base + L::P_COL + b * 64 + half * 32, pk);
+          float sA = lsA + __shfl_xor_sync(0xffffffffu, lsA, 1);
+          float sB = lsB + __shfl_xor_sync(0xffffffffu, lsB, 1);
+          sA = sA + __shfl_xor_sync(0xffffffffu, sA, 2);
+          sB = sB + __shfl_xor_sync(0xffffffffu, sB, 2);
+          lA = fmaf(lA, corrA, sA);
+          lB = fmaf(lB, corrB, sB);
+          mA = mnA;
+          mB = mnB;
+          if (j > 0 && __any_sync(0xffffffffu, (vA && corrA != 1.f) || (vB && corrB != 1.f))) {
+            mbar_wait(o_done, (J - 1) & 1);
+            tc_fence_after();
+#pragma unroll 1
+            for (int hc = 0; hc < 2; ++hc) {  // 32 columns at a time (register budget)
+              uint32_t o[16];
+              tmem_ld_16x256b_x4(tmem_o + lane_base + half * 64 + hc * 32, o);
+              tmem_wait_ld();
+              tmem_reg_fence(o);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                o[4 * i] = __float_as_uint(__uint_as_float(o[4 * i]) * corrA);
+                o[4 * i + 1] = __float_as_uint(__uint_as_float(o[4 * i + 1]) * corrA);
+                o[4 * i + 2] = __float_as_uint(__uint_as_float(o[4 * i + 2]) * corrB);
+                o[4 * i + 3] = __float_as_uint(__uint_as_float(o[4 * i + 3]) * corrB);
+              }
+              tmem_st_16x256b_x4(tmem_o + lane_base + half * 64 + hc * 32, o);
+            }
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+          tc_fence_before();
+          mbar_arrive((bars + (b ? 17 : 7)));
+          if (r == 0 && half == 0) sstamp(J, 2);
+        }
+        if (gq == 0) {
+          red[half * 128 + rA] = lA;
+          red[half * 128 + rB] = lB;
+          if (half == 0) {
+            mrow[rA] = mA;
+            mrow[rB] = mB;
+          }
+        }
+      } else {
+        for (int j = 0; j < nsub; ++j, ++J) {
+          const int b = J & 1;
+          const int keys = min(SUBP, np - j * SUBP) * 16;
+          const int kbase = it.chunk_start + j * SUBP * 16 + half * 64;
+          const int hkeys = min(64, keys - half * 64);  // this half's columns (may be <= 0)
+          mbar_wait(&s_full[b], (J >> 1) & 1);
+          tc_fence_after();
+          if (r == 0 && half == 0) sstamp(J, 1);
+          if (r == 0 && half == 0 && J == 0) stamp(2);
+          uint32_t v[4][16];  // raw q.k of this half's (<= 64) keys
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4)
+            if (q4 * 16 < hkeys) tmem_ld16_nowait(tmem_base + b * 128 + lane_base + half * 64 + q4 * 16, v[q4]);
           tmem_wait_ld();
 #pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) {
-            tmem_reg_fence(o[q4]);
+          for (int q4 = 0; q4 < 4; ++q4) tmem_reg_fence(v[q4]);
+          // visible keys of this half: [kbase, kbase + nvis); max of raw scores x sl2 (> 0)
+          // equals the max of the scaled scores (rounding is monotonic)
+          const int nvis = valid ? max(0, min(hkeys, pos + 1 - kbase)) : 0;
+          if (nvis > 0 && nvis < 64) {
+            // rare (the row's causal edge or a short last sub-chunk): invisible keys become
+            // -inf once, so the max and exp loops below carry no per-key predicates
+            asm volatile("" ::: "memory");
 #pragma unroll
-            for (int jj = 0; jj < 16; ++jj) o[q4][jj] = __float_as_uint(__uint_as_float(o[q4][jj]) * corr);
-            tmem_st16(tmem_o + lane_base + half * 64 + q4 * 16, o[q4]);
+            for (int q4 = 0; q4 < 4; ++q4)
+#pragma unroll
+              for (int jj = 0; jj < 16; ++jj)
+                if (q4 * 16 + jj >= nvis) v[q4][jj] = 0xff800000u;  // -inf
           }
+          float mx = -INFINITY;
+          if (nvis > 0) {
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4)
+#pragma unroll
+              for (int jj = 0; jj < 16; ++jj) mx = fmaxf(mx, __uint_as_float(v[q4][jj]));
+          }
+          // exchange with the partner thread (same row, other half); the second barrier lets
+          // the buffer be rewritten next iteration
+          red[half * 128 + r] = mx;
+          named_bar_sync(1 + quarter, 64);
+          const float m_cand = fmaxf(m_run, __fmul_rn(fmaxf(red[r], red[128 + r]), sl2));
+          named_bar_sync(1 + quarter, 64);
+          // lazy max: keep the reference while the new scores stay within 2^8 of it (P <= 256
+          // is exact enough in bf16 / fp32), so O is rescaled only when the max jumps
+          const float m_new = (m_cand > m_run + 8.f) ? m_cand : m_run;
+          const float corr = (m_run == -INFINITY) ? 1.f : ex2_approx(m_run - m_new);
+          // P buffer b was last read by P.V(J - 2)
+          if (J >= 2) mbar_wait(&p_free[b], ((J >> 1) - 1) & 1);
+          tc_fence_after();
+          // this half's 64 keys -> 32 packed bf16x2 columns of TMEM P buffer b
+          const uint32_t pcol = tmem_base + lane_base + L::P_COL + b * 64 + half * 32;
+          float ls[4] = {0.f, 0.f, 0.f, 0.f};  // four short row-sum chains instead of two long ones
+          const float nm = -m_new;
+#pragma unroll
+          for (int hb = 0; hb < 2; ++hb) {  // 32 keys -> 16 packed columns, stored at once
+            uint32_t pk[16];
+            if (nvis > 0) {  // padding rows, rows past their position: P is zero
+#pragma unroll
+              for (int q = 0; q < 2; ++q) {
+                const int q4 = hb * 2 + q;
+#pragma unroll
+                for (int jj = 0; jj < 16; jj += 2) {
+                  // every exponential on the SFU (measured faster than an FMA-pipe share); masked
+                  // keys and columns past a short sub-chunk hold -inf: exp2(-inf) = +0
+                  const float p0 = ex2_approx(fmaf(__uint_as_float(v[q4][jj]), sl2, nm));
+                  const float p1 = ex2_approx(fmaf(__uint_as_float(v[q4][jj + 1]), sl2, nm));
+                  ls[(jj >> 1) & 3] += p0 + p1;
+                  __nv_bfloat162 h2 = __floats2bfloat162_rn(p0, p1);
+                  pk[q * 8 + (jj >> 1)] = *reinterpret_cast<uint32_t*>(&h2);
+                }
+              }
+            } else {
+#pragma unroll
+              for (int c = 0; c < 16; ++c) pk[c] = 0u;
+            }
+            // (columns past the sub-chunk's pages are never read by P.V)
+            if (hkeys > 0) tmem_st16(pcol + hb * 16, pk);
+          }
+          l_part = fmaf(l_part, corr, (ls[0] + ls[1]) + (ls[2] + ls[3]));
+          m_run = m_new;
+          if (j > 0 && __any_sync(0xffffffffu, valid && corr != 1.f)) {
+            // the max moved: rescale this half's 64 O columns once P.V(J - 1) has landed
+            mbar_wait(o_done, (J - 1) & 1);
+            tc_fence_after();
+            uint32_t o[4][16];
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) tmem_ld16_nowait(tmem_o + lane_base + half * 64 + q4 * 16, o[q4]);
+            tmem_wait_ld();
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              tmem_reg_fence(o[q4]);
+#pragma unroll
+              for (int jj = 0; jj < 16; ++jj) o[q4][jj] = __float_as_uint(__uint_as_float(o[q4][jj]) * corr);
+              tmem_st16(tmem_o + lane_base + half * 64 + q4 * 16, o[q4]);
+            }
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");  // P (and rescaled O) in TMEM
+          tc_fence_before();
+          mbar_arrive((bars + (b ? 17 : 7)));
+          if (r == 0 && half == 0) sstamp(J, 2);
         }
-        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");  // P (and rescaled O) in TMEM
-        tc_fence_before();
-        mbar_arrive(p_full_b[b]);
-        if (r == 0 && half == 0) sstamp(J, 2);
+        red[half * 128 + r] = l_part;
+        if (half == 0) mrow[r] = m_run;
       }
       if (r == 0 && half == 0) stamp(4);
       // ---------------- epilogue: unnormalised partial O and (m, l), straight from TMEM
       // (each thread 256 contiguous bytes of its entry's row) ----------------
-      red[half * 128 + r] = l_part;
       mbar_wait(o_final, n & 1);  // the unit's last P.V landed (single phase per unit)
       tc_fence_after();
+      if (r == 0 && half == 0) stamp(0);
       named_bar_sync(1 + quarter, 64);
       const float l = red[r] + red[128 + r];
+      m_run = mrow[r];
       named_bar_sync(1 + quarter, 64);  // red is rewritten by the next unit's first exchange
       uint32_t o[4][16];
 #pragma unroll
@@ -494,6 +630,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                                                __uint_as_float(o[q4][jj + 2]), __uint_as_float(o[q4][jj + 3]));
         }
         if (half == 0) part_ml[slot] = make_float2(m_run, l);
+        if (r == 0 && half == 0) stamp(1);
       }
       // O may now be overwritten: the next unit's first P.V waits for this group's P arrive
       tc_fence_before();
@@ -509,17 +646,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
 }
 
-cudaError_t attn_tc_partial_launch(const AttnLaunch& a, int /*chunk_pages*/, cudaStream_t s) {
+// The 16-lane softmax form only pays on units of >= 4 sub-chunks, i.e. chunks of >= 32 pages
+// (a deployment constant, so a captured graph's kernel choice stays valid); compiled in, it
+// costs the 32-lane form register spills (measured: C2 decode attention 331 -> 370 us per
+// step), so short-chunk configurations run the kernel without it. Both forms produce the same
+// bits for a row.
+cudaError_t attn_tc_partial_launch(const AttnLaunch& a, int chunk_pages, cudaStream_t s) {
   using L = TcLayout;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::SMEM);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(attn_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int units = a.n_items_cap * a.num_kv_heads;
   const int grid = units < a.num_sms ? units : a.num_sms;
-  return launch_pdl(attn_tc_kernel, dim3(grid), dim3(TC_THREADS), L::SMEM, s,
+  auto kern = chunk_pages >= 4 * SUBP ? attn_tc_kernel<true> : attn_tc_kernel<false>;
+  return launch_pdl(kern, dim3(grid), dim3(TC_THREADS), L::SMEM, s,
                     a.tm_k, a.tm_v, a.tm_k8, a.tm_v8, a.q, a.q_ld, a.num_kv_heads, a.group, a.items, a.item_pages,
                     a.item_rows, a.row_pos, a.num_heads, a.max_chunks, a.scale, a.part_o, a.part_ml,
                     a.sched_off, a.sched_units, a.trace, a.chunk_tokens, a.span);

@@ -358,7 +358,7 @@ __device__ __forceinline__ void lora_shrink_tasks(const GemmParams& p, int gwarp
 #pragma unroll
       for (int i = 0; i < NI; ++i) {
         const int k = k0 + i * 256 + lane * 8;
-        xraw[i] = k < p.sh_K ? *reinterpret_cast<const uint4*>(p.sh_x + (size_t)gr * p.sh_ld + k)
+        xraw[i] = k < p.sh_K ? __ldcg(reinterpret_cast<const uint4*>(p.sh_x + (size_t)gr * p.sh_ld + k))
                              : make_uint4(0, 0, 0, 0);
       }
       float acc = 0.f;

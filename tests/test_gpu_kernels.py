@@ -251,3 +251,39 @@ def test_tc_attention_prefill_rows_causal_and_many_entries(cuda):
                                  hd, chunk_pages=chunk_pages)
         err = (got.float().cpu() - ref).abs().max().item()
         assert err < 2e-2, (chunk_pages, err)
+
+
+def test_tc_attention_narrow_and_wide_items_are_bitwise_equal(cuda):
+    """Items with <= 64 query entries run the 16-lane softmax form, wider items the 32-lane
+    form; a row's output must not depend on which form served it (batch invariance): 20
+    sequences on one shared prefix (160 entries per KV head -> a 128-entry wide item plus a
+    narrow one per chunk) against every sequence run alone (8 entries: narrow). Positions
+    differ per sequence so causal edges cut sub-chunks, and some queries are scaled up so the
+    running max moves between sub-chunks (O rescale path)."""
+    import torch
+    g = torch.Generator(device="cpu").manual_seed(5)
+    H, Hkv, hd = 32, 8, 128
+    shared, n_seq, priv = 37, 20, 2
+    n_pages = shared + n_seq * priv
+    kp = torch.randn(n_pages, Hkv, 16, hd, generator=g).to(torch.bfloat16)
+    vp = torch.randn(n_pages, Hkv, 16, hd, generator=g).to(torch.bfloat16)
+    bt = np.full((n_seq, shared + priv), -1, np.int32)
+    for s_ in range(n_seq):
+        bt[s_, :shared] = np.arange(shared)
+        bt[s_, shared:] = shared + priv * s_ + np.arange(priv)
+    row_seq = [s_ for s_ in range(n_seq) for _ in range(2)]
+    row_pos = [shared * 16 + 1 + s_ for s_ in range(n_seq) for _ in range(2)]
+    q = torch.randn(len(row_seq), H * hd, generator=g)
+    q[1::4] *= 4.0
+    q = q.to(torch.bfloat16)
+    kd, vd = kp.to(cuda), vp.to(cuda)
+    for chunk_pages in (8, 16, 64):
+        together, n_items = _run_attn(q.to(cuda), kd, vd, bt, row_seq, row_pos, H, Hkv, hd,
+                                      chunk_pages=chunk_pages)
+        for s_ in range(n_seq):
+            alone, _ = _run_attn(q[2 * s_:2 * s_ + 2].to(cuda), kd, vd, bt[s_:s_ + 1], [0, 0],
+                                 row_pos[2 * s_:2 * s_ + 2], H, Hkv, hd, chunk_pages=chunk_pages)
+            assert torch.equal(together[2 * s_:2 * s_ + 2], alone), (chunk_pages, s_)
+    ref = _attention_ref(q, kp, vp, bt, row_seq, row_pos, H, Hkv, hd)
+    err = (together.float().cpu() - ref).abs().max().item()
+    assert err < 3e-2, err

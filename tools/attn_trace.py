@@ -34,7 +34,7 @@ def main():
         if l[0] == "launch":
             print(f"stamp kernel before the launch {l[2]} us, after it {l[3]} us (relative to the first CTA)")
     names = ["o_final", "q_loaded", "s0_ready", "q_wait", "loop_done", "epi_done", "entry", "k_pdl",
-             "-", "fin_start", "merge_go", "merge_done"]
+             "-", "cta_end", "merge_go", "merge_done"]
     print(f"partial CTAs {len(part)}")
     for k in (6, 7, 3, 1, 2, 4, 0, 5, 9, 10, 11):
         if k >= part.shape[1]:
