@@ -38,7 +38,10 @@ __device__ __forceinline__ void merge_slice4(const float* __restrict__ part_o,
                                              int nch, int d, __nv_bfloat16* __restrict__ dst) {
   constexpr int B0 = 24, B1 = 16, B2 = 8;
   if (nch <= B0) {
-    // the common case: every load in one round trip, then the same two passes in registers
+    // the common case: every load in one round trip, then the same two passes in registers,
+    // branch-free -- chunks past nch carry (m, l, O) = (-inf, 0, 0), i.e. weight exp2(-inf) = 0
+    // and fma(0, 0, x) = x -- so the exponentials of all chunks issue back to back (measured:
+    // the C4 merge 2.3 -> 1.6 us against a per-chunk branch around each fold)
     float2 ml[B0];
     float4 po[B0];
 #pragma unroll
@@ -54,8 +57,7 @@ __device__ __forceinline__ void merge_slice4(const float* __restrict__ part_o,
     float L = 0.f;
     float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int k = 0; k < B0; ++k)
-      if (k < nch) fold4(L, O, ml[k], po[k], M);
+    for (int k = 0; k < B0; ++k) fold4(L, O, ml[k], po[k], M);
     store4<HD>(dst, O, L);
     return;
   }
