@@ -9,6 +9,13 @@ constexpr int BM = 128;  // MMA M (weight rows per tile)
 constexpr int BK = 64;   // K elements per stage (one 128-byte swizzle row)
 constexpr uint32_t W_BYTES = BM * BK * 2;
 constexpr int MAX_RANK = 32;
+// stream-K scratch word that holds no published partial (an all-ones NaN: the tensor cores
+// only ever produce the canonical 0x7fffffff NaN)
+constexpr uint32_t WS_EMPTY = 0xFFFFFFFFu;
+__device__ __forceinline__ bool ws_empty(const float4& x) {
+  return (__float_as_uint(x.x) == WS_EMPTY) | (__float_as_uint(x.y) == WS_EMPTY) |
+         (__float_as_uint(x.z) == WS_EMPTY) | (__float_as_uint(x.w) == WS_EMPTY);
+}
 // barriers, reduction scratch, staged row metadata and the LoRA U rows of the launch
 template <int NT>
 constexpr size_t aux_smem() {
@@ -137,19 +144,27 @@ __device__ __forceinline__ void warp_argmax16(const float (&v)[16], int idx, int
   argmax_pick(bv, bi, __shfl_xor_sync(0xffffffffu, bv, 1), __shfl_xor_sync(0xffffffffu, bi, 1));
 }
 
-// Per-CTA shared state of the epilogue warps.
-struct EpiShared {
+// Per-CTA shared state of the epilogue warps (16-byte aligned and sized: the row metadata
+// that follows it is read as int4 vectors).
+struct alignas(16) EpiShared {
   int flag;
   int shrink_ready;
   int fin_last;  // the epilogue's finalize decision for the CTA's last tile (helpers read it)
   float red_val[64];
   int red_idx[64];
 };
+// barriers (<= 16 stages) + TMEM slot, EpiShared, row metadata + SGMV table, helper EpiShared
+static_assert((2 * 16 + 2) * 8 + 16 + 2 * sizeof(EpiShared) + (5 * 16 + 64 + 1 + 512 + 3) * 4 <=
+                  aux_smem<16>(), "aux shared-memory layout overflows");
+
 
 __device__ __forceinline__ float silu_ref(float g) {
-  // Sign-split logistic as in src/tensor.py:199-214 (_sigmoid, silu).
-  float z = expf(-fabsf(g));
-  float sig = g >= 0.f ? __fdiv_rn(1.f, 1.f + z) : __fdiv_rn(z, 1.f + z);
+  // Sign-split logistic as in src/tensor.py:199-214 (_sigmoid, silu): 1/(1+z) for g >= 0,
+  // z/(1+z) otherwise, z = exp(-|g|) (never overflows). MUFU exp2 / reciprocal (a few f32
+  // ulps, far below the bf16 rounding of the result): no division slow-path branch, so the
+  // 16 rows of a finalize interleave instead of running one latency chain after another.
+  const float z = __expf(-fabsf(g));
+  const float sig = __fdividef(g >= 0.f ? 1.f : z, 1.f + z);
   return __fmul_rn(g, sig);
 }
 
@@ -177,6 +192,13 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
                                            int ep_t, EpiShared& sh, const RowMeta& rm, int bar,
                                            const float* pre = nullptr, const float2* cs_pre = nullptr) {
   const int m = tile * BM + ep_t;
+  // row kinds of the 16 rows (-1: padding or beyond n_rows, staged that way)
+  int kd[16];
+#pragma unroll
+  for (int j = 0; j < 16; j += 4) {
+    const int4 k4 = *reinterpret_cast<const int4*>(rm.kind + n0 + j);
+    kd[j] = k4.x; kd[j + 1] = k4.y; kd[j + 2] = k4.z; kd[j + 3] = k4.w;
+  }
   // ---- RMSNorm of the input rows (X was the raw residual stream) ----
   if (p.in_ssq != nullptr) {
 #pragma unroll
@@ -189,27 +211,28 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
         if (n < p.n_rows) p.out_f32[(size_t)(p.row0 + n) * p.ld_out + m] = v[j];
       }
   } else if constexpr (MODE == EPI_RESID) {
+      // Every row's math first (16 independent chains the scheduler can interleave), then
+      // the predicated stores: a per-row branch would serialise the rows' latencies.
       const int wq = ep_t >> 5, ln = ep_t & 31;
-      float sq[16], old[16];
-      // all residual loads before any store (the stores may alias them for the compiler, which
-      // would otherwise expose one L2 round trip per row)
+      float old[16], xn[16], sq[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int n = n0 + j;
         old[j] = pre != nullptr ? pre[j]
-                 : (n < p.n_rows && rm.kind[n] >= 0) ? __ldcg(p.resid + (size_t)(p.row0 + n) * p.M + m)
-                                                     : 0.f;
+                 : kd[j] >= 0 ? __ldcg(p.resid + (size_t)(p.row0 + n) * p.M + m) : 0.f;
       }
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        const int n = n0 + j;
-        sq[j] = 0.f;
-        if (n < p.n_rows && rm.kind[n] >= 0) {
-          const size_t idx = (size_t)(p.row0 + n) * p.M + m;
-          const float xn = __fadd_rn(old[j], v[j]);
-          p.resid[idx] = xn;
-          p.resid_bf16[idx] = __float2bfloat16_rn(xn);
-          sq[j] = __fmul_rn(xn, xn);
+        xn[j] = __fadd_rn(old[j], v[j]);
+        sq[j] = kd[j] >= 0 ? __fmul_rn(xn[j], xn[j]) : 0.f;
+      }
+      float* rp = p.resid + (size_t)(p.row0 + n0) * p.M + m;
+      __nv_bfloat16* bp = p.resid_bf16 + (size_t)(p.row0 + n0) * p.M + m;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (kd[j] >= 0) {
+          rp[(size_t)j * p.M] = xn[j];
+          bp[(size_t)j * p.M] = __float2bfloat16_rn(xn[j]);
         }
       }
       const float wsum = warp_reduce16(sq, ln);
@@ -225,14 +248,17 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
       }
       named_bar_sync(bar, 128);
   } else if constexpr (MODE == EPI_SILU) {
+      float f[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const float partner = __shfl_xor_sync(0xffffffffu, v[j], 1);
-        const int n = n0 + j;
-        if ((m & 1) == 0 && n < p.n_rows && rm.kind[n] >= 0) {
-          const float f = __fmul_rn(silu_ref(v[j]), partner);
-          p.out_bf16[(size_t)(p.row0 + n) * (p.M >> 1) + (m >> 1)] = __float2bfloat16_rn(f);
-        }
+        f[j] = __fmul_rn(silu_ref(v[j]), partner);
+      }
+      if ((m & 1) == 0) {
+        __nv_bfloat16* op = p.out_bf16 + (size_t)(p.row0 + n0) * (p.M >> 1) + (m >> 1);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (kd[j] >= 0) op[(size_t)j * (p.M >> 1)] = __float2bfloat16_rn(f[j]);
       }
   } else if constexpr (MODE == EPI_QKV) {
       const int hd = p.head_dim;
@@ -240,7 +266,6 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
       const int base = region == 0 ? 0 : (region == 1 ? p.q_dim : p.q_dim + p.kv_dim);
       const int i = (m - base) % hd;
       const int head = (m - base) / hd;
-      __nv_bfloat16* pages = region == 1 ? p.k_pages : p.v_pages;
       // RoPE factors of all 16 rows loaded up front (one round trip, not one per row), or
       // already prefetched by the caller while the tile was streaming
       float2 csv[16];
@@ -248,31 +273,37 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
       for (int j = 0; j < 16; ++j) {
         const int n = n0 + j;
         csv[j] = cs_pre != nullptr ? cs_pre[j]
-                 : (region < 2 && n < p.n_rows && rm.kind[n] >= 0)
+                 : (region < 2 && kd[j] >= 0)
                      ? __ldg(p.rope + (size_t)rm.pos[n] * (hd >> 1) + (i >> 1))
                      : make_float2(1.f, 0.f);
       }
+      float out[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const float partner = __shfl_xor_sync(0xffffffffu, v[j], 1);
-        const int n = n0 + j;
-        const int kind = n < p.n_rows ? rm.kind[n] : -1;
-        if (kind < 0) continue;
-        float out = v[j];
-        if (region < 2) {
-          // Interleaved-pair RoPE, src/tensor.py:309-315.
-          const float2 cs = csv[j];
-          if ((i & 1) == 0)
-            out = __fsub_rn(__fmul_rn(v[j], cs.x), __fmul_rn(partner, cs.y));
-          else
-            out = __fadd_rn(__fmul_rn(partner, cs.y), __fmul_rn(v[j], cs.x));
+        // Interleaved-pair RoPE, src/tensor.py:309-315 (q and k only; v passes through).
+        const float2 cs = csv[j];
+        const float even = __fsub_rn(__fmul_rn(v[j], cs.x), __fmul_rn(partner, cs.y));
+        const float odd = __fadd_rn(__fmul_rn(partner, cs.y), __fmul_rn(v[j], cs.x));
+        out[j] = region == 2 ? v[j] : ((i & 1) == 0 ? even : odd);
+      }
+      if (region == 0) {
+        __nv_bfloat16* qp = p.out_bf16 + (size_t)(p.row0 + n0) * p.q_dim + m;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (kd[j] >= 0) qp[(size_t)j * p.q_dim] = __float2bfloat16_rn(out[j]);
+      } else {
+        // Encoder rows only: K/V for position pos into its page (src/model.py:486-494).
+        __nv_bfloat16* pages = (region == 1 ? p.k_pages : p.v_pages) + (size_t)head * 16 * hd + i;
+        int ko[16];
+#pragma unroll
+        for (int j = 0; j < 16; j += 4) {
+          const int4 k4 = *reinterpret_cast<const int4*>(rm.kvoff + n0 + j);
+          ko[j] = k4.x; ko[j + 1] = k4.y; ko[j + 2] = k4.z; ko[j + 3] = k4.w;
         }
-        if (region == 0) {
-          p.out_bf16[(size_t)(p.row0 + n) * p.q_dim + m] = __float2bfloat16_rn(out);
-        } else if (kind == 0) {
-          // Encoder rows only: K/V for position pos into its page (src/model.py:486-494).
-          pages[(size_t)rm.kvoff[n] + (size_t)head * 16 * hd + i] = __float2bfloat16_rn(out);
-        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (kd[j] == 0) pages[ko[j]] = __float2bfloat16_rn(out[j]);
       }
   } else if constexpr (MODE == EPI_ARGMAX) {
       const int wq = ep_t >> 5, ln = ep_t & 31;
@@ -494,11 +525,22 @@ __global__ void __launch_bounds__(256, 1)
   pdl_launch();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) stamp(0);
+  // stream-K partial of CTA cs (its first tile), 16-column chunk cc, for this thread's
+  // feature: layout [cta][chunk][4 float4][128 features], a warp's float4 access is 512
+  // contiguous bytes
+  auto ws_slot = [&](int cs, int cc) {
+    return reinterpret_cast<float4*>(p.ws) + (((size_t)cs * (NT / 16) + cc) * 4) * BM + (threadIdx.x & 127);
+  };
   // Finalization of 16-column chunks [cc0, cc1) of tile t by one 128-thread group (thread
-  // ep_t owns output feature t * 128 + ep_t; TMEM lane quarter = warp % 4): fold the stream-K
-  // partials in segment order (or read the accumulator when the tile is this CTA's alone) and
-  // run the fused epilogue. Wide launches software-pipeline it: the next chunk's first PF
-  // partials and residual rows are requested before the current chunk is folded.
+  // ep_t owns output feature t * 128 + ep_t; TMEM lane quarter = warp % 4). A tile split over
+  // several CTAs is finalized by the CTA holding its FIRST K segment (segment 0: the tile
+  // starts inside that CTA's range, so it is the CTA's last tile and its accumulator is the
+  // last to complete). The other segments are the first tiles of the following CTAs; each
+  // publishes its fp32 partial into its own ws slot, which holds the WS_EMPTY pattern
+  // whenever it is unpublished. The finalizer folds seg 0 (TMEM) + seg 1 + ... in segment
+  // order -- fixed by (M, K, grid) only -- polling each 4-byte word until it is not
+  // WS_EMPTY (no atomics, no fences: one L2 round trip when the partials are there), and
+  // re-arms the slots it consumed. Wide launches software-pipeline the residual rows.
   auto fin_chunks = [&](int t, int cc0, int cc1, int ep_t, EpiShared& shx, int bar, const float* pre0,
                         const float2* cs0) {
     const long long t0 = (long long)t * sp.Ut;
@@ -506,99 +548,72 @@ __global__ void __launch_bounds__(256, 1)
     const int nseg = c_last - c_first + 1;
     const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
     const bool stamps = ep_t == 0 && bar == 1;
-      constexpr int PF = NT > 16 ? 2 : 1;
-      constexpr bool PIPE = NT > 16;
-      float4 nb[PF][4];
-      float npre[16];
-      auto seg_src = [&](int s, int cc) {
-        const int cs = c_first + s;
-        const int sl = (sp.ubegin(cs) >= t0) ? 0 : 1;  // tile t is cs's first tile
-        return reinterpret_cast<const float4*>(p.ws) + ((((size_t)cs * 2 + sl) * (NT / 16) + cc) * 4) * BM + ep_t;
-      };
-      auto fetch = [&](int cc) {
-        if (nseg > 1) {
+    constexpr bool PIPE = NT > 16;
+    float npre[16];
+    auto fetch_resid = [&](int cc) {
+      if (MODE == EPI_RESID) {
+        const int m = t * BM + ep_t;
 #pragma unroll
-          for (int s = 0; s < PF; ++s)
-            if (s < nseg) {
-              const float4* src = seg_src(s, cc);
-#pragma unroll
-              for (int q = 0; q < 4; ++q) nb[s][q] = __ldcg(src + q * BM);
-            }
+        for (int j = 0; j < 16; ++j) {
+          const int n = cc * 16 + j;
+          npre[j] = (n < p.n_rows) ? __ldcg(p.resid + (size_t)(p.row0 + n) * p.M + m) : 0.f;
         }
-        if (MODE == EPI_RESID) {
-          const int m = t * BM + ep_t;
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int n = cc * 16 + j;
-            npre[j] = (n < p.n_rows) ? __ldcg(p.resid + (size_t)(p.row0 + n) * p.M + m) : 0.f;
-          }
-        }
-      };
-      if (PIPE) fetch(cc0);
-#pragma unroll 1
-      for (int cc = cc0; cc < cc1; ++cc) {
-        float4 cb[PF][4];
-        float cpre[16];
-        if (PIPE) {
-#pragma unroll
-          for (int s = 0; s < PF; ++s)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) cb[s][q] = nb[s][q];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) cpre[j] = npre[j];
-          if (cc + 1 < cc1) fetch(cc + 1);
-        }
-        float v[16];
-        if (nseg == 1) {
-          tmem_ld16(tmem_base + lane_base + cc * 16, v);
-        } else {
-          // segments [0, PF) were prefetched (wide launches); the rest are loaded SEG_BATCH
-          // at a time with every load of a batch issued before its first add
-          constexpr int SEG_BATCH = 4;
-          const int s_start = PIPE ? min(PF, nseg) : 0;
-          if (PIPE) {
-#pragma unroll
-            for (int s = 0; s < PF; ++s)
-              if (s < nseg) {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  const float x[4] = {cb[s][q].x, cb[s][q].y, cb[s][q].z, cb[s][q].w};
-#pragma unroll
-                  for (int e = 0; e < 4; ++e) v[4 * q + e] = (s == 0) ? x[e] : __fadd_rn(v[4 * q + e], x[e]);
-                }
-              }
-          }
-#pragma unroll 1
-          for (int s0 = s_start; s0 < nseg; s0 += SEG_BATCH) {
-            float4 buf[SEG_BATCH][4];
-#pragma unroll
-            for (int s = 0; s < SEG_BATCH; ++s) {
-              if (s0 + s < nseg) {
-                const float4* src = seg_src(s0 + s, cc);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) buf[s][q] = __ldcg(src + q * BM);
-              }
-            }
-#pragma unroll
-            for (int s = 0; s < SEG_BATCH; ++s) {
-              if (s0 + s < nseg) {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  const float x[4] = {buf[s][q].x, buf[s][q].y, buf[s][q].z, buf[s][q].w};
-#pragma unroll
-                  for (int e = 0; e < 4; ++e)
-                    v[4 * q + e] = (s0 + s == 0) ? x[e] : __fadd_rn(v[4 * q + e], x[e]);
-                }
-              }
-            }
-          }
-        }
-        if (stamps && cc == 0) stamp(10);
-        const float* prow = PIPE ? (MODE == EPI_RESID ? cpre : nullptr) : (cc == 0 ? pre0 : nullptr);
-        finalize16<NT, MODE>(p, t, cc * 16, v, ep_t, shx, rm, bar, prow,
-                             (MODE == EPI_QKV && cc == 0) ? cs0 : nullptr);
-        if (stamps && cc == 0) stamp(11);
       }
+    };
+    if (PIPE) fetch_resid(cc0);
+#pragma unroll 1
+    for (int cc = cc0; cc < cc1; ++cc) {
+      float cpre[16];
+      if (PIPE) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) cpre[j] = npre[j];
+        if (cc + 1 < cc1) fetch_resid(cc + 1);
+      }
+      float v[16];
+      tmem_ld16(tmem_base + lane_base + cc * 16, v);
+      // segments 1.. in batches: every load of a batch issued before its first add
+      constexpr int SEG_BATCH = 6;
+#pragma unroll 1
+      for (int s0 = 1; s0 < nseg; s0 += SEG_BATCH) {
+        float4 buf[SEG_BATCH][4];
+#pragma unroll
+        for (int s = 0; s < SEG_BATCH; ++s)
+          if (s0 + s < nseg) {
+            const float4* src = ws_slot(c_first + s0 + s, cc);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) buf[s][q] = ld_relaxed_f4(src + q * BM);
+          }
+#pragma unroll
+        for (int s = 0; s < SEG_BATCH; ++s)
+          if (s0 + s < nseg) {
+            const float4* src = ws_slot(c_first + s0 + s, cc);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              while (ws_empty(buf[s][q])) buf[s][q] = ld_relaxed_f4(src + q * BM);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              v[4 * q + 0] = __fadd_rn(v[4 * q + 0], buf[s][q].x);
+              v[4 * q + 1] = __fadd_rn(v[4 * q + 1], buf[s][q].y);
+              v[4 * q + 2] = __fadd_rn(v[4 * q + 2], buf[s][q].z);
+              v[4 * q + 3] = __fadd_rn(v[4 * q + 3], buf[s][q].w);
+            }
+          }
+      }
+      // re-arm the consumed slots for the next launch that uses this scratch
+      const float4 empty4 = make_float4(__uint_as_float(WS_EMPTY), __uint_as_float(WS_EMPTY),
+                                        __uint_as_float(WS_EMPTY), __uint_as_float(WS_EMPTY));
+#pragma unroll 1
+      for (int s = 1; s < nseg; ++s) {
+        float4* dst = ws_slot(c_first + s, cc);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) __stcg(dst + q * BM, empty4);
+      }
+      if (stamps && cc == 0) stamp(10);
+      const float* prow = PIPE ? (MODE == EPI_RESID ? cpre : nullptr) : (cc == 0 ? pre0 : nullptr);
+      finalize16<NT, MODE>(p, t, cc * 16, v, ep_t, shx, rm, bar, prow,
+                           (MODE == EPI_QKV && cc == 0) ? cs0 : nullptr);
+      if (stamps && cc == 0) stamp(11);
+    }
   };
   constexpr bool HELPERS = NT >= 32;
 
@@ -822,33 +837,22 @@ __global__ void __launch_bounds__(256, 1)
       mbar_wait(tmem_full, tphase);
       tc_fence_after();
       if (ep_t == 0) stamp(13);
-      // Non-final stream-K segments publish their fp32 partial (layout [cta][slot][16-column
-      // chunk][4 float4][128 features]: a warp's float4 access is 512 contiguous bytes, so
-      // publish and fold move whole lines) and the last to arrive folds all partials in
-      // segment order (deterministic). One finalize call site, so the tail's code stays
-      // compact in the instruction caches.
-      bool fin = true;
-      if (nseg > 1) {
-        const int slot = (t == t_first) ? 0 : 1;
-        float4* wsp = reinterpret_cast<float4*>(p.ws) + ((size_t)c * 2 + slot) * (NT / 16) * 4 * BM + ep_t;
+      // A tile split over several CTAs: segment 0's CTA finalizes it (see fin_chunks); any
+      // other segment publishes its partial and hands the accumulator back at once.
+      const bool fin = nseg == 1 || c == c_first;
+      if (!fin) {
 #pragma unroll 1
         for (int cc = 0; cc < NT / 16; ++cc) {
           float v[16];
           tmem_ld16(tmem_base + lane_base + cc * 16, v);
+          float4* wsp = ws_slot(c, cc);
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            __stcg(wsp + (cc * 4 + q) * BM, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+            __stcg(wsp + q * BM, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
         }
         tc_fence_before();
         mbar_arrive(tmem_empty);
-        named_bar_sync(1, 128);
-        if (ep_t == 0) {
-          sh.flag = atom_add_acq_rel(&p.counters[t], 1);
-          stamp(15);
-        }
-        named_bar_sync(1, 128);
-        fin = (sh.flag == nseg - 1);
-        named_bar_sync(1, 128);
+        if (ep_t == 0) stamp(15);
       }
       // wide launches: warps 0-3 (their roles are over once the last tile's MMAs are issued)
       // finalize the upper half of the last tile's 16-column chunks
@@ -860,12 +864,8 @@ __global__ void __launch_bounds__(256, 1)
       if (fin) {
         fin_chunks(t, 0, helped ? NT / 32 : NT / 16, ep_t, sh, 1, have_pre ? pre : nullptr, cs_pre);
         if (helped) named_bar_sync(5, 256);
-        if (nseg == 1) {
-          tc_fence_before();
-          mbar_arrive(tmem_empty);
-        } else if (ep_t == 0) {
-          p.counters[t] = 0;
-        }
+        tc_fence_before();
+        mbar_arrive(tmem_empty);
       }
       if (ep_t == 0) stamp(14);
       tphase ^= 1;
@@ -877,7 +877,7 @@ __global__ void __launch_bounds__(256, 1)
     named_bar_sync(4, 256);  // the epilogue has decided whether this CTA finalizes t_last
     if (sh.fin_last) {
       tc_fence_after();
-      EpiShared& sh2 = *reinterpret_cast<EpiShared*>(rm.kind + 5 * NT + 64 + 1 + 512);
+      EpiShared& sh2 = *reinterpret_cast<EpiShared*>(rm.kind + ((5 * NT + 64 + 1 + 512 + 3) & ~3));
       fin_chunks(t_last, NT / 32, NT / 16, threadIdx.x, sh2, 2, nullptr, nullptr);
       tc_fence_before();
       named_bar_sync(5, 256);
@@ -953,7 +953,11 @@ cudaError_t gemm_launch(const CUtensorMap& tw, const CUtensorMap& tx, const CUte
   }
 }
 
-size_t gemm_ws_floats(int num_sms) { return (size_t)num_sms * 2 * 256 * BM; }
+size_t gemm_ws_floats(int num_sms) { return (size_t)num_sms * 256 * BM; }
+
+cudaError_t gemm_ws_clear(float* ws, int num_sms, cudaStream_t s) {
+  return cudaMemsetAsync(ws, 0xFF, gemm_ws_floats(num_sms) * sizeof(float), s);
+}
 
 int gemm_stages(int nt) {
   switch (nt) {

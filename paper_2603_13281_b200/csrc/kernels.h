@@ -39,6 +39,8 @@ cudaError_t gemm_launch(const CUtensorMap& tw, const CUtensorMap& tx, const CUte
 int gemm_pick_nt(int rows);
 int gemm_stages(int nt);
 size_t gemm_ws_floats(int num_sms);
+// stream-K scratch starts (and is always left) holding the "unpublished" pattern
+cudaError_t gemm_ws_clear(float* ws, int num_sms, cudaStream_t s);
 
 // --------------------------------------------------------------- attention (attention.cu)
 struct AttnItem {

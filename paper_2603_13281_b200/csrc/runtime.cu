@@ -910,6 +910,8 @@ icr_status icr_model_create(const icr_model_config* cfg, const icr_layer_weights
   ALLOC(m->merge_cnt, rp * c.num_kv_heads * sizeof(int));
   ALLOC(m->rope, (size_t)c.max_positions * (c.head_dim / 2) * sizeof(float2));
   ALLOC(m->ws, gemm_ws_floats(m->num_sms) * sizeof(float));
+  if (gemm_ws_clear(m->ws, m->num_sms, 0) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
+    return bail(fail(ICR_CUDA, "stream-K scratch init failed"));
   {
     const int max_tiles = std::max({m->vpad, 2 * c.ffn_dim, q_dim + 2 * kv_dim, c.hidden_dim}) / 128;
     ALLOC(m->counters, (size_t)max_tiles * sizeof(int));
@@ -1396,7 +1398,11 @@ icr_status icr_bench_gemm(const void* w, const void* x, int M, int K, int rows, 
   static int* ctr = nullptr;
   static float* out = nullptr;
   static size_t out_n = 0;
-  if (!ws) CUDA_TRY(cudaMalloc(&ws, gemm_ws_floats(sms * 4) * sizeof(float)));
+  if (!ws) {
+    CUDA_TRY(cudaMalloc(&ws, gemm_ws_floats(sms * 4) * sizeof(float)));
+    CUDA_TRY(gemm_ws_clear(ws, sms * 4, 0));
+    CUDA_TRY(cudaDeviceSynchronize());
+  }
   if (!ctr) {
     CUDA_TRY(cudaMalloc(&ctr, 65536 * sizeof(int)));
     CUDA_TRY(cudaMemset(ctr, 0, 65536 * sizeof(int)));
@@ -1680,7 +1686,11 @@ icr_status icr_gemm_bf16(const void* w_dev, const void* x_dev, float* out_dev, i
     return fail(ICR_SHAPE, "icr_gemm_bf16 needs M %% 128 == 0, K %% 64 == 0 (M=%d K=%d rows=%d)", M, K, n_rows);
   cudaStream_t s = (cudaStream_t)stream;
   const int sms = query_sms();
-  if (!g_ws) CUDA_TRY(cudaMalloc(&g_ws, gemm_ws_floats(sms) * sizeof(float)));
+  if (!g_ws) {
+    CUDA_TRY(cudaMalloc(&g_ws, gemm_ws_floats(sms) * sizeof(float)));
+    CUDA_TRY(gemm_ws_clear(g_ws, sms, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+  }
   if (g_counters_n < M / 128) {
     if (g_counters) cudaFree(g_counters);
     CUDA_TRY(cudaMalloc(&g_counters, (M / 128) * sizeof(int)));
@@ -1940,6 +1950,7 @@ icr_status icr_linear_bf16(const void* w_dev, const void* x_dev, float* out_dev,
   const bool lora = rank > 0;
   do {
     if ((e = cudaMemsetAsync(scratch + ws_b, 0, off - ws_b, s)) != cudaSuccess) break;
+    if ((e = gemm_ws_clear(ws, sms, s)) != cudaSuccess) break;
     if ((e = cudaMemcpyAsync(dmeta, hmeta.data(), meta_n * sizeof(int), cudaMemcpyHostToDevice, s)) != cudaSuccess) break;
     if ((st = make_map(&wm, w_dev, M, K, 128))) break;
     // the low-rank chunk: B (tile-major, 64 columns) against the U rows; a zero chunk over a
