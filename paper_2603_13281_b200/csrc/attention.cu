@@ -353,19 +353,10 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
   }
 }
 
-// Fixed-order merge of chunk partials (attn_merge.cuh): one CTA per (row, KV group), one
-// thread per (head-in-group, 4 dims). Few threads and no shared memory: a merge CTA fits
-// beside the next GEMM's CTA, which can then start streaming its weights while the merge
-// runs. Both partial kernels (mma.sync and tcgen05) feed it.
+// Fixed-order merge of chunk partials (attn_merge.cuh) for the mma.sync path: one CTA per
+// (row, KV group), one thread per (head-in-group, 4 dims), no shared memory. (The tcgen05
+// partial kernel merges in-kernel with the same merge_unit.)
 constexpr int MERGE_THREADS = 128;
-// Long-chunk (>= 32-page) configurations: each merge CTA reserves 116 KB of shared memory it
-// never touches, so at most one shares an SM (beside one GEMM CTA of the next projection, never
-// beside a partial CTA). Launched early through PDL, the merge CTAs would otherwise pile onto
-// the few SMs the partial grid leaves free, and the merge is bound by each SM's L1 bandwidth
-// (measured at C4: ~6 CTAs per SM, 2.9 us of merge after the partials; spread: see DESIGN).
-// Short-chunk decode keeps the compact launch: its merge is small and a spread merge would wait
-// for partial CTAs to retire before it can even start (measured: +21 us per C2 step).
-constexpr int MERGE_SPREAD_SMEM = 116 * 1024;
 
 template <int HD>
 __global__ void __launch_bounds__(MERGE_THREADS)
@@ -401,17 +392,12 @@ template <int HD>
 static cudaError_t attn_launch_hd(const AttnLaunch& a, cudaStream_t s) {
   if (use_tc(HD)) {
     cudaError_t e = attn_tc_partial_launch(a, a.chunk_tokens / 16, s);
-    if (e != cudaSuccess) return e;
+    // long chunks (>= 32 pages) merge inside the partial kernel; short-chunk (decode)
+    // launches keep the compact merge kernel: its small CTAs share SMs with the next GEMM's,
+    // which streams its weights meanwhile (measured: in-kernel costs the C2 step +0.06 ms)
+    if (e != cudaSuccess || a.chunk_tokens >= 32 * 16) return e;
     const int mthreads = std::min(MERGE_THREADS, ((a.group * HD / 4 + 31) / 32) * 32);
-    static bool mattr = false;
-    if (!mattr) {
-      e = cudaFuncSetAttribute(attn_merge_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               MERGE_SPREAD_SMEM);
-      if (e != cudaSuccess) return e;
-      mattr = true;
-    }
-    const size_t msmem = a.chunk_tokens >= 32 * 16 ? (size_t)MERGE_SPREAD_SMEM : 0;
-    return launch_pdl(attn_merge_kernel<HD>, dim3(a.n_rows, a.num_kv_heads), dim3(mthreads), msmem, s,
+    return launch_pdl(attn_merge_kernel<HD>, dim3(a.n_rows, a.num_kv_heads), dim3(mthreads), 0, s,
                       a.part_o, a.part_ml, a.row_pos, a.row_kind, a.num_heads, a.group,
                       a.max_chunks, a.chunk_tokens, a.out, a.out_ld,
                       a.trace ? a.trace + 4096 * 16 : nullptr, a.span);

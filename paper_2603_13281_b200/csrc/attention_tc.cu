@@ -25,6 +25,7 @@
 // which CTA runs it.
 #include "kernels.h"
 #include "ptx.cuh"
+#include "attn_merge.cuh"
 
 namespace icr {
 
@@ -84,6 +85,15 @@ __device__ __forceinline__ void cp_async16_s(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
 }
 
+// The in-kernel merge as a call: its 24-chunk register batch gets its own allocation instead
+// of raising the pressure of the whole kernel (inlined, the long-chunk variant spills).
+__device__ __noinline__ void merge_unit_call(const float* __restrict__ part_o,
+                                             const float2* __restrict__ part_ml, int kind, int nch,
+                                             int r, int g, int num_heads, int group, int max_chunks,
+                                             __nv_bfloat16* __restrict__ out, int out_ld, int lt) {
+  merge_unit<128>(part_o, part_ml, kind, nch, r, g, num_heads, group, max_chunks, out, out_ld, lt, 128);
+}
+
 // Persistent: CTA c runs the (item, KV head) units sched_units[sched_off[c] .. sched_off[c+1])
 // (a host LPT schedule over min(#SMs, units) CTAs, one per SM). Every role walks the same unit
 // list, so each knows the item sequence without communication; mbarrier phases follow a
@@ -101,7 +111,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                    int num_heads, int max_chunks, float scale, float* __restrict__ part_o,
                    float2* __restrict__ part_ml, const int* __restrict__ sched_off,
                    const int* __restrict__ sched_units, unsigned long long* __restrict__ trace,
-                   int chunk_tokens, unsigned long long* __restrict__ span) {
+                   int chunk_tokens, unsigned long long* __restrict__ span,
+                   const int* __restrict__ row_kind, int n_rows, __nv_bfloat16* __restrict__ out,
+                   int out_ld, int* __restrict__ merge_sync) {
   using L = TcLayout;
   extern __shared__ __align__(1024) uint8_t tc_smem[];
   uint8_t* smem = tc_smem;  // no static shared memory: the dynamic window starts 1024-aligned
@@ -610,6 +622,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       // (each thread 256 contiguous bytes of its entry's row) ----------------
       mbar_wait(o_final, n & 1);  // the unit's last P.V landed (single phase per unit)
       tc_fence_after();
+      // the partial buffers (and the merge counters) belong to this launch only once the
+      // previous kernel has completed
+      if (k == k_begin) pdl_wait();
       if (r == 0 && half == 0) stamp(0);
       named_bar_sync(1 + quarter, 64);
       const float l = red[r] + red[128 + r];
@@ -663,6 +678,43 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<L::TMEM_COLS>(tmem_base);
+  if constexpr (kNarrow) {
+    // ---------------- merge, in-kernel (long-chunk configurations): every CTA publishes its
+    // units' partials (the barrier orders all of the CTA's partial stores before thread 0's
+    // release), then merges (row, KV head) tasks cta + i * G, one per 128-thread group at a
+    // time, once every unit of the launch is in -- no second launch and no PDL hand-off on
+    // the critical path. The fold is merge_unit (attn_merge.cuh), the same fixed-order
+    // function as the separate merge kernel of short-chunk configurations.
+    int* done = merge_sync;
+    int* exited = merge_sync + 1;
+    if (threadIdx.x == 0) {
+      stamp(8);
+      red_add_release(done, k_end - k_begin);
+    }
+    const int total = sched_off[gridDim.x];
+    const int grp = threadIdx.x >> 7, lt = threadIdx.x & 127;
+    const int ngrp = TC_THREADS / 128;
+    bool waited = false;
+    for (int task = cta + grp * (int)gridDim.x; task < n_rows * num_kv_heads;
+         task += ngrp * (int)gridDim.x) {
+      const int r = task / num_kv_heads, g = task % num_kv_heads;
+      const int kind = row_kind[r], nch = row_pos[r] / chunk_tokens + 1;  // before the wait
+      if (!waited) {
+        if (lt == 0)
+          while (ld_acquire(done) < total) __nanosleep(32);
+        named_bar_sync(1 + grp, 128);
+        if (grp == 0 && lt == 0) stamp(10);
+        waited = true;
+      }
+      merge_unit_call(part_o, part_ml, kind, nch, r, g, num_heads, group, max_chunks, out, out_ld, lt);
+    }
+    __syncthreads();
+    // the last CTA out re-arms the counters (every poll of `done` precedes its CTA's exit count)
+    if (threadIdx.x == 0 && atomicAdd(exited, 1) == (int)gridDim.x - 1) {
+      atomicExch(done, 0);
+      atomicExch(exited, 0);
+    }
+  }
   if (threadIdx.x == 0) {
     stamp(9);
     if (span != nullptr) atomicMax(span + 1, globaltimer());
@@ -690,7 +742,8 @@ cudaError_t attn_tc_partial_launch(const AttnLaunch& a, int chunk_pages, cudaStr
   return launch_pdl(kern, dim3(grid), dim3(TC_THREADS), L::SMEM, s,
                     a.tm_k, a.tm_v, a.tm_k8, a.tm_v8, a.q, a.q_ld, a.num_kv_heads, a.group, a.items, a.item_pages,
                     a.item_rows, a.row_pos, a.num_heads, a.max_chunks, a.scale, a.part_o, a.part_ml,
-                    a.sched_off, a.sched_units, a.trace, a.chunk_tokens, a.span);
+                    a.sched_off, a.sched_units, a.trace, a.chunk_tokens, a.span,
+                    a.row_kind, a.n_rows, a.out, a.out_ld, a.merge_cnt);
 }
 
 }  // namespace icr

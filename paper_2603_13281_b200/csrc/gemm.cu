@@ -599,6 +599,7 @@ __global__ void __launch_bounds__(256, 1)
             }
           }
       }
+      if (stamps && cc == 0) stamp(10);
       // re-arm the consumed slots for the next launch that uses this scratch
       const float4 empty4 = make_float4(__uint_as_float(WS_EMPTY), __uint_as_float(WS_EMPTY),
                                         __uint_as_float(WS_EMPTY), __uint_as_float(WS_EMPTY));
@@ -608,7 +609,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
         for (int q = 0; q < 4; ++q) __stcg(dst + q * BM, empty4);
       }
-      if (stamps && cc == 0) stamp(10);
+      if (stamps && cc == 0) stamp(5);
       const float* prow = PIPE ? (MODE == EPI_RESID ? cpre : nullptr) : (cc == 0 ? pre0 : nullptr);
       finalize16<NT, MODE>(p, t, cc * 16, v, ep_t, shx, rm, bar, prow,
                            (MODE == EPI_QKV && cc == 0) ? cs0 : nullptr);
@@ -885,7 +886,6 @@ __global__ void __launch_bounds__(256, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 0) stamp(5);
   if (warp == 2) tmem_dealloc<C::TMEM_COLS>(tmem_base);
   if (threadIdx.x == 0) stamp(9);  // exit
 }

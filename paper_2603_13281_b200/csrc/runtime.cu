@@ -908,6 +908,8 @@ icr_status icr_model_create(const icr_model_config* cfg, const icr_layer_weights
   ALLOC(m->part_o, rp * c.num_heads * m->max_chunks * c.head_dim * sizeof(float));
   ALLOC(m->part_ml, rp * c.num_heads * m->max_chunks * sizeof(float2));
   ALLOC(m->merge_cnt, rp * c.num_kv_heads * sizeof(int));
+  if (cudaMemset(m->merge_cnt, 0, rp * c.num_kv_heads * sizeof(int)) != cudaSuccess)
+    return bail(fail(ICR_CUDA, "merge counter init failed"));
   ALLOC(m->rope, (size_t)c.max_positions * (c.head_dim / 2) * sizeof(float2));
   ALLOC(m->ws, gemm_ws_floats(m->num_sms) * sizeof(float));
   if (gemm_ws_clear(m->ws, m->num_sms, 0) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
@@ -1506,6 +1508,9 @@ icr_status icr_bench_attention(const void* q_dev, const void* k_pages, const voi
   CUDA_TRY(cudaMalloc(&d_rows, std::max<size_t>(plan.rows.size(), 1) * sizeof(int2)));
   CUDA_TRY(cudaMalloc(&d_po, (size_t)n_rows * num_heads * max_chunks * head_dim * sizeof(float)));
   CUDA_TRY(cudaMalloc(&d_pml, (size_t)n_rows * num_heads * max_chunks * sizeof(float2)));
+  int* d_mcnt = nullptr;
+  CUDA_TRY(cudaMalloc(&d_mcnt, 2 * sizeof(int)));
+  CUDA_TRY(cudaMemset(d_mcnt, 0, 2 * sizeof(int)));
   int* d_sched = nullptr;
   CUDA_TRY(cudaMalloc(&d_sched, (plan.sched_off.size() + plan.sched_units.size()) * sizeof(int)));
   CUDA_TRY(cudaMemcpy(d_sched, plan.sched_off.data(), plan.sched_off.size() * sizeof(int), cudaMemcpyHostToDevice));
@@ -1545,6 +1550,7 @@ icr_status icr_bench_attention(const void* q_dev, const void* k_pages, const voi
   a.num_sms = query_sms();
   a.out = (__nv_bfloat16*)out_dev;
   a.out_ld = num_heads * head_dim;
+  a.merge_cnt = d_mcnt;
   {
     int maxpage = 0;
     for (size_t i = 0; i < plan.pages.size(); ++i) maxpage = std::max(maxpage, plan.pages[i]);
@@ -1669,7 +1675,7 @@ icr_status icr_bench_attention(const void* q_dev, const void* k_pages, const voi
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  void* bufs[] = {d_pos, d_kind, d_pages, d_n, d_items, d_rows, d_po, d_pml, d_sched, d_span};
+  void* bufs[] = {d_pos, d_kind, d_pages, d_n, d_items, d_rows, d_po, d_pml, d_sched, d_span, d_mcnt};
   for (void* p : bufs) cudaFree(p);
   if (e != cudaSuccess) return fail(ICR_CUDA, "attention bench: %s", cudaGetErrorString(e));
   return ICR_OK;

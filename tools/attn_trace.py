@@ -34,9 +34,9 @@ def main():
         if l[0] == "launch":
             print(f"stamp kernel before the launch {l[2]} us, after it {l[3]} us (relative to the first CTA)")
     names = ["o_final", "q_loaded", "s0_ready", "q_wait", "loop_done", "epi_done", "entry", "k_pdl",
-             "-", "cta_end", "merge_go", "merge_done"]
+             "published", "cta_end", "merge_go", "merge_done"]
     print(f"partial CTAs {len(part)}")
-    for k in (6, 7, 3, 1, 2, 4, 0, 5, 9, 10, 11):
+    for k in (6, 7, 3, 1, 2, 4, 0, 5, 8, 10, 9, 11):
         if k >= part.shape[1]:
             continue
         col = part[:, k]
