@@ -685,13 +685,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // time, once every unit of the launch is in -- no second launch and no PDL hand-off on
     // the critical path. The fold is merge_unit (attn_merge.cuh), the same fixed-order
     // function as the separate merge kernel of short-chunk configurations.
-    int* done = merge_sync;
-    int* exited = merge_sync + 1;
+    // One 64-bit counter that never needs re-arming: every launch adds exactly 2^20 to it
+    // (CTA 0 adds 2^20 - (G - 1), the others 1, each after publishing its units), so the
+    // launch is complete when the counter reaches the next multiple of 2^20 above the value
+    // a CTA saw. (Launches are ordered: a CTA adds only after griddepcontrol.wait, i.e. after
+    // the previous launch, whose adds all precede it.)
+    unsigned long long* done = reinterpret_cast<unsigned long long*>(merge_sync);
+    unsigned long long* s_target = reinterpret_cast<unsigned long long*>(red);
     if (threadIdx.x == 0) {
       stamp(8);
-      red_add_release(done, k_end - k_begin);
+      const unsigned long long mine = cta == 0 ? (1ull << 20) - (gridDim.x - 1) : 1ull;
+      const unsigned long long old = atom_add_release_u64(done, mine);
+      *s_target = ((old >> 20) + 1) << 20;
     }
-    const int total = sched_off[gridDim.x];
+    __syncthreads();
+    const unsigned long long target = *s_target;
     const int grp = threadIdx.x >> 7, lt = threadIdx.x & 127;
     const int ngrp = TC_THREADS / 128;
     bool waited = false;
@@ -701,18 +709,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int kind = row_kind[r], nch = row_pos[r] / chunk_tokens + 1;  // before the wait
       if (!waited) {
         if (lt == 0)
-          while (ld_acquire(done) < total) __nanosleep(32);
+          while (ld_acquire_u64(done) < target) __nanosleep(32);
         named_bar_sync(1 + grp, 128);
         if (grp == 0 && lt == 0) stamp(10);
         waited = true;
       }
       merge_unit_call(part_o, part_ml, kind, nch, r, g, num_heads, group, max_chunks, out, out_ld, lt);
-    }
-    __syncthreads();
-    // the last CTA out re-arms the counters (every poll of `done` precedes its CTA's exit count)
-    if (threadIdx.x == 0 && atomicAdd(exited, 1) == (int)gridDim.x - 1) {
-      atomicExch(done, 0);
-      atomicExch(exited, 0);
     }
   }
   if (threadIdx.x == 0) {

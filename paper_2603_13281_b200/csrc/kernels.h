@@ -75,7 +75,7 @@ struct AttnLaunch {
   float scale;
   float* part_o;
   float2* part_ml;
-  int* merge_cnt;  // tcgen05 path: {units done, CTAs exited} of the in-kernel merge (self-resetting, zeroed at allocation)
+  int* merge_cnt;  // tcgen05 long-chunk path: 64-bit launch counter of the in-kernel merge (zeroed once, 8-byte aligned)
   CUtensorMap tm_k, tm_v;  // page-arena maps: one 64-dim half page of one KV head per box
   CUtensorMap tm_k8, tm_v8;  // the same arena as runs: 8 consecutive page ids of one KV head,
                              // both halves, in one box (32 KB, [half][page][key][128 B])

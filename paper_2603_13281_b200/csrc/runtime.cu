@@ -1765,8 +1765,8 @@ icr_status icr_paged_attention(const void* q_dev, const void* k_pages, const voi
   CUDA_TRY(cudaMalloc(&d_po, (size_t)n_rows * num_heads * max_chunks * head_dim * sizeof(float)));
   CUDA_TRY(cudaMalloc(&d_pml, (size_t)n_rows * num_heads * max_chunks * sizeof(float2)));
   const size_t cnt_n = (size_t)n_rows * num_kv_heads;
-  CUDA_TRY(cudaMalloc(&d_cnt, cnt_n * sizeof(int)));
-  CUDA_TRY(cudaMemsetAsync(d_cnt, 0, cnt_n * sizeof(int), s));
+  CUDA_TRY(cudaMalloc(&d_cnt, std::max<size_t>(cnt_n, 2) * sizeof(int)));
+  CUDA_TRY(cudaMemsetAsync(d_cnt, 0, std::max<size_t>(cnt_n, 2) * sizeof(int), s));
   CUDA_TRY(cudaMalloc(&d_sched, (plan.sched_off.size() + plan.sched_units.size()) * sizeof(int)));
   CUDA_TRY(cudaMemcpyAsync(d_sched, plan.sched_off.data(), plan.sched_off.size() * sizeof(int),
                            cudaMemcpyHostToDevice, s));
