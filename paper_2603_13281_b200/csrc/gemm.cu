@@ -29,7 +29,9 @@ struct Cfg {
   static constexpr uint32_t STAGE = W_BYTES + X_BYTES;
   static constexpr int STAGES_RAW = (int)((220 * 1024 - aux_smem<NT>()) / STAGE);
   static constexpr int STAGES = STAGES_RAW > 16 ? 16 : STAGES_RAW;
-  static constexpr uint32_t TMEM_COLS = NT < 32 ? 32 : NT;
+  // two accumulator buffers of NT columns: a CTA's next (tile, row group) accumulates while
+  // the epilogue drains the previous one
+  static constexpr uint32_t TMEM_COLS = 2 * NT < 32 ? 32 : 2 * NT;
   static constexpr uint32_t IDESC = idesc_bf16_f32(BM, NT);
   static constexpr size_t SMEM = 1024 + (size_t)STAGES * STAGE + aux_smem<NT>();
 };
@@ -154,7 +156,7 @@ struct alignas(16) EpiShared {
   int red_idx[64];
 };
 // barriers (<= 16 stages) + TMEM slot, EpiShared, row metadata + SGMV table, helper EpiShared
-static_assert((2 * 16 + 2) * 8 + 16 + 2 * sizeof(EpiShared) + (5 * 16 + 64 + 1 + 512 + 3) * 4 <=
+static_assert((2 * 16 + 4) * 8 + 16 + 2 * sizeof(EpiShared) + (5 * 16 + 64 + 1 + 512 + 3) * 4 <=
                   aux_smem<16>(), "aux shared-memory layout overflows");
 
 
@@ -188,9 +190,10 @@ struct RowMeta {
 };
 
 template <int NT, int MODE>
-__device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0, float (&v)[16],
-                                           int ep_t, EpiShared& sh, const RowMeta& rm, int bar,
-                                           const float* pre = nullptr, const float2* cs_pre = nullptr) {
+__device__ __forceinline__ void finalize16(const GemmParams& p, int row0, int n_rows, int tile, int n0,
+                                           float (&v)[16], int ep_t, EpiShared& sh, const RowMeta& rm,
+                                           int bar, const float* pre = nullptr,
+                                           const float2* cs_pre = nullptr) {
   const int m = tile * BM + ep_t;
   // row kinds of the 16 rows (-1: padding or beyond n_rows, staged that way)
   int kd[16];
@@ -208,7 +211,7 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int n = n0 + j;
-        if (n < p.n_rows) p.out_f32[(size_t)(p.row0 + n) * p.ld_out + m] = v[j];
+        if (n < n_rows) p.out_f32[(size_t)(row0 + n) * p.ld_out + m] = v[j];
       }
   } else if constexpr (MODE == EPI_RESID) {
       // Every row's math first (16 independent chains the scheduler can interleave), then
@@ -219,15 +222,15 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
       for (int j = 0; j < 16; ++j) {
         const int n = n0 + j;
         old[j] = pre != nullptr ? pre[j]
-                 : kd[j] >= 0 ? __ldcg(p.resid + (size_t)(p.row0 + n) * p.M + m) : 0.f;
+                 : kd[j] >= 0 ? __ldcg(p.resid + (size_t)(row0 + n) * p.M + m) : 0.f;
       }
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         xn[j] = __fadd_rn(old[j], v[j]);
         sq[j] = kd[j] >= 0 ? __fmul_rn(xn[j], xn[j]) : 0.f;
       }
-      float* rp = p.resid + (size_t)(p.row0 + n0) * p.M + m;
-      __nv_bfloat16* bp = p.resid_bf16 + (size_t)(p.row0 + n0) * p.M + m;
+      float* rp = p.resid + (size_t)(row0 + n0) * p.M + m;
+      __nv_bfloat16* bp = p.resid_bf16 + (size_t)(row0 + n0) * p.M + m;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         if (kd[j] >= 0) {
@@ -240,10 +243,10 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
       named_bar_sync(bar, 128);
       if (ep_t < 16) {
         const int n = n0 + ep_t;
-        if (n < p.n_rows) {
+        if (n < n_rows) {
           const float s = ((sh.red_val[ep_t] + sh.red_val[16 + ep_t]) + sh.red_val[32 + ep_t]) +
                           sh.red_val[48 + ep_t];
-          p.out_ssq[(size_t)tile * p.ss_stride + p.row0 + n] = s;
+          p.out_ssq[(size_t)tile * p.ss_stride + row0 + n] = s;
         }
       }
       named_bar_sync(bar, 128);
@@ -255,7 +258,7 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
         f[j] = __fmul_rn(silu_ref(v[j]), partner);
       }
       if ((m & 1) == 0) {
-        __nv_bfloat16* op = p.out_bf16 + (size_t)(p.row0 + n0) * (p.M >> 1) + (m >> 1);
+        __nv_bfloat16* op = p.out_bf16 + (size_t)(row0 + n0) * (p.M >> 1) + (m >> 1);
 #pragma unroll
         for (int j = 0; j < 16; ++j)
           if (kd[j] >= 0) op[(size_t)j * (p.M >> 1)] = __float2bfloat16_rn(f[j]);
@@ -288,7 +291,7 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
         out[j] = region == 2 ? v[j] : ((i & 1) == 0 ? even : odd);
       }
       if (region == 0) {
-        __nv_bfloat16* qp = p.out_bf16 + (size_t)(p.row0 + n0) * p.q_dim + m;
+        __nv_bfloat16* qp = p.out_bf16 + (size_t)(row0 + n0) * p.q_dim + m;
 #pragma unroll
         for (int j = 0; j < 16; ++j)
           if (kd[j] >= 0) qp[(size_t)j * p.q_dim] = __float2bfloat16_rn(out[j]);
@@ -309,7 +312,7 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
       const int wq = ep_t >> 5, ln = ep_t & 31;
       float vals[16];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) vals[j] = (m < p.m_valid && n0 + j < p.n_rows) ? v[j] : -INFINITY;
+      for (int j = 0; j < 16; ++j) vals[j] = (m < p.m_valid && n0 + j < n_rows) ? v[j] : -INFINITY;
       float bv;
       int bi;
       warp_argmax16(vals, m, ln, bv, bi);
@@ -324,8 +327,8 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int tile, int n0
           if (ov > val || (ov == val && oi < idx)) { val = ov; idx = oi; }
         }
         const int n = n0 + ep_t;
-        if (n < p.n_rows)
-          p.tile_best[(size_t)tile * p.best_stride + p.row0 + n] =
+        if (n < n_rows)
+          p.tile_best[(size_t)tile * p.best_stride + row0 + n] =
               make_float2(val, __int_as_float(idx));
       }
       named_bar_sync(bar, 128);
@@ -470,9 +473,9 @@ __global__ void __launch_bounds__(256, 1)
   const int NS = ring_stages<NT>(p.stages);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NS * C::STAGE);
   uint64_t* empty = full + NS;
-  uint64_t* tmem_full = empty + NS;
-  uint64_t* tmem_empty = tmem_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
+  uint64_t* tmem_full = empty + NS;   // [2] per accumulator buffer
+  uint64_t* tmem_empty = tmem_full + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
   EpiShared& sh = *reinterpret_cast<EpiShared*>(tmem_slot + 4);
   RowMeta rm;
   rm.kind = reinterpret_cast<int*>(&sh + 1);
@@ -507,11 +510,11 @@ __global__ void __launch_bounds__(256, 1)
   const long long u_begin = sp.ubegin(c), u_end = sp.ubegin(c + 1);
   const int t_first = (int)((unsigned)u_begin / (unsigned)sp.Ut);
   const int t_last = (int)((unsigned)(u_end - 1) / (unsigned)sp.Ut);
+  const int ntiles = t_last - t_first + 1;
 
   if (warp == 0 && elect_one()) {
     for (int i = 0; i < NS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    mbar_init(tmem_full, 1);
-    mbar_init(tmem_empty, 128);
+    for (int b = 0; b < 2; ++b) { mbar_init(&tmem_full[b], 1); mbar_init(&tmem_empty[b], 128); }
     fence_barrier_init();
     tma_prefetch_desc(&tm_w);
     tma_prefetch_desc(&tm_x);
@@ -541,8 +544,9 @@ __global__ void __launch_bounds__(256, 1)
   // order -- fixed by (M, K, grid) only -- polling each 4-byte word until it is not
   // WS_EMPTY (no atomics, no fences: one L2 round trip when the partials are there), and
   // re-arms the slots it consumed. Wide launches software-pipeline the residual rows.
-  auto fin_chunks = [&](int t, int cc0, int cc1, int ep_t, EpiShared& shx, int bar, const float* pre0,
-                        const float2* cs0) {
+  auto fin_chunks = [&](int t, int b, int cc0, int cc1, int ep_t, EpiShared& shx, int bar,
+                        const float* pre0, const float2* cs0) {
+    const int grow0 = p.row0, gnr = p.n_rows;
     const long long t0 = (long long)t * sp.Ut;
     const int c_first = sp.owner(t0), c_last = sp.owner(t0 + sp.Ut - 1);
     const int nseg = c_last - c_first + 1;
@@ -556,7 +560,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const int n = cc * 16 + j;
-          npre[j] = (n < p.n_rows) ? __ldcg(p.resid + (size_t)(p.row0 + n) * p.M + m) : 0.f;
+          npre[j] = (n < gnr) ? __ldcg(p.resid + (size_t)(grow0 + n) * p.M + m) : 0.f;
         }
       }
     };
@@ -570,7 +574,7 @@ __global__ void __launch_bounds__(256, 1)
         if (cc + 1 < cc1) fetch_resid(cc + 1);
       }
       float v[16];
-      tmem_ld16(tmem_base + lane_base + cc * 16, v);
+      tmem_ld16(tmem_base + b * NT + lane_base + cc * 16, v);
       // segments 1.. in batches: every load of a batch issued before its first add
       constexpr int SEG_BATCH = 6;
 #pragma unroll 1
@@ -611,7 +615,7 @@ __global__ void __launch_bounds__(256, 1)
       }
       if (stamps && cc == 0) stamp(5);
       const float* prow = PIPE ? (MODE == EPI_RESID ? cpre : nullptr) : (cc == 0 ? pre0 : nullptr);
-      finalize16<NT, MODE>(p, t, cc * 16, v, ep_t, shx, rm, bar, prow,
+      finalize16<NT, MODE>(p, grow0, gnr, t, cc * 16, v, ep_t, shx, rm, bar, prow,
                            (MODE == EPI_QKV && cc == 0) ? cs0 : nullptr);
       if (stamps && cc == 0) stamp(11);
     }
@@ -669,6 +673,7 @@ __global__ void __launch_bounds__(256, 1)
           tma_load_2d_hint(st, &tm_w, &full[stage], ch * BK, cu.t * BM, pol);
       };
       auto load_x = [&](const Cursor& cu, int stage) {
+        const int xr = x_row0;
         int ch;
         const bool lo = chunk_of(cu, ch);
         uint8_t* dst = smem + (size_t)stage * C::STAGE + W_BYTES;
@@ -683,9 +688,9 @@ __global__ void __launch_bounds__(256, 1)
             asm volatile("fence.proxy.async.global;\n" ::: "memory");
             lora_ready = true;
           }
-          tma_load_2d(dst, &tm_lu, &full[stage], ch * BK, x_row0);
+          tma_load_2d(dst, &tm_lu, &full[stage], ch * BK, xr);
         } else {
-          tma_load_2d(dst, &tm_x, &full[stage], ch * BK, x_row0);
+          tma_load_2d(dst, &tm_x, &full[stage], ch * BK, xr);
         }
       };
       Cursor start;
@@ -720,12 +725,15 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp == 1) {
     // ---------------- tcgen05.mma issuer ----------------
     int stage = 0;
-    uint32_t phase = 0, tphase = 0;
-    for (int t = t_first; t <= t_last; ++t) {
+    uint32_t phase = 0;
+    for (int job = 0; job < ntiles; ++job) {
+      // the CTA's tiles alternate between the two accumulator buffers: a tile's MMAs never
+      // wait for the previous tile's epilogue (publish) to drain TMEM
+      const int t = t_first + job, bf = job & 1;
       const long long t0 = (long long)t * sp.Ut;
       const int kb = (int)((u_begin > t0 ? u_begin : t0) - t0);
       const int ke = (int)((u_end < t0 + sp.Ut ? u_end : t0 + sp.Ut) - t0);
-      mbar_wait(tmem_empty, tphase ^ 1);
+      mbar_wait(&tmem_empty[bf], ((job >> 1) & 1) ^ 1);
       tc_fence_after();
       for (int k = kb; k < ke; ++k) {
         mbar_wait(&full[stage], phase);
@@ -733,23 +741,22 @@ __global__ void __launch_bounds__(256, 1)
         if (p.skip_mma) {
           if (elect_one()) {
             mbar_arrive(&empty[stage]);
-            if (k == ke - 1) mbar_arrive(tmem_full);
+            if (k == ke - 1) mbar_arrive(&tmem_full[bf]);
           }
         } else if (elect_one()) {
           const uint32_t a = smem_u32(smem + (size_t)stage * C::STAGE);
           const uint32_t b = a + W_BYTES;
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
-            tc_mma_bf16(tmem_base, sdesc_kmajor_sw128(a + kk * 32), sdesc_kmajor_sw128(b + kk * 32),
-                        C::IDESC, (k > kb || kk > 0) ? 1u : 0u);
+            tc_mma_bf16(tmem_base + bf * NT, sdesc_kmajor_sw128(a + kk * 32),
+                        sdesc_kmajor_sw128(b + kk * 32), C::IDESC, (k > kb || kk > 0) ? 1u : 0u);
           }
           tc_commit(&empty[stage]);
-          if (k == ke - 1) { tc_commit(tmem_full); stamp(12); }
+          if (k == ke - 1) { tc_commit(&tmem_full[bf]); stamp(12); }
         }
         __syncwarp();
         if (++stage == NS) { stage = 0; phase ^= 1; }
       }
-      tphase ^= 1;
     }
   } else if (warp == 2 || warp == 3) {
     // ---------------- LoRA shrink (SGMV) on the two otherwise idle warps ----------------
@@ -779,12 +786,13 @@ __global__ void __launch_bounds__(256, 1)
     // the launch that used reset_sync has completed (PDL): re-arm its shrink counter for
     // its next use (two launches later at the earliest)
     if (p.reset_sync != nullptr && blockIdx.x == 0 && ep_t == 0) *p.reset_sync = 0;
+    const int grow0 = p.row0, gnr = p.n_rows;
     // stage this launch's row metadata (+ RMSNorm inverse) in smem
     for (int n = ep_t; n < NT; n += 128) {
       int kind = -1, ad = -1, pos = 0, kvoff = 0;
       float inv = 1.f;
-      if (n < p.n_rows) {
-        const int gn = p.row0 + n;
+      if (n < gnr) {
+        const int gn = grow0 + n;
         kind = p.row_kind ? p.row_kind[gn] : 0;
         ad = p.row_adapter ? p.row_adapter[gn] : -1;
         pos = p.row_pos ? p.row_pos[gn] : 0;
@@ -806,8 +814,8 @@ __global__ void __launch_bounds__(256, 1)
       rm.inv[n] = inv;
     }
     named_bar_sync(1, 128);
-    uint32_t tphase = 0;
     for (int t = t_first; t <= t_last; ++t) {
+      const int job = t - t_first, bf = job & 1;
       const long long t0 = (long long)t * sp.Ut;
       const int c_first = sp.owner(t0), c_last = sp.owner(t0 + sp.Ut - 1);
       const int nseg = c_last - c_first + 1;
@@ -819,7 +827,7 @@ __global__ void __launch_bounds__(256, 1)
         const int m = t * BM + ep_t;
 #pragma unroll
         for (int j = 0; j < 16; ++j)
-          pre[j] = (j < p.n_rows && rm.kind[j] >= 0) ? __ldcg(p.resid + (size_t)(p.row0 + j) * p.M + m) : 0.f;
+          pre[j] = (j < gnr && rm.kind[j] >= 0) ? __ldcg(p.resid + (size_t)(grow0 + j) * p.M + m) : 0.f;
       }
       // likewise the RoPE factors of the first 16 rows (the table lines are evicted by the
       // weight stream between layers: an HBM round trip under load)
@@ -831,11 +839,11 @@ __global__ void __launch_bounds__(256, 1)
         const int i = (m - base) % p.head_dim;
 #pragma unroll
         for (int j = 0; j < 16; ++j)
-          cs_pre[j] = (region < 2 && j < p.n_rows && rm.kind[j] >= 0)
+          cs_pre[j] = (region < 2 && j < gnr && rm.kind[j] >= 0)
                           ? __ldg(p.rope + (size_t)rm.pos[j] * (p.head_dim >> 1) + (i >> 1))
                           : make_float2(1.f, 0.f);
       }
-      mbar_wait(tmem_full, tphase);
+      mbar_wait(&tmem_full[bf], (job >> 1) & 1);
       tc_fence_after();
       if (ep_t == 0) stamp(13);
       // A tile split over several CTAs: segment 0's CTA finalizes it (see fin_chunks); any
@@ -845,14 +853,14 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll 1
         for (int cc = 0; cc < NT / 16; ++cc) {
           float v[16];
-          tmem_ld16(tmem_base + lane_base + cc * 16, v);
+          tmem_ld16(tmem_base + bf * NT + lane_base + cc * 16, v);
           float4* wsp = ws_slot(c, cc);
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             __stcg(wsp + q * BM, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
         }
         tc_fence_before();
-        mbar_arrive(tmem_empty);
+        mbar_arrive(&tmem_empty[bf]);
         if (ep_t == 0) stamp(15);
       }
       // wide launches: warps 0-3 (their roles are over once the last tile's MMAs are issued)
@@ -863,13 +871,12 @@ __global__ void __launch_bounds__(256, 1)
         named_bar_sync(4, 256);
       }
       if (fin) {
-        fin_chunks(t, 0, helped ? NT / 32 : NT / 16, ep_t, sh, 1, have_pre ? pre : nullptr, cs_pre);
+        fin_chunks(t, bf, 0, helped ? NT / 32 : NT / 16, ep_t, sh, 1, have_pre ? pre : nullptr, cs_pre);
         if (helped) named_bar_sync(5, 256);
         tc_fence_before();
-        mbar_arrive(tmem_empty);
+        mbar_arrive(&tmem_empty[bf]);
       }
       if (ep_t == 0) stamp(14);
-      tphase ^= 1;
     }
   }
 
@@ -879,7 +886,7 @@ __global__ void __launch_bounds__(256, 1)
     if (sh.fin_last) {
       tc_fence_after();
       EpiShared& sh2 = *reinterpret_cast<EpiShared*>(rm.kind + ((5 * NT + 64 + 1 + 512 + 3) & ~3));
-      fin_chunks(t_last, NT / 32, NT / 16, threadIdx.x, sh2, 2, nullptr, nullptr);
+      fin_chunks(t_last, (ntiles - 1) & 1, NT / 32, NT / 16, threadIdx.x, sh2, 2, nullptr, nullptr);
       tc_fence_before();
       named_bar_sync(5, 256);
     }
