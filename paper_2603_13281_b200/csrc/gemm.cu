@@ -19,8 +19,9 @@ __device__ __forceinline__ bool ws_empty(const float4& x) {
 // barriers, reduction scratch, staged row metadata and the LoRA U rows of the launch
 template <int NT>
 constexpr size_t aux_smem() {
-  // + SGMV segment table: slots + 1 offsets and up to 256 row ids
-  return 2048 + (size_t)NT * 5 * 4 + (64 + 1 + 512) * 4;
+  // + SGMV segment table: slots + 1 offsets and up to 256 row ids; + the residual epilogue's
+  // per-warp sum-of-squares partials of every 16-column chunk (wide launches)
+  return 2048 + (size_t)NT * 5 * 4 + (64 + 1 + 512) * 4 + (size_t)NT * 16;
 }
 
 template <int NT>
@@ -156,7 +157,7 @@ struct alignas(16) EpiShared {
   int red_idx[64];
 };
 // barriers (<= 16 stages) + TMEM slot, EpiShared, row metadata + SGMV table, helper EpiShared
-static_assert((2 * 16 + 4) * 8 + 16 + 2 * sizeof(EpiShared) + (5 * 16 + 64 + 1 + 512 + 3) * 4 <=
+static_assert((2 * 16 + 4) * 8 + 16 + 2 * sizeof(EpiShared) + (5 * 16 + 64 + 1 + 512 + 3) * 4 + 16 * 16 <=
                   aux_smem<16>(), "aux shared-memory layout overflows");
 
 
@@ -193,7 +194,7 @@ template <int NT, int MODE>
 __device__ __forceinline__ void finalize16(const GemmParams& p, int row0, int n_rows, int tile, int n0,
                                            float (&v)[16], int ep_t, EpiShared& sh, const RowMeta& rm,
                                            int bar, const float* pre = nullptr,
-                                           const float2* cs_pre = nullptr) {
+                                           const float2* cs_pre = nullptr, float* ssq_part = nullptr) {
   const int m = tile * BM + ep_t;
   // row kinds of the 16 rows (-1: padding or beyond n_rows, staged that way)
   int kd[16];
@@ -239,17 +240,23 @@ __device__ __forceinline__ void finalize16(const GemmParams& p, int row0, int n_
         }
       }
       const float wsum = warp_reduce16(sq, ln);
-      if ((ln & 1) == 0) sh.red_val[wq * 16 + ((ln >> 1) & 15)] = wsum;
-      named_bar_sync(bar, 128);
-      if (ep_t < 16) {
-        const int n = n0 + ep_t;
-        if (n < n_rows) {
-          const float s = ((sh.red_val[ep_t] + sh.red_val[16 + ep_t]) + sh.red_val[32 + ep_t]) +
-                          sh.red_val[48 + ep_t];
-          p.out_ssq[(size_t)tile * p.ss_stride + row0 + n] = s;
+      if (ssq_part != nullptr) {
+        // wide launches: the 4 warps' partials of every chunk are combined once, after the
+        // last chunk (fin_chunks) -- no barrier pair per chunk
+        if ((ln & 1) == 0) ssq_part[((n0 >> 4) * 4 + wq) * 16 + ((ln >> 1) & 15)] = wsum;
+      } else {
+        if ((ln & 1) == 0) sh.red_val[wq * 16 + ((ln >> 1) & 15)] = wsum;
+        named_bar_sync(bar, 128);
+        if (ep_t < 16) {
+          const int n = n0 + ep_t;
+          if (n < n_rows) {
+            const float s = ((sh.red_val[ep_t] + sh.red_val[16 + ep_t]) + sh.red_val[32 + ep_t]) +
+                            sh.red_val[48 + ep_t];
+            p.out_ssq[(size_t)tile * p.ss_stride + row0 + n] = s;
+          }
         }
+        named_bar_sync(bar, 128);
       }
-      named_bar_sync(bar, 128);
   } else if constexpr (MODE == EPI_SILU) {
       float f[16];
 #pragma unroll
@@ -483,6 +490,9 @@ __global__ void __launch_bounds__(256, 1)
   rm.pos = rm.ad + NT;
   rm.kvoff = rm.pos + NT;
   rm.inv = reinterpret_cast<float*>(rm.kvoff + NT);
+  // [NT/16 chunks][4 warps][16 rows] sum-of-squares partials (after the helpers' EpiShared)
+  float* ssq_part = reinterpret_cast<float*>(
+      reinterpret_cast<EpiShared*>(rm.kind + ((5 * NT + 64 + 1 + 512 + 3) & ~3)) + 1);
 
   auto stamp = [&](int slot) {
     if (p.trace != nullptr) {
@@ -616,8 +626,20 @@ __global__ void __launch_bounds__(256, 1)
       if (stamps && cc == 0) stamp(5);
       const float* prow = PIPE ? (MODE == EPI_RESID ? cpre : nullptr) : (cc == 0 ? pre0 : nullptr);
       finalize16<NT, MODE>(p, grow0, gnr, t, cc * 16, v, ep_t, shx, rm, bar, prow,
-                           (MODE == EPI_QKV && cc == 0) ? cs0 : nullptr);
+                           (MODE == EPI_QKV && cc == 0) ? cs0 : nullptr,
+                           (MODE == EPI_RESID && PIPE) ? ssq_part : nullptr);
       if (stamps && cc == 0) stamp(11);
+    }
+    if constexpr (MODE == EPI_RESID && PIPE) {
+      named_bar_sync(bar, 128);  // every warp of this group wrote its chunks' partials
+      for (int idx = ep_t; idx < (cc1 - cc0) * 16; idx += 128) {
+        const int cc = cc0 + (idx >> 4), r = idx & 15, n = cc * 16 + r;
+        if (n < gnr) {
+          const float* q = ssq_part + (cc * 4) * 16 + r;
+          p.out_ssq[(size_t)t * p.ss_stride + grow0 + n] = ((q[0] + q[16]) + q[32]) + q[48];
+        }
+      }
+      named_bar_sync(bar, 128);  // read before the next tile's chunks overwrite the partials
     }
   };
   constexpr bool HELPERS = NT >= 32;
