@@ -621,7 +621,7 @@ __global__ void __launch_bounds__(256, 1)
       for (int s = 1; s < nseg; ++s) {
         float4* dst = ws_slot(c_first + s, cc);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) __stcg(dst + q * BM, empty4);
+        for (int q = 0; q < 4; ++q) dst[q * BM] = empty4;  // weak: never ahead of later loads
       }
       if (stamps && cc == 0) stamp(5);
       const float* prow = PIPE ? (MODE == EPI_RESID ? cpre : nullptr) : (cc == 0 ? pre0 : nullptr);
