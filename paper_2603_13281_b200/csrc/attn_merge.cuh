@@ -15,8 +15,10 @@ namespace icr {
 // One thread: 4 consecutive dims [d, d + 4) of one (row, head); base = the slot of chunk 0.
 template <int HD>
 __device__ __forceinline__ void store4(__nv_bfloat16* dst, float4 O, float L) {
-  __nv_bfloat162 lo = __floats2bfloat162_rn(__fdiv_rn(O.x, L), __fdiv_rn(O.y, L));
-  __nv_bfloat162 hi = __floats2bfloat162_rn(__fdiv_rn(O.z, L), __fdiv_rn(O.w, L));
+  // one correctly rounded reciprocal, four multiplies (no division slow paths on the tail)
+  const float r = __frcp_rn(L);
+  __nv_bfloat162 lo = __floats2bfloat162_rn(__fmul_rn(O.x, r), __fmul_rn(O.y, r));
+  __nv_bfloat162 hi = __floats2bfloat162_rn(__fmul_rn(O.z, r), __fmul_rn(O.w, r));
   uint2 pk;
   pk.x = *reinterpret_cast<uint32_t*>(&lo);
   pk.y = *reinterpret_cast<uint32_t*>(&hi);
@@ -24,7 +26,9 @@ __device__ __forceinline__ void store4(__nv_bfloat16* dst, float4 O, float L) {
 }
 
 __device__ __forceinline__ void fold4(float& L, float4& O, float2 ml, float4 po, float M) {
-  const float w = exp2f(ml.x - M);
+  // MUFU exp2 (~2 ulp; the partials' own softmax uses it): exp2(-inf) = 0 for absent chunks
+  float w;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(w) : "f"(ml.x - M));
   L = fmaf(ml.y, w, L);
   O.x = fmaf(po.x, w, O.x);
   O.y = fmaf(po.y, w, O.y);
