@@ -823,9 +823,24 @@ __global__ void __launch_bounds__(256, 1)
           kvoff = (page * p.num_kv_heads * 16 + (pos & 15)) * p.head_dim;
         }
         if (p.in_ssq != nullptr) {
+          // the row's per-tile partial sums in tile order; wide launches keep 16 loads in
+          // flight per batch (decode launches measured faster with the compact loop)
           float ss = 0.f;
+          if constexpr (NT == 16) {
 #pragma unroll 4
-          for (int t = 0; t < p.ss_tiles; ++t) ss = __fadd_rn(ss, p.in_ssq[(size_t)t * p.ss_stride + gn]);
+            for (int t = 0; t < p.ss_tiles; ++t) ss = __fadd_rn(ss, p.in_ssq[(size_t)t * p.ss_stride + gn]);
+          } else {
+#pragma unroll 1
+          for (int t0 = 0; t0 < p.ss_tiles; t0 += 16) {
+            float part[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              part[q] = t0 + q < p.ss_tiles ? __ldcg(p.in_ssq + (size_t)(t0 + q) * p.ss_stride + gn) : 0.f;
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              if (t0 + q < p.ss_tiles) ss = __fadd_rn(ss, part[q]);
+          }
+          }
           inv = __fdiv_rn(1.f, sqrtf(__fadd_rn(__fdiv_rn(ss, p.ss_d), p.eps)));
         }
       }
