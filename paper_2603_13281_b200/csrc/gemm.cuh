@@ -15,15 +15,18 @@
 //  * programmatic dependent launch: the producer streams the first ring of WEIGHT tiles
 //    before `griddepcontrol.wait`, i.e. while the previous kernel is still draining --
 //    only the activation tiles depend on it;
-//  * split tiles are reduced deterministically: every segment writes its fp32 partial,
-//    the last arriving segment sums them in segment order (fixed by (M, K, grid) only,
-//    never by N) -- so a token row's result does not depend on batch composition;
+//  * split tiles are reduced deterministically: the CTA holding a tile's first K segment
+//    (its last tile) folds its own TMEM accumulator + the partials the other segments'
+//    CTAs published (polled until not WS_EMPTY), in segment order -- fixed by (M, K, grid)
+//    only, never by N -- so a token row's result does not depend on batch composition;
+//  * two TMEM accumulator buffers: a CTA's tiles alternate, so its last tile accumulates
+//    while its first tile's partial is still being published;
 //  * RMSNorm folded in: X is bf16(x) (the raw residual stream); the epilogue scales row n
 //    by inv_n = 1/sqrt(mean(x_n^2)+eps) from per-128-feature sum-of-squares partials that
 //    the residual-producing epilogue wrote (gain folded into W on upload);
-//  * LoRA shrink (SGMV, U = x A^T per decoder row) is computed by the otherwise idle
-//    epilogue warps of every CTA while the weights stream; the expand (B U) is applied in
-//    the epilogue to decoder rows only;
+//  * LoRA shrink (SGMV, U = x A^T per decoder row) is computed by the otherwise idle warps
+//    2-3 of every CTA while the weights stream; the expand (B_cat U) runs as extra tcgen05
+//    K-chunks, U being zero on encoder rows;
 //  * fused epilogues: RoPE + paged-KV write (encoder rows only), residual add (+ bf16 copy
 //    + sum-of-squares partials for the next norm), SiLU*up, LM-head per-tile argmax.
 #pragma once
@@ -96,9 +99,11 @@ struct GemmParams {
   // EPI_ARGMAX
   float2* tile_best;            // [m_tiles][best_stride] (value, index-as-float-bits)
   int best_stride;
-  // stream-K bookkeeping (scratch; counters self-reset)
-  float* ws;                    // [grid][2][N][128]
-  int* counters;                // [m_tiles]
+  // stream-K bookkeeping: ws = [grid][N/16 chunks][4 float4][128] published partials, each
+  // word WS_EMPTY when unpublished (cleared once at allocation, re-armed by the finalizer);
+  // counters: unused by the current exchange (kept for the C ABI's scratch layout)
+  float* ws;
+  int* counters;
   int max_segs;
   // tuning / diagnostics (0 = defaults)
   unsigned long long* trace;  // per-CTA %globaltimer stamps [grid][16] (null = off)
