@@ -356,13 +356,26 @@ struct ShrinkTask {
   uint4 a[NI];
 };
 
+// When the (target, slot, rank index) tasks are fewer than half the shrink warps (q, o:
+// 128 tasks for 296 warps), each slot's decoder rows are split into rsplit contiguous parts
+// handled by different warps -- every (row, j) dot is still computed whole by one warp
+// (single-slice K only), so U's bits do not change.
 template <int SL>
-__device__ __forceinline__ int shrink_tasks_total(const GemmParams& p) {
-  return p.sh_targets * p.slots * p.rank * ((p.sh_K + SL - 1) / SL);
+__device__ __forceinline__ int shrink_rsplit(const GemmParams& p, int nwarps, int n_dec) {
+  const int splits = (p.sh_K + SL - 1) / SL;
+  const int base = p.sh_targets * p.slots * p.rank * splits;
+  const int rows_per_slot = n_dec / max(p.slots, 1);
+  return splits > 1 ? 1 : max(1, min(min(8, rows_per_slot), nwarps / base));
+}
+
+template <int SL>
+__device__ __forceinline__ int shrink_tasks_total(const GemmParams& p, int nwarps, int n_dec) {
+  return p.sh_targets * p.slots * p.rank * ((p.sh_K + SL - 1) / SL) * shrink_rsplit<SL>(p, nwarps, n_dec);
 }
 
 template <int SL>
 __device__ __forceinline__ void shrink_load_a(const GemmParams& p, int task, int lane, ShrinkTask<SL>& st) {
+  // task: the (target, slot, j, slice) index, without the row split
   const int splits = (p.sh_K + SL - 1) / SL;
   const int per_t = p.slots * p.rank;
   const int ks = task % splits, combo = task / splits;
@@ -376,19 +389,22 @@ __device__ __forceinline__ void shrink_load_a(const GemmParams& p, int task, int
   }
 }
 
-template <int SL>
+template <int SL, bool SPLIT_ROWS>
 __device__ __forceinline__ void lora_shrink_tasks(const GemmParams& p, int gwarp, int nwarps, int lane,
                                                   const int* s_off, const int* s_rows, ShrinkTask<SL>& st) {
   constexpr int NI = ShrinkTask<SL>::NI;
   const int per_t = p.slots * p.rank;
   const int splits = (p.sh_K + SL - 1) / SL;
-  const int tasks = p.sh_targets * per_t * splits;
+  const int rsplit = SPLIT_ROWS ? shrink_rsplit<SL>(p, nwarps, s_off[p.slots]) : 1;
+  const int tasks = p.sh_targets * per_t * splits * rsplit;
   for (int task = gwarp; task < tasks; task += nwarps) {
-    const int ks = task % splits, combo = task / splits;
+    const int rs = task % rsplit, btask = task / rsplit;
+    const int ks = btask % splits, combo = btask / splits;
     const int t = combo / per_t, rem = combo % per_t;
     const int a = rem / p.rank, j = rem % p.rank;
-    const int r0 = s_off[a], r1 = s_off[a + 1];
-    if (task != gwarp) shrink_load_a<SL>(p, task, lane, st);  // the first was preloaded
+    const int n_a = s_off[a + 1] - s_off[a];
+    const int r0 = s_off[a] + (n_a * rs) / rsplit, r1 = s_off[a] + (n_a * (rs + 1)) / rsplit;
+    if (task != gwarp) shrink_load_a<SL>(p, btask, lane, st);  // the first was preloaded
     if (r0 == r1) continue;
     const int k0 = ks * SL;
 #pragma unroll 1
@@ -458,13 +474,19 @@ __device__ __forceinline__ void lora_shrink_tasks(const GemmParams& p, int gwarp
 // The shrink of one warp: A of its first task preloaded before the PDL wait, then the tasks.
 // One 4096-element slice per task: q, o, gate|up need no combine; down (K = 14336) combines 4.
 constexpr int SHRINK_SL = 4096;
-template <int SL>
+template <int SL, bool SPLIT_ROWS>
 __device__ __forceinline__ void shrink_warp(const GemmParams& p, int gwarp, int nwarps, int lane,
                                             const int* s_off, const int* s_rows, bool wait_first) {
   ShrinkTask<SL> st;
-  if (gwarp < shrink_tasks_total<SL>(p)) shrink_load_a<SL>(p, gwarp, lane, st);
+  if constexpr (SPLIT_ROWS) {
+    const int n_dec = s_off[p.slots];
+    const int rsplit = shrink_rsplit<SL>(p, nwarps, n_dec);
+    if (gwarp < shrink_tasks_total<SL>(p, nwarps, n_dec)) shrink_load_a<SL>(p, gwarp / rsplit, lane, st);
+  } else {
+    if (gwarp < p.sh_targets * p.slots * p.rank * ((p.sh_K + SL - 1) / SL)) shrink_load_a<SL>(p, gwarp, lane, st);
+  }
   if (wait_first) pdl_wait();
-  lora_shrink_tasks<SL>(p, gwarp, nwarps, lane, s_off, s_rows, st);
+  lora_shrink_tasks<SL, SPLIT_ROWS>(p, gwarp, nwarps, lane, s_off, s_rows, st);
 }
 
 template <int NT, int MODE>
@@ -794,7 +816,9 @@ __global__ void __launch_bounds__(256, 1)
       const int nseg = s_off[p.slots];
       for (int i = t64; i < nseg; i += 64) s_rows[i] = p.seg_rows[i];
       named_bar_sync(3, 64);
-      shrink_warp<SHRINK_SL>(p, blockIdx.x * 2 + (warp - 2), gridDim.x * 2, lane, s_off, s_rows, true);
+      // wide launches (many decoder rows per adapter slot) split each slot's rows over warps
+      shrink_warp<SHRINK_SL, (NT > 32)>(p, blockIdx.x * 2 + (warp - 2), gridDim.x * 2, lane, s_off, s_rows,
+                                        true);
       asm volatile("fence.proxy.async.global;\n" ::: "memory");  // U is read by TMA
       __syncwarp();
       if (lane == 0) red_add_release(p.sync, 1);
