@@ -480,6 +480,10 @@ __device__ __forceinline__ void shrink_warp(const GemmParams& p, int gwarp, int 
   ShrinkTask<SL> st;
   if constexpr (SPLIT_ROWS) {
     const int n_dec = s_off[p.slots];
+    if (n_dec == 0) {  // no decoder rows (prefill): nothing to shrink
+      if (wait_first) pdl_wait();
+      return;
+    }
     const int rsplit = shrink_rsplit<SL>(p, nwarps, n_dec);
     if (gwarp < shrink_tasks_total<SL>(p, nwarps, n_dec)) shrink_load_a<SL>(p, gwarp / rsplit, lane, st);
   } else {
@@ -543,6 +547,9 @@ __global__ void __launch_bounds__(256, 1)
   const int t_first = (int)((unsigned)u_begin / (unsigned)sp.Ut);
   const int t_last = (int)((unsigned)(u_end - 1) / (unsigned)sp.Ut);
   const int ntiles = t_last - t_first + 1;
+  // shrink warps per CTA: 2-3, and in wide launches also the epilogue warps 4-7, which
+  // otherwise only wait for the first accumulator during the main loop
+  constexpr int SHRINK_WARPS = NT > 32 ? 6 : 2;
 
   if (warp == 0 && elect_one()) {
     for (int i = 0; i < NS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
@@ -815,11 +822,15 @@ __global__ void __launch_bounds__(256, 1)
       named_bar_sync(3, 64);
       const int nseg = s_off[p.slots];
       for (int i = t64; i < nseg; i += 64) s_rows[i] = p.seg_rows[i];
+      if constexpr (SHRINK_WARPS > 2) named_bar_arrive(6, 64 + 128);  // the table is staged
       named_bar_sync(3, 64);
       // wide launches (many decoder rows per adapter slot) split each slot's rows over warps
-      shrink_warp<SHRINK_SL, (NT > 32)>(p, blockIdx.x * 2 + (warp - 2), gridDim.x * 2, lane, s_off, s_rows,
-                                        true);
+      shrink_warp<SHRINK_SL, (NT > 32)>(p, blockIdx.x * SHRINK_WARPS + (warp - 2), gridDim.x * SHRINK_WARPS,
+                                        lane, s_off, s_rows, true);
       asm volatile("fence.proxy.async.global;\n" ::: "memory");  // U is read by TMA
+      // the epilogue warps' shrink tasks of this CTA are done too: the CTA still counts 2
+      // arrivals per launch, whatever its width (row-group launches share the counter)
+      if constexpr (SHRINK_WARPS > 2) named_bar_sync(7, 64 + 128);
       __syncwarp();
       if (lane == 0) red_add_release(p.sync, 1);
       if (lane == 0 && warp == 2) stamp(1);
@@ -828,6 +839,19 @@ __global__ void __launch_bounds__(256, 1)
     // ---------------- epilogue (TMEM -> registers -> global) ----------------
     const int ep_t = threadIdx.x - 128;
     const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+    if constexpr (SHRINK_WARPS > 2) {
+      if (p.sh_x != nullptr) {
+        // wide launches: shrink tasks first (the first accumulator is far away)
+        const int* s_off = rm.kind + 5 * NT;
+        const int* s_rows = s_off + (p.slots + 1);
+        named_bar_sync(6, 64 + 128);  // warps 2-3 staged the SGMV table
+        shrink_warp<SHRINK_SL, true>(p, blockIdx.x * SHRINK_WARPS + 2 + (warp - 4), gridDim.x * SHRINK_WARPS,
+                                     lane_id(), s_off, s_rows, true);
+        asm volatile("fence.proxy.async.global;\n" ::: "memory");
+        __syncwarp();
+        named_bar_arrive(7, 64 + 128);  // counted by warps 2-3
+      }
+    }
     pdl_wait();
     // the launch that used reset_sync has completed (PDL): re-arm its shrink counter for
     // its next use (two launches later at the earliest)
