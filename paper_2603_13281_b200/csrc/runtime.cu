@@ -380,7 +380,12 @@ struct icr_model {
   // graphs
   bool use_graphs = true;
   cudaStream_t capture_stream = nullptr;
-  std::map<GraphKey, cudaGraphExec_t> graphs;
+  struct GraphEntry {
+    cudaGraphExec_t exec;
+    unsigned long long used;  // LRU tick
+  };
+  std::map<GraphKey, GraphEntry> graphs;
+  unsigned long long graph_tick = 0;
   // instrumentation of the last forward
   long long last_launches = 0;
   long long last_meta_bytes = 0;
@@ -453,7 +458,7 @@ static icr_status ensure_meta(icr_model* m, size_t ints) {
   for (int i = 0; i < 2; ++i) CUDA_TRY(cudaMallocHost(&m->staging[i], cap * sizeof(int)));
   m->meta_cap = cap;
   // graphs captured against the old buffer are stale
-  for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
+  for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second.exec);
   m->graphs.clear();
   return ICR_OK;
 }
@@ -800,9 +805,15 @@ static icr_status run_forward(icr_model* m, const Meta& mt, float* logits_dev, c
                      logits_dev};
   auto it = m->graphs.find(key);
   if (it == m->graphs.end()) {
-    if (m->graphs.size() >= 64) {
-      for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
-      m->graphs.clear();
+    // serving mixes batch shapes (rows, emitting rows, attention items): keep up to 256
+    // captured forwards, evicting the least recently used one at a time
+    constexpr size_t kMaxGraphs = 256;
+    if (m->graphs.size() >= kMaxGraphs) {
+      auto lru = m->graphs.begin();
+      for (auto g2 = m->graphs.begin(); g2 != m->graphs.end(); ++g2)
+        if (g2->second.used < lru->second.used) lru = g2;
+      cudaGraphExecDestroy(lru->second.exec);
+      m->graphs.erase(lru);
     }
     cudaGraph_t g;
     CUDA_TRY(cudaStreamBeginCapture(m->capture_stream, cudaStreamCaptureModeThreadLocal));
@@ -814,12 +825,13 @@ static icr_status run_forward(icr_model* m, const Meta& mt, float* logits_dev, c
     ce = cudaGraphInstantiate(&ex, g, 0);
     cudaGraphDestroy(g);
     if (ce != cudaSuccess) return fail(ICR_CUDA, "graph instantiate: %s", cudaGetErrorString(ce));
-    it = m->graphs.emplace(key, ex).first;
+    it = m->graphs.emplace(key, icr_model::GraphEntry{ex, 0}).first;
   } else {
     m->last_mt = mt;
     m->last_items = mt.n_items;
   }
-  CUDA_TRY(cudaGraphLaunch(it->second, s));
+  it->second.used = ++m->graph_tick;
+  CUDA_TRY(cudaGraphLaunch(it->second.exec, s));
   return ICR_OK;
 }
 
@@ -986,7 +998,7 @@ icr_status icr_model_create(const icr_model_config* cfg, const icr_layer_weights
 icr_status icr_model_destroy(icr_model* m) {
   if (!m) return ICR_OK;
   cudaDeviceSynchronize();
-  for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
+  for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second.exec);
   void* bufs[] = {m->x, m->xb, m->ssq, m->ssq_lm, m->qb, m->att, m->f, m->hlm, m->ubd,
                   m->tile_best, m->out_tok, m->hid, m->hid_ssq, m->slot_idx, m->part_o, m->part_ml, m->merge_cnt, m->rope, m->ws,
                   m->counters, m->sync, m->sh_part, m->sh_cnt, m->meta_dev};

@@ -346,7 +346,9 @@ def _pre_step(session: GenerationSession, token: int) -> int:
         raise StateError("session is closed")
     if not session._prefilled:
         raise StateError("decode before prefill")
-    _check_tokens(session, [token])
+    t = int(token)
+    if not 0 <= t < session.config.vocab_size:
+        raise IndexError(f"token {t} outside vocab [0, {session.config.vocab_size})")
     pos = session.cache.position_count
     if pos + 1 > session.max_context:
         raise CapacityError(f"context full at {pos}/{session.max_context}")
