@@ -135,6 +135,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   float* mrow = reinterpret_cast<float*>(smem + L::MROW_OFF);
 
   const int cta = blockIdx.x;
+  unsigned long long merge_target = 0;  // thread 0: the in-kernel merge's counter target
   auto stamp = [&](int k) {
     if (trace != nullptr && cta < 4096) trace[(size_t)cta * 16 + k] = globaltimer();
   };
@@ -267,6 +268,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       pid_cur = pid_n0;
     }
     if (!waited) pdl_wait();
+    if constexpr (kNarrow) {
+      // the merge's completion target, read while the units still stream (off the tail): this
+      // launch's adds total < 2^20, so the value's generation is the previous launch's
+      if (threadIdx.x == 0)
+        merge_target = ((ld_acquire_u64(reinterpret_cast<const unsigned long long*>(merge_sync)) >> 20) + 1) << 20;
+    }
     __syncwarp();
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
@@ -695,8 +702,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (threadIdx.x == 0) {
       stamp(8);
       const unsigned long long mine = cta == 0 ? (1ull << 20) - (gridDim.x - 1) : 1ull;
-      const unsigned long long old = atom_add_release_u64(done, mine);
-      *s_target = ((old >> 20) + 1) << 20;
+      red_add_release_u64(done, mine);
+      *s_target = merge_target;
     }
     __syncthreads();
     const unsigned long long target = *s_target;
