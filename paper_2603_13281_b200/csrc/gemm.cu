@@ -583,6 +583,9 @@ __global__ void __launch_bounds__(256, 1)
   // order -- fixed by (M, K, grid) only -- polling each 4-byte word until it is not
   // WS_EMPTY (no atomics, no fences: one L2 round trip when the partials are there), and
   // re-arms the slots it consumed. Wide launches software-pipeline the residual rows.
+  // Waiting on other CTAs is safe because a launch's CTAs are all resident together (grid =
+  // min(units, #SMs), one CTA per SM; a PDL successor is only scheduled once every CTA of this
+  // grid has started) -- the same assumption as the grid-wide LoRA-shrink count.
   auto fin_chunks = [&](int t, int b, int cc0, int cc1, int ep_t, EpiShared& shx, int bar,
                         const float* pre0, const float2* cs0) {
     const int grow0 = p.row0, gnr = p.n_rows;
