@@ -143,6 +143,12 @@ icr_status icr_decode_loop(icr_model* m, const icr_batch* first, const int32_t* 
  * icr_forward / icr_decode_loop step. */
 icr_status icr_model_stats(icr_model* m, int64_t* out3);
 
+/* Invariant check of the GEMM's split-tile exchange: *out = the number of stream-K scratch
+ * words of the model that do not hold the "unpublished" pattern (0 after every completed
+ * forward: each published partial is consumed and re-armed by its tile's finalizer).
+ * Synchronises the stream. */
+icr_status icr_debug_ws_check(icr_model* m, int64_t* out, void* stream);
+
 /* Per-kernel-kind device time of the last forward, replayed without the graph with an
  * event after every launch: kind_ms[0..8] = embed, qkv, attention, o, gate|up, down,
  * LM gather, LM head, argmax; kind_ms[9] = total (ms). Recomputes identical K/V. */

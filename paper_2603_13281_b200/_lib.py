@@ -26,7 +26,7 @@ _STATUS = {
 # Every symbol the header declares; tests/test_capi.py checks the library exports them.
 EXPORTED = (
     "icr_model_create", "icr_model_destroy", "icr_forward", "icr_decode_loop",
-    "icr_model_stats", "icr_profile_step", "icr_profile_gemm", "icr_profile_ablate", "icr_profile_trace", "icr_host_timing", "icr_bench_gemm",
+    "icr_model_stats", "icr_debug_ws_check", "icr_profile_step", "icr_profile_gemm", "icr_profile_ablate", "icr_profile_trace", "icr_host_timing", "icr_bench_gemm",
     "icr_bench_attention", "icr_gemm_bf16", "icr_paged_attention", "icr_layer_forward",
     "icr_seq_logits", "icr_linear_bf16",
     "icr_last_error", "icr_abi_version", "icr_num_sms",
@@ -80,6 +80,7 @@ def load():
         "icr_decode_loop": [p, C.POINTER(BatchC), C.POINTER(C.c_int32), i,
                             C.POINTER(C.c_int32), C.POINTER(C.c_float), p],
         "icr_model_stats": [p, C.POINTER(C.c_int64)],
+        "icr_debug_ws_check": [p, C.POINTER(C.c_int64), p],
         "icr_profile_gemm": [p, i, i, C.POINTER(C.c_float), p],
         "icr_profile_ablate": [p, i, i, C.POINTER(C.c_float), p],
         "icr_profile_trace": [p, C.c_char_p, p],

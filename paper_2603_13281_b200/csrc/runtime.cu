@@ -1213,6 +1213,18 @@ icr_status icr_profile_trace(icr_model* m, const char* path, void* stream) {
   return ICR_OK;
 }
 
+icr_status icr_debug_ws_check(icr_model* m, int64_t* out, void* stream) {
+  if (!m || !out) return fail(ICR_CONFIG, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<uint32_t> h(gemm_ws_floats(m->num_sms));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  CUDA_TRY(cudaMemcpy(h.data(), m->ws, h.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  int64_t n = 0;
+  for (uint32_t w : h) n += w != 0xFFFFFFFFu;
+  *out = n;
+  return ICR_OK;
+}
+
 // Instrumentation: [launches, metadata bytes, attention items] of the last forward.
 icr_status icr_model_stats(icr_model* m, int64_t* out3) {
   if (!m || !out3) return fail(ICR_CONFIG, "null argument");

@@ -532,6 +532,14 @@ def test_over_256_row_adapted_batch_equals_single_session_steps(c1_setup):
             assert s.last_logits.tobytes() == want[i][1][step], f"session {i} step {step}"
     for s in batch:
         s.close()
+    # every published split-tile partial of all those launches (16- to 256-row, every epilogue
+    # mode, logits capture) was consumed and re-armed by its finalizer
+    import ctypes as C
+
+    from paper_2603_13281_b200 import _lib
+    left = C.c_int64(-1)
+    _lib.check(rt._lib.icr_debug_ws_check(rt._handle, C.byref(left), _lib.stream_handle()))
+    assert left.value == 0, f"{left.value} stream-K scratch words left published"
 
 
 def test_rank24_adapters_in_straddling_slots_match_oracle(cuda):
