@@ -481,7 +481,7 @@ def run_b200(args) -> None:
 
     # ---------------- C2: the headline ----------------
     E2E = min(K, 64)
-    max_ctx = (PROMPT + W + K + E2E + 32 + 15) // 16 * 16
+    max_ctx = (PROMPT + W + K + W + E2E + 32 + 15) // 16 * 16
     tail_pages = (max_ctx - PROMPT) // 16 + 2
     rt = base.runtime(max_seqs=N_ADAPTERS + 2, max_context=max_ctx, max_rows=512,
                       adapter_slots=N_ADAPTERS, lora_rank=RANK,
@@ -513,6 +513,11 @@ def run_b200(args) -> None:
 
     # ---------------- end to end through the public API (e2e) ----------------
     toks = [int(t) for t in toks]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    for _ in range(W):  # untimed: the public-API path's first calls (graph capture for the
+        toks = E.decode_step_batch(sessions, toks)  # step shapes the device loop did not use)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
